@@ -1,0 +1,187 @@
+/* rc.h -- C ABI of the B200-native cell-local reactive update (arXiv 2312.13513).
+ *
+ * The paper's GPU solver computes, per finite-volume cell, thermophysical and
+ * transport properties "with Newton's method and high-order temperature
+ * polynomials" (§3.1, class Thermo) and the chemical source term
+ * by "individual neural networks ... for each component, excluding inert
+ * gases", hidden layers 1600/800/400, GELU, inputs "temperature, pressure and
+ * mass fractions", output "the rate of change for a given species"
+ * (§2, class DNNInference).  This library is that update behind
+ * a plain C interface: mechanism tables plus component-major (SoA) cell arrays
+ * in, properties and source terms out ("coalesced the same
+ * components of fields").  The paper leaves Box-Cox, the mixing rules, the
+ * element projection and dt unstated; DESIGN.md lists the readings (R1-R16).
+ *
+ * Conventions for every call:
+ *  - Return value: RC_OK (0) or a negative RC_E* code.  rc_last_error() returns
+ *    a thread-local message for the last failure on the calling thread.
+ *  - Argument checks happen before any launch; a failing call launches nothing.
+ *  - Work is enqueued on the caller's stream; no call synchronises the device,
+ *    allocates device memory (except *_create), or copies to the host.
+ *  - Handles (rc_mech, rc_mlp) are immutable after create, device-resident on
+ *    the device current at create time, and safe to share across streams and
+ *    host threads.  Cell arrays and workspace are BORROWED: they must stay
+ *    valid until the enqueued work completes.
+ *  - Per-cell numerical anomalies never fail a call; they are counted in
+ *    rc_cells.diag (SPEC.md:420 precedent: count, don't abort).
+ *  - No cross-GPU reduction happens inside the library: multi-GPU callers
+ *    all-reduce rc_cells.red / diag themselves (NCCL via torch.distributed).
+ *  - Units: SI with kmol (J/kg, J/kg/K, kg/m^3, Pa, K, Pa s, W/m/K, m^2/s,
+ *    kg/m^3/s, W/m^3).  h is absolute (formation-inclusive) enthalpy.
+ */
+#ifndef RC_H
+#define RC_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* only the rc_* entry points are exported */
+#endif
+
+enum {
+  RC_OK = 0,
+  RC_EINVAL = -1,        /* bad argument: NULL, size, stride, alignment, range */
+  RC_ENOMEM = -2,        /* device allocation failed (create calls only) */
+  RC_ECUDA = -3,         /* a CUDA runtime/driver call or launch failed */
+  RC_EALIGN = -4,        /* pointer not 16-byte aligned or ld not a multiple of 2 */
+  RC_EUNSUPPORTED = -5,  /* shape the kernels do not implement (see each call) */
+  RC_EDTMISMATCH = -6    /* rc_cells.dt != the bundle's training dt */
+};
+
+enum { RC_MODE_H = 0, RC_MODE_T = 1 };               /* rc_cells.mode */
+enum { RC_BF16 = 0, RC_TF32 = 1 };                    /* rc_mlp_desc.precision */
+
+/* Diagnostic counters in rc_cells.diag[] (int64, accumulated with atomics). */
+enum {
+  RC_DIAG_NEWTON_BISECT = 0,  /* cells whose Newton fell back to bisection */
+  RC_DIAG_NEWTON_MAXIT = 1,   /* ... of which because 50 iterations were reached */
+  RC_DIAG_NONFINITE = 2,      /* (cell, stage) pairs with a non-finite output */
+  RC_DIAG_NEGY_IN = 3,        /* cells with some input Y_k < 0 (counted by thermo) */
+  RC_DIAG_NEGY_OUT = 4,       /* cells with some max(Y_k,0) + dY_k < 0 after projection */
+  RC_DIAG_COUNT = 5
+};
+
+typedef struct rc_mech rc_mech; /* opaque: device-resident species tables */
+typedef struct rc_mlp rc_mlp;   /* opaque: device-resident MLP bundle */
+
+/* ---------------------------------------------------------------------------
+ * Mechanism tables (HOST pointers; copied at create; caller may free after).
+ * Limits: 1 <= ns <= 32 (kernels specialise ns = 9 and ns = 20; others run a
+ * generic path), 1 <= ne <= 8.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t ns, ne;                 /* species, elements */
+  const double *W_elem;           /* [ne] atomic weights, kg/kmol; W_k = sum_e atoms[e][k] W_elem[e] */
+  const int32_t *atoms;           /* [ne][ns] atom counts a_ek */
+  const double *nasa_lo;          /* [ns][7] NASA-7 a1..a7, T_lo <= T <= T_mid */
+  const double *nasa_hi;          /* [ns][7] NASA-7 a1..a7, T_mid <  T <= T_hi */
+  const double *T_lo, *T_mid, *T_hi; /* [ns] K */
+  const double *visc;             /* [ns][5]  sqrt(mu_k)/T^(1/4) = sum_n c_n (ln T)^n */
+  const double *cond;             /* [ns][5]  lambda_k/sqrt(T)   = sum_n c_n (ln T)^n */
+  const double *diff;             /* [ns(ns+1)/2][5] D_jk p/T^(3/2) = sum_n c_n (ln T)^n, packed j<=k at k(k+1)/2+j */
+  const uint8_t *inert;           /* [ns] 1 = no net predicts this species ("excluding inert gases") */
+} rc_mech_desc;
+
+/* Builds, on the current device: molar masses, per-range mixture-NASA
+ * coefficient rows, Wilke constants (W_j/W_k)^(1/4) and 1/sqrt(8(1+W_k/W_j)),
+ * and the element projection P = I - E^T (E E^T)^-1 E with E_ek = a_ek A_e/W_k
+ * (reading R6).  Errors: RC_EINVAL (NULL/range, singular E E^T),
+ * RC_ENOMEM, RC_ECUDA. */
+int rc_mech_create(const rc_mech_desc *desc, rc_mech **out);
+void rc_mech_destroy(rc_mech *m);
+int rc_mech_ns(const rc_mech *m);
+
+/* ---------------------------------------------------------------------------
+ * MLP bundle (HOST pointers, fp64; converted at create).  One net per
+ * non-inert species, d_in = ns + 2 inputs [T, p, BCT(Y_1..ns)], hidden widths
+ * hidden[0..2], 1 output.  Row-major [out][in] weights.
+ * Kernels require hidden[0] % 32 == 0 and hidden[1] % 16 == 0 and
+ * hidden[2] % 16 == 0, and d_in <= 64 (else RC_EUNSUPPORTED).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_nets;                 /* = number of non-inert species */
+  int32_t hidden[3];              /* (1600, 800, 400) in the paper */
+  const int32_t *species_of_net;  /* [n_nets] species index predicted by net i */
+  const double *params;           /* [n_nets][P] per net: W1[h1][d_in] b1[h1] W2[h2][h1] b2[h2]
+                                     W3[h3][h2] b3[h3] W4[1][h3] b4[1] */
+  const double *x_mean, *x_std;   /* [d_in] input z-score (R4) */
+  const double *y_mean, *y_std;   /* [n_nets] output de-normalisation (R2) */
+  double lambda_bc;               /* Box-Cox lambda (R3; 0.1) -- must satisfy 1/lambda integer <= 16 */
+  double dt;                      /* training dt of the bundle, s (R7) */
+  int32_t precision;              /* RC_BF16 (bf16 x bf16 -> fp32) | RC_TF32 */
+} rc_mlp_desc;
+
+int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *desc, rc_mlp **out);
+void rc_mlp_destroy(rc_mlp *n);
+
+/* ---------------------------------------------------------------------------
+ * Cell state: caller-owned DEVICE arrays, component-major (field[k*ld + c]).
+ * Every pointer 16-byte aligned; ld >= n and ld even.  Output pointers may be
+ * NULL to skip that output (the stage still runs if any of its outputs is
+ * requested).  Inputs are never written except T (h-mode: in = guess, out =
+ * converged) and h (T-mode: out).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int64_t n, ld;
+  int32_t mode;                   /* RC_MODE_H: Newton from h (T in = guess); RC_MODE_T: h = h(T) */
+  double *h;                      /* [ld]  J/kg */
+  double *T;                      /* [ld]  K */
+  const double *p;                /* [ld]  Pa */
+  const double *Y;                /* [ns][ld] mass fractions (may hold tiny negatives) */
+  double *cp, *rho;               /* [ld] (a1) */
+  double *mu, *lambda;            /* [ld] Wilke viscosity, Mathur conductivity (a2) */
+  double *D;                      /* [ns][ld] mixture-averaged diffusivities (a2) */
+  double *wdot;                   /* [ns][ld] species source terms rho dY_k / dt (a5) */
+  double *qdot;                   /* [ld] heat release -sum_k h_k(T) wdot_k (a5) */
+  float *o;                       /* [n_nets][ld] raw net outputs (optional, parity/debug) */
+  double dt;                      /* must equal the bundle's dt when chemistry runs */
+  double *red;                    /* [2] device: red[0] = max over cells of T (atomic max,
+                                     caller/rc_step zeroes), red[1] = sum qdot (written by chem) */
+  int64_t *diag;                  /* [RC_DIAG_COUNT] device counters (atomic adds), may be NULL */
+} rc_cells;
+
+/* Workspace bytes rc_chem / rc_step need for n cells (activations of one cell
+ * chunk, partial sums).  Alignment 256 B. */
+size_t rc_workspace_bytes(const rc_mech *m, const rc_mlp *n, int64_t ncells);
+
+/* a1: Newton h -> T (h-mode) or h(T) (T-mode); cp, rho.
+ * Newton: T <- clamp(T + (h* - h(T))/cp(T), min T_lo, max T_hi), stop after an
+ * unclamped update with |dT| <= 1e-10 T; 50 iterations or two consecutive
+ * clamps -> bisection to width 1e-10 T (R8). */
+int rc_thermo(const rc_mech *m, const rc_cells *c, void *stream);
+
+/* a2: Wilke viscosity, Mathur conductivity, mixture-averaged D_k with
+ * X+ = max(X, 0) and the D_kk pure-species fallback (R10, R11).  Reads T as
+ * stored (run after rc_thermo). */
+int rc_transport(const rc_mech *m, const rc_cells *c, void *stream);
+
+/* a3-a5: Box-Cox prologue, per-species MLP on the tensor cores, inverse
+ * Box-Cox, element projection, wdot, qdot; red[1] = sum qdot.  Reads T and rho
+ * as stored (run after rc_thermo).  Errors: RC_EDTMISMATCH, RC_EINVAL
+ * (workspace too small / NULL wdot), RC_ECUDA. */
+int rc_chem(const rc_mech *m, const rc_mlp *n, const rc_cells *c, void *ws, size_t ws_bytes, void *stream);
+
+/* a1 + a2 + a3-a5 in order on one stream; zeroes red and diag first. */
+int rc_step(const rc_mech *m, const rc_mlp *n, const rc_cells *c, void *ws, size_t ws_bytes, void *stream);
+
+/* Multi-GPU block partition: rank r of world G gets
+ * [begin, end) with boundaries floor(r N / G) rounded down to 128 cells (the
+ * MLP tile) except end = N for the last rank.  Pure host function. */
+int rc_partition(int64_t n_global, int rank, int world, int64_t *begin, int64_t *end);
+
+/* Number of kernel launches the last rc_* call on this thread enqueued. */
+int64_t rc_last_launch_count(void);
+
+const char *rc_last_error(void);
+const char *rc_version(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* RC_H */

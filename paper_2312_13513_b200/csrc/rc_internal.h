@@ -1,0 +1,113 @@
+// rc_internal.h -- private definitions of the B200 (sm_100a) reactive-cell library.
+// Nothing here is shared with oracle/ (the CPU oracle is independent test code).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/rc.h"
+
+#define RC_MAX_NS 32
+#define RC_MAX_NE 8
+#define RC_RU 8314.46261815324  // J/kmol/K (R12)
+
+// ---------------------------------------------------------------------------
+// Device-resident species tables.  One contiguous fp64 buffer; each kernel
+// stages the segment it needs into shared memory with one bulk TMA copy
+// (cp.async.bulk), "constant memory for storing constant
+// coefficients" re-done the Blackwell way.
+// ---------------------------------------------------------------------------
+struct ThermoSeg {        // doubles, offsets relative to the segment start
+  // [0] Tmin  [1] Tmax  [2] Tmid (if uniform) [3] uniform flag (1.0 / 0.0)
+  // [4 .. 4+6ns)      hlo[k][j]: j<5: (R/W_k) a_{j+1}^lo/(j+1); j=5: (R/W_k) a6^lo
+  // [.. + 6ns)        hhi[k][j]
+  // [.. + ns)         invW[k]
+  // [.. + ns)         Tmid[k]
+  __host__ __device__ static int hlo(int) { return 4; }
+  __host__ __device__ static int hhi(int ns) { return 4 + 6 * ns; }
+  __host__ __device__ static int invW(int ns) { return 4 + 12 * ns; }
+  __host__ __device__ static int tmid(int ns) { return 4 + 13 * ns; }
+  __host__ __device__ static int size(int ns) { return (4 + 14 * ns + 1) & ~1; }  // even -> 16-byte multiple
+};
+
+struct TransportSeg {
+  // visc[ns][5] cond[ns][5] diff[np][5] W[ns] invW[ns] c1[ns][ns] c2[ns][ns]
+  __host__ __device__ static int visc(int) { return 0; }
+  __host__ __device__ static int cond(int ns) { return 5 * ns; }
+  __host__ __device__ static int diff(int ns) { return 10 * ns; }
+  __host__ __device__ static int W(int ns) { return 10 * ns + 5 * (ns * (ns + 1) / 2); }
+  __host__ __device__ static int invW(int ns) { return W(ns) + ns; }
+  __host__ __device__ static int c1(int ns) { return W(ns) + 2 * ns; }
+  __host__ __device__ static int c2(int ns) { return c1(ns) + ns * ns; }
+  __host__ __device__ static int size(int ns) { return (c2(ns) + ns * ns + 1) & ~1; }
+};
+
+struct rc_mech {
+  int ns, ne, device;
+  bool uniform_tmid;
+  double Tmin, Tmax;
+  std::vector<double> W, P, thermo_host, transport_host;
+  std::vector<uint8_t> inert;
+  double *d_thermo = nullptr;     // ThermoSeg
+  double *d_transport = nullptr;  // TransportSeg
+  double *d_P = nullptr;          // [ns][ns] element projection (R6)
+};
+
+struct rc_mlp {
+  int n_nets, d_in, h1, h2, h3, precision, ns, device;
+  int kpad1;                      // padded K of layer 1 (64 bf16 / 32 fp32)
+  double lambda_bc, dt;
+  int inv_lambda;                 // 1/lambda as an integer power
+  std::vector<int> species_of_net;
+  // device buffers
+  void *d_W1 = nullptr, *d_W2 = nullptr, *d_W3 = nullptr;   // [nets][N][K] bf16 or fp32(tf32-rounded)
+  float *d_b1 = nullptr, *d_b2 = nullptr, *d_b3 = nullptr;  // [nets][N]
+  float *d_w4 = nullptr;                                    // [nets][h3]
+  float *d_b4 = nullptr;                                    // [nets]
+  float *d_xmean = nullptr, *d_xinvstd = nullptr;           // [d_in]
+  double *d_ymean = nullptr, *d_ystd = nullptr;             // [nets]
+  int *d_species = nullptr;                                 // [nets]
+};
+
+// ---------------------------------------------------------------------------
+// errors / bookkeeping
+// ---------------------------------------------------------------------------
+int rc_fail(int code, const char *fmt, ...);
+void rc_count_launch(int n = 1);
+void rc_reset_launches();
+#define RC_CUDA_TRY(x)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess) return rc_fail(RC_ECUDA, "%s: %s", #x, cudaGetErrorString(e_)); \
+  } while (0)
+#define RC_LAUNCH_CHECK()                                                                           \
+  do {                                                                                              \
+    cudaError_t e_ = cudaGetLastError();                                                            \
+    if (e_ != cudaSuccess) return rc_fail(RC_ECUDA, "launch failed: %s", cudaGetErrorString(e_));   \
+    rc_count_launch();                                                                              \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Kernel launchers (defined in the .cu files)
+// ---------------------------------------------------------------------------
+struct CellsDev {
+  int64_t n, ld;
+  int mode;
+  double *h, *T;
+  const double *p, *Y;
+  double *cp, *rho, *mu, *lambda, *D, *wdot, *qdot;
+  float *o;
+  double *red;
+  int64_t *diag;
+};
+
+int launch_thermo(const rc_mech *m, const CellsDev &c, cudaStream_t s);
+int launch_transport(const rc_mech *m, const CellsDev &c, cudaStream_t s);
+
+struct ChemWs;  // defined in mlp_sm100.cu
+size_t chem_workspace_bytes(const rc_mech *m, const rc_mlp *n, int64_t ncells);
+int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, size_t ws_bytes, cudaStream_t s);
+int mlp_upload(rc_mlp *n, const rc_mlp_desc *d);

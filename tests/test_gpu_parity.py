@@ -1,0 +1,184 @@
+"""CUDA path vs oracle, element by element on the same seeded inputs, through
+the C ABI (include/rc.h).  Gates (BASELINE.json north_star):
+  fp64 thermo/transport (T, cp, rho, mu, lambda, D_k)  |g - o| <= 1e-10 |o|
+  bf16 MLP output o ("relative 2e-2 of the output norm")   ||g - o|| / ||o|| <= 2e-2
+  bf16 wdot, qdot, sum qdot (derived, R17)        ||g - o|| / ||o|| <= 5e-2
+  T_max                                                 1e-10
+  GPU wdot conserves mass and elements                  1e-12 of sum |wdot|
+  sharded == unsharded                                  bitwise
+"""
+import numpy as np
+import pytest
+
+from _harness import Gpu, inputs, max_rel, mech, rel_fro, run_oracle
+from workload import CONFIGS
+from workload.cells import uniform
+
+pytestmark = pytest.mark.gpu
+
+FP64_TOL = 1e-10
+BF16_TOL = 2e-2        # on the MLP output o (north_star)
+BF16_DERIVED_TOL = 5e-2  # on wdot / qdot: bf16 weight rounding of the nets with the smallest |o|
+                         # (e.g. O2, |o| ~ 0.01 with random init) dominates wdot (R17)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2312_13513_b200 import build
+    build.build()
+
+
+def _E(m):
+    W = (m["atoms"] * m["W_elem"][:, None]).sum(0)
+    return m["atoms"] * m["W_elem"][:, None] / W[None, :]
+
+
+def check_fp64(g, o, cols=None):
+    for k in ("T", "cp", "rho", "mu", "lambda"):
+        gv = g[k] if cols is None else g[k][cols]
+        assert max_rel(gv, o[k]) <= FP64_TOL, (k, max_rel(gv, o[k]))
+    gD = g["D"] if cols is None else g["D"][:, cols]
+    assert max_rel(gD, o["D"]) <= FP64_TOL, ("D", max_rel(gD, o["D"]))
+
+
+def check_chem(g, o, m, cols=None, tol=BF16_TOL, dtol=BF16_DERIVED_TOL):
+    go = g["o"] if cols is None else g["o"][:, cols]
+    gw = g["wdot"] if cols is None else g["wdot"][:, cols]
+    gq = g["qdot"] if cols is None else g["qdot"][cols]
+    eo, ew, eq = rel_fro(go, o["o"]), rel_fro(gw, o["wdot"]), rel_fro(gq, o["qdot"])
+    assert eo <= tol, ("o", eo)
+    assert ew <= dtol, ("wdot", ew)
+    assert eq <= dtol, ("qdot", eq)
+    # conservation of the GPU's own wdot (its projection runs in fp64)
+    tot = np.abs(gw).sum(axis=0) + 1e-300
+    assert np.all(np.abs(gw.sum(axis=0)) <= 1e-12 * tot)
+    assert np.all(np.abs(_E(m) @ gw) <= 1e-12 * tot[None, :])
+    return eo, ew, eq
+
+
+def test_c1_full_parity():
+    """C1: 1,000 premixed cells (ragged: 7 full 128-row tiles + 104), small MLP."""
+    c = inputs("C1")
+    o = run_oracle("C1", c)
+    g = Gpu("C1").run(c)
+    check_fp64(g, o)
+    eo, ew, eq = check_chem(g, o, mech("h2_9sp"))
+    assert g["red"][0] == pytest.approx(o["red"][0], rel=FP64_TOL)
+    assert g["red"][1] == pytest.approx(o["red"][1], rel=BF16_DERIVED_TOL)
+    assert np.array_equal(g["diag"][[0, 1, 3]], o["diag"][[0, 1, 3]])
+    assert g["diag"][2] == 0
+    print(f"C1 bf16 errors: o {eo:.2e} wdot {ew:.2e} qdot {eq:.2e}")
+
+
+def test_c1_transport_and_thermo_only_paths():
+    c = inputs("C1", begin=100, end=357)
+    o = run_oracle("C1", c, chem=False)
+    g = Gpu("C1").run(c, chem=False)
+    check_fp64(g, o)
+    assert "wdot" not in g or g.get("wdot") is None
+
+
+def _sample(cfg, n):
+    N = CONFIGS[cfg].n_cells
+    return np.unique((uniform(4242, np.arange(n)) * N).astype(np.int64))
+
+
+@pytest.mark.parametrize("cfg", ["C2"])
+def test_full_size_sampled(cfg):
+    """BASELINE configs[1] at full size (1,048,576 cells, paper MLP 1600/800/400),
+    the bench's launch configuration; the oracle checks a hashed sample."""
+    n = CONFIGS[cfg].n_cells
+    c = inputs(cfg, begin=0, end=n)
+    g = Gpu(cfg).run(c)
+    cols = _sample(cfg, 192)
+    sub = {k: (v[..., cols] if isinstance(v, np.ndarray) else v) for k, v in c.items()}
+    o = run_oracle(cfg, sub)
+    check_fp64(g, o, cols)
+    eo, ew, eq = check_chem(g, o, mech(CONFIGS[cfg].mech), cols)
+    print(f"{cfg} sampled bf16 errors: o {eo:.2e} wdot {ew:.2e} qdot {eq:.2e}")
+    # whole-field properties that hold at any size
+    assert np.all(np.isfinite(g["wdot"])) and g["diag"][2] == 0
+    assert g["red"][0] == pytest.approx(g["T"].max(), rel=0, abs=0)
+    tot = np.abs(g["wdot"]).sum(axis=0) + 1e-300
+    assert np.all(np.abs(g["wdot"].sum(axis=0)) <= 1e-12 * tot)
+
+
+def test_ch4_paper_shape_sample():
+    """C4 (CH4/air, 20 species, 19 nets, d_in 22): parity on a hashed sample."""
+    cols = _sample("C4", 256)
+    c = inputs("C4", idx=cols)
+    o = run_oracle("C4", c)
+    g = Gpu("C4").run(c)
+    check_fp64(g, o)
+    check_chem(g, o, mech("ch4_20sp"))
+
+
+def test_padding_untouched_and_single_cell():
+    c = inputs("C1", begin=0, end=1)
+    o = run_oracle("C1", c)
+    g = Gpu("C1").run(c, ld=64)
+    check_fp64(g, o)
+    check_chem(g, o, mech("h2_9sp"))
+
+
+def test_empty_is_noop():
+    import torch
+    import paper_2312_13513_b200 as rc
+    G = Gpu("C1")
+    st = rc.CellState(0, G.ns, G.n_nets, ld=2)
+    ws = rc.aligned_workspace(G.mlp, 128)
+    rc.rc_step(G.mech, G.mlp, st.cells(rc.RC_MODE_H, dt=G.dt), ws)
+    torch.cuda.synchronize()
+    assert st.diag.sum().item() == 0
+
+
+def test_errors():
+    import paper_2312_13513_b200 as rc
+    G = Gpu("C1")
+    st = rc.CellState(10, G.ns, G.n_nets)
+    ws = rc.aligned_workspace(G.mlp, 10)
+    with pytest.raises(rc.RcError) as e:
+        rc.rc_step(G.mech, G.mlp, st.cells(rc.RC_MODE_H, dt=2e-6), ws)
+    assert e.value.code == rc._rc.RC_EDTMISMATCH
+    bad = st.cells(rc.RC_MODE_H, dt=G.dt)
+    bad.ld = 5
+    with pytest.raises(rc.RcError) as e:
+        rc.rc_step(G.mech, G.mlp, bad, ws)
+    assert e.value.code == rc._rc.RC_EINVAL
+    bad = st.cells(rc.RC_MODE_H, dt=G.dt)
+    bad.p = bad.p + 8
+    with pytest.raises(rc.RcError) as e:
+        rc.rc_step(G.mech, G.mlp, bad, ws)
+    assert e.value.code == rc._rc.RC_EALIGN
+
+
+def test_out_of_range_h_bisects_like_oracle():
+    c = inputs("C1", begin=500, end=520)
+    c["h"][3] = c["h"][3] + 5e7          # far above h(T_max): Newton clamps twice -> bisection
+    c["h"][7] = -5e7 + c["h"][7]         # far below h(T_min)
+    o = run_oracle("C1", c, chem=False)
+    g = Gpu("C1").run(c, chem=False)
+    assert o["diag"][0] == 2
+    assert np.array_equal(g["diag"][:2], o["diag"][:2])
+    assert max_rel(g["T"], o["T"]) <= FP64_TOL
+
+
+def test_sharded_equals_unsharded_bitwise():
+    """Cells are independent: running G shards (rc_partition) one after another
+    reproduces the unsharded per-cell outputs bit for bit."""
+    import paper_2312_13513_b200 as rc
+    c = inputs("C2", begin=300000, end=300000 + 5000)
+    G = Gpu("C2")
+    whole = G.run(c)
+    for world in (2, 3):
+        for r in range(world):
+            b, e = rc.rc_partition(5000, r, world)
+            part = {k: (v[..., b:e] if isinstance(v, np.ndarray) else v) for k, v in c.items()}
+            g = G.run(part)
+            for k in ("T", "cp", "rho", "mu", "lambda", "qdot"):
+                assert np.array_equal(g[k], whole[k][b:e]), (k, world, r)
+            for k in ("D", "wdot", "o"):
+                assert np.array_equal(g[k], whole[k][:, b:e]), (k, world, r)
