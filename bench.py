@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the full per-cell thermo + transport + DNN-chemistry
+step (BASELINE.json metric: Mcells/s, % roofline) on 1..8 B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--precision bf16]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+  python bench.py --impl reference ...                   (the CPU oracle, timed as it stands)
+
+One step = rc_step over every local cell (a1 thermo Newton, a2 transport, a3-a5
+MLP chemistry) + the a6 global reductions (NCCL all-reduce of max T and
+sum qdot / counters when N > 1).  Inputs are synthetic states from workload/
+(shapes of the paper's workloads, DESIGN.md input recipe) with random-init
+weights of the paper's MLP shape.  Default workload: C2 =
+BASELINE configs[1], 1,048,576 H2/air cells, MLP 11->1600->800->400->1 x 8 nets.
+Multi-GPU is weak scaling: every rank owns C2-sized blocks of a periodic tiling
+of the C2 grid (no halo, no data-path collective).
+Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SUSTAINED = "bf16_tflops_sustained"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "tf32"])
+    ap.add_argument("--strong", action="store_true", help="partition the config's cells (strong scaling)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle baseline")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, SUSTAINED: 1400.0}, "fallback"
+
+
+# FP64 FMA rate measured on this pool's B200 by tools/microbench/peaks.cu (profiles/peaks_r01.json)
+def fp64_peak():
+    try:
+        with open(os.path.join(ROOT, "profiles", "peaks_r01.json")) as f:
+            return json.load(f)["fp64_fma_tflops"], "measured (tools/microbench/peaks.cu)"
+    except (OSError, KeyError):
+        return 37.0, "fallback (148 SM x 64 DFMA/clk x 1.965 GHz)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.p is None:
+            return
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                self.rows.append(f)
+
+    def summary(self):
+        rows = getattr(self, "rows", [])
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def local_cells(cfg, rank, world, strong):
+    """Global cell indices owned by this rank.  Weak: a C-sized block per rank of a
+    periodic tiling of the config grid; strong: rc_partition of the config."""
+    import paper_2312_13513_b200 as rc
+    n = cfg.n_cells
+    if strong:
+        b, e = rc.rc_partition(n, rank, world)
+        return np.arange(b, e, dtype=np.int64), n
+    return (np.arange(rank * n, (rank + 1) * n, dtype=np.int64) % n), n * world
+
+
+def algorithmic(cfg, bundle, ns, n):
+    """Per-step algorithmic work: bytes for the HBM-bound
+    stages, FLOPs for the MLP, FP64 flops for transport."""
+    d, (h1, h2, h3) = bundle["d_in"], bundle["hidden"]
+    nets = bundle["n_nets"]
+    flops_net = 2 * (d * h1 + h1 * h2 + h2 * h3 + h3)
+    npair = ns * (ns + 1) // 2
+    return {
+        "thermo_bytes": n * ((3 + ns) * 8 + 3 * 8),
+        "transport_bytes": n * ((2 + ns) * 8 + (2 + ns) * 8),
+        # fits 11 ns, Wilke 7 ns^2, pairs 10 per pair (poly 8 + 2 fma), D_k 3 ns + ns^2 (numerators)
+        "transport_fp64_flops": n * (11 * ns + 7 * ns * ns + 10 * npair + 3 * ns + ns * ns + 40),
+        "L1_flops": n * nets * 2 * d * h1,
+        "L2_flops": n * nets * 2 * h1 * h2,
+        "L3_flops": n * nets * 2 * (h2 * h3 + h3),
+        "mlp_flops": n * nets * flops_net,
+        "L1_bytes": n * nets * h1 * 2,                # h1 activations written (bf16)
+        "epilogue_bytes": n * (3 * 8 + ns * 8 + ns * 8 + 8),
+        "prologue_bytes": n * ((2 + ns) * 8 + 64 * 2),
+    }
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2312_13513_b200 as rc
+    from workload import CONFIGS, load_mech, make_bundle, make_cells_at
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS[a.config]
+    mech_d = load_mech(cfg.mech)
+    bundle = make_bundle(cfg.mech, hidden=cfg.hidden)
+    mech = rc.Mechanism(mech_d)
+    prec = rc.RC_BF16 if a.precision == "bf16" else rc.RC_TF32
+    mlp = rc.MLPBundle(mech, bundle, prec)
+    ns, nets = mech_d["ns"], bundle["n_nets"]
+    idx, n_global = local_cells(cfg, rank, world, a.strong)
+    n = idx.size
+    host = make_cells_at(cfg, idx)
+    st = rc.CellState(n, ns, nets, outputs=("cp", "rho", "mu", "lam", "D", "wdot", "qdot"))
+    st.load(host["T_true"], host["p"], host["Y"])
+    stream = torch.cuda.current_stream()
+    # h of each cell from the previous step's state: h(T_true, Y) by the library's own T-mode thermo
+    rc.rc_thermo(mech, st.cells(rc.RC_MODE_T, chem=False, transport=False), stream)
+    T_guess = torch.from_numpy(host["T_guess"]).to("cuda")
+    ws = rc.aligned_workspace(mlp, n)
+    red_sum = torch.zeros(6, dtype=torch.float64, device="cuda")
+    cells = st.cells(rc.RC_MODE_H, dt=bundle["dt"])
+
+    def step():
+        st.T[:n].copy_(T_guess)                       # each step restarts Newton from the same guess
+        rc.rc_step(mech, mlp, cells, ws, stream)
+        if world > 1:                                  # a6: global max T and sums (NCCL over NVLink)
+            dist.all_reduce(st.red[:1], op=dist.ReduceOp.MAX)
+            red_sum[0:1].copy_(st.red[1:2])
+            red_sum[1:].copy_(st.diag.to(torch.float64))
+            dist.all_reduce(red_sum, op=dist.ReduceOp.SUM)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = rc.rc_last_launch_count()     # our kernels per rc_step (the T restore copy is torch's)
+    rc.rc_profile_enable(True)
+    rc.rc_profile_read(reset=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record(stream)
+        for _ in range(a.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / a.steps
+    prof = rc.rc_profile_read(reset=True)
+    rc.rc_profile_enable(False)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    total_cells = n * world if not a.strong else n_global
+    value = total_cells / (ms_max * 1e-3) / 1e6
+
+    # ---- end to end through the C ABI from pinned HOST buffers (H2D in, D2H out, every step)
+    e2e = None
+    if not a.no_e2e:
+        e2e = run_e2e(a, rc, mech, mlp, bundle, host, st, ws, n, ns, world, stream)
+
+    out = None
+    if rank == 0:
+        pk, pk_src = peaks()
+        f64, f64_src = fp64_peak()
+        alg = algorithmic(cfg, bundle, ns, n)
+        K = a.steps
+
+        def per(stage):
+            ms_s, cnt = prof[stage]
+            return ms_s / K, cnt / K
+
+        kernels = {}
+        for st_name, work, unit, bound, peak in [
+            ("thermo", alg["thermo_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),
+            ("transport", alg["transport_fp64_flops"], "TFLOP/s", "alu", f64),
+            ("prologue", alg["prologue_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),
+            ("L1", alg["L1_flops"], "TFLOP/s", "tensor", pk[SUSTAINED]),
+            ("L2", alg["L2_flops"], "TFLOP/s", "tensor", pk[SUSTAINED]),
+            ("L3", alg["L3_flops"], "TFLOP/s", "tensor", pk[SUSTAINED]),
+            ("epilogue", alg["epilogue_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),
+        ]:
+            t_ms, cnt = per(st_name)
+            if t_ms <= 0:
+                continue
+            scale = 1e9 if unit == "GB/s" else 1e12
+            ach = work / (t_ms * 1e-3) / scale
+            kernels[st_name] = {"bound": bound, "achieved": round(ach, 2), "peak": peak, "unit": unit,
+                                "frac": round(ach / peak, 4), "ms_per_step": round(t_ms, 4),
+                                "launches_per_step": cnt, "share": None}
+        tot_k = sum(v["ms_per_step"] for v in kernels.values())
+        for v in kernels.values():
+            v["share"] = round(v["ms_per_step"] / tot_k, 4) if tot_k else None
+        l2 = kernels.get("L2", {})
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "traffic_r01.json")
+        if os.path.exists(tf):
+            try:
+                traffic = json.load(open(tf)).get("L2_gemm_dram_bytes_per_launch")
+            except (OSError, ValueError):
+                traffic = None
+        mlp_ms = sum(per(s)[0] for s in ("L1", "L2", "L3"))
+        out = {
+            "metric": "Mcells/s per thermo+transport+DNN-chem step",
+            "value": round(value, 4),
+            "unit": "Mcells/s",
+            "n_gpus": world,
+            "steps": a.steps,
+            "warmup": a.warmup,
+            "ms_per_step": round(ms_max, 4),
+            "higher_is_better": True,
+            "scaling": "strong" if a.strong else "weak",
+            "vs_baseline": None,
+            "dtype": f"{a.precision} MLP (fp32 accumulate) + f64 thermo/transport/epilogue",
+            "data": "synthetic (seeded manifold states, random-init paper-shape MLP weights)",
+            "config": {"workload": f"{cfg.name}: {cfg.note}", "cells_per_gpu": int(n), "cells_total": int(total_cells),
+                       "mech": cfg.mech, "hidden": list(cfg.hidden), "nets": nets, "parallelism": f"cells dp{world}",
+                       "l2": "working set > L2 (1M cells x 8 nets activations in 32768-cell chunks ~0.9 GB; "
+                             "cell state 0.2 GB) - no flush needed",
+                       "precision": a.precision},
+            "roofline": {"kernel": "L2 GEMM (h1 1600 -> h2 800, tcgen05 bf16)", "bound": "tensor",
+                         "achieved": l2.get("achieved"), "peak": pk[SUSTAINED], "unit": "TFLOP/s",
+                         "frac": l2.get("frac"), "traffic": traffic,
+                         "peak_source": f"{pk_src} {SUSTAINED} (MEASURED_PEAKS.json)",
+                         "work_per_launch": "2*cells_chunk*1600*800*nets FLOP"},
+            "mlp_tflops": round(alg["mlp_flops"] / (mlp_ms * 1e-3) / 1e12, 2) if mlp_ms else None,
+            "kernels": kernels,
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches_per_step * a.steps),
+            "e2e": e2e,
+            "fp64_peak_source": f64_src,
+        }
+    if world > 1:
+        dist.barrier()
+    # ---- CPU oracle baseline, rank 0 at N = 1 only
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg, bundle, mech_d, a.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(a, rc, mech, mlp, bundle, host, st, ws, n, ns, world, stream):
+    """Same metric, timed from pinned host inputs to host outputs through rc_step."""
+    import torch
+    import torch.distributed as dist
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+    h_host = pin(st.h[:n].cpu().numpy())
+    in_T, in_p, in_Y = pin(host["T_guess"]), pin(host["p"]), pin(host["Y"])
+    outs = {"T": torch.empty(n, dtype=torch.float64).pin_memory(),
+            "cp": torch.empty(n, dtype=torch.float64).pin_memory(),
+            "rho": torch.empty(n, dtype=torch.float64).pin_memory(),
+            "mu": torch.empty(n, dtype=torch.float64).pin_memory(),
+            "lam": torch.empty(n, dtype=torch.float64).pin_memory(),
+            "D": torch.empty(ns, n, dtype=torch.float64).pin_memory(),
+            "wdot": torch.empty(ns, n, dtype=torch.float64).pin_memory(),
+            "qdot": torch.empty(n, dtype=torch.float64).pin_memory()}
+    cells = st.cells(rc.RC_MODE_H, dt=bundle["dt"])
+    h2d = (h_host.numel() + in_T.numel() + in_p.numel() + in_Y.numel()) * 8
+    d2h = sum(v.numel() for v in outs.values()) * 8
+
+    def step():
+        st.h[:n].copy_(h_host, non_blocking=True)
+        st.T[:n].copy_(in_T, non_blocking=True)
+        st.p[:n].copy_(in_p, non_blocking=True)
+        st.Y[:, :n].copy_(in_Y, non_blocking=True)
+        rc.rc_step(mech, mlp, cells, ws, stream)
+        for k, v in outs.items():
+            src = getattr(st, k)
+            v.copy_(src[:n] if src.dim() == 1 else src[:, :n], non_blocking=True)
+
+    for _ in range(max(1, a.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot = n * world if not a.strong else None
+    val = (tot if tot else n * world) / (t.item() * 1e-3) / 1e6
+    return {"value": round(val, 4), "unit": "Mcells/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": round(t.item(), 4), "api": "rc_step (C ABI) with pinned host buffers"}
+
+
+def oracle_time(cfg, bundle, mech_d, idx):
+    import oracle
+    from workload import make_cells_at
+    c = make_cells_at(cfg, idx)
+    om, ob = oracle.Mech(mech_d), oracle.Mlp(bundle)
+    h = oracle.step(om, None, c["T_true"], c["p"], c["Y"], mode="T", transport=False, chem=False)["h"]
+    t0 = time.perf_counter()
+    oracle.step(om, ob, c["T_guess"], c["p"], c["Y"], h=h)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, bundle, mech_d, seconds):
+    """The fp64 oracle as it stands, on the box's host cores, on a bounded hashed sample."""
+    import oracle
+    from workload.cells import uniform
+    oracle.build()
+    cores = len(os.sched_getaffinity(0))
+    n_all = cfg.n_cells
+    probe = np.unique((uniform(777, np.arange(max(16, cores))) * n_all).astype(np.int64))
+    t_probe = oracle_time(cfg, bundle, mech_d, probe)
+    per_cell = t_probe / probe.size
+    m = int(min(n_all, max(probe.size, seconds / max(per_cell, 1e-9))))
+    idx = np.unique((uniform(778, np.arange(m)) * n_all).astype(np.int64))
+    t = oracle_time(cfg, bundle, mech_d, idx)
+    return {"value": round(idx.size / t / 1e6, 8), "unit": "Mcells/s", "cores": cores, "kind": "oracle",
+            "sample": f"{idx.size} hashed-random cells of {cfg.name} (full step a1-a5, fp64, {t:.1f} s)"}
+
+
+def run_reference(a):
+    """--impl reference: the CPU oracle (this tier's reference arm), timed as it stands."""
+    import oracle
+    from workload import CONFIGS, load_mech, make_bundle
+    from workload.cells import uniform
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    oracle.build()
+    cfg = CONFIGS[a.config]
+    mech_d = load_mech(cfg.mech)
+    bundle = make_bundle(cfg.mech, hidden=cfg.hidden)
+    cores = len(os.sched_getaffinity(0))
+    n_all = cfg.n_cells
+    probe = np.unique((uniform(779, np.arange(max(16, cores))) * n_all).astype(np.int64))
+    per_cell = oracle_time(cfg, bundle, mech_d, probe) / probe.size
+    budget = min(10.0, 150.0 / max(1, a.steps + a.warmup))   # whole run within a few minutes
+    m = int(min(n_all, max(cores, budget / max(per_cell, 1e-9))))
+    times = []
+    for s in range(a.warmup + a.steps):
+        idx = np.unique((uniform(800 + s, np.arange(m)) * n_all).astype(np.int64))
+        t = oracle_time(cfg, bundle, mech_d, idx)
+        if s >= a.warmup:
+            times.append((idx.size, t))
+    cells = sum(c for c, _ in times)
+    secs = sum(t for _, t in times)
+    v = cells / secs / 1e6
+    out = {"impl": "reference", "metric": "Mcells/s per thermo+transport+DNN-chem step", "value": round(v, 8),
+           "unit": "Mcells/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+           "ms_per_step": round(1e3 * secs / len(times), 2), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": {"workload": f"{cfg.name}: {cfg.note}"},
+           "cpu_baseline": {"value": round(v, 8), "unit": "Mcells/s", "cores": cores, "kind": "oracle",
+                            "sample": f"{m} hashed-random cells of {cfg.name} per step"},
+           "e2e": {"value": round(v, 8), "unit": "Mcells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)

@@ -98,8 +98,8 @@ int rc_mech_ns(const rc_mech *m);
  * MLP bundle (HOST pointers, fp64; converted at create).  One net per
  * non-inert species, d_in = ns + 2 inputs [T, p, BCT(Y_1..ns)], hidden widths
  * hidden[0..2], 1 output.  Row-major [out][in] weights.
- * Kernels require hidden[0] % 32 == 0 and hidden[1] % 16 == 0 and
- * hidden[2] % 16 == 0, and d_in <= 64 (else RC_EUNSUPPORTED).
+ * Kernels require hidden[1] % 16 == 0 and
+ * hidden[2] % 16 == 0 (hidden[0] % 64 == 0 for the fused layer-1/2 kernel), and ns <= 28 (else RC_EUNSUPPORTED).
  * ------------------------------------------------------------------------- */
 typedef struct {
   int32_t n_nets;                 /* = number of non-inert species */
@@ -171,6 +171,25 @@ int rc_step(const rc_mech *m, const rc_mlp *n, const rc_cells *c, void *ws, size
  * [begin, end) with boundaries floor(r N / G) rounded down to 128 cells (the
  * MLP tile) except end = N for the last rank.  Pure host function. */
 int rc_partition(int64_t n_global, int rank, int world, int64_t *begin, int64_t *end);
+
+/* ---------------------------------------------------------------------------
+ * Per-stage device timing (SURVEY.md §5 "CUDA events per stage").  When
+ * enabled, every launch is bracketed by CUDA events on the caller's stream
+ * (a few microseconds of overhead per launch).  rc_profile_read waits for the
+ * recorded events, returns the summed milliseconds and launch counts per
+ * stage since the last reset, and optionally resets.  Process-global.
+ * ------------------------------------------------------------------------- */
+enum {
+  RC_STAGE_THERMO = 0, RC_STAGE_TRANSPORT = 1, RC_STAGE_PROLOGUE = 2, RC_STAGE_L1 = 3, RC_STAGE_L2 = 4,
+  RC_STAGE_L3 = 5, RC_STAGE_EPILOGUE = 6, RC_STAGE_FINALIZE = 7, RC_STAGE_COUNT = 8
+};
+int rc_profile_enable(int on);
+int rc_profile_read(double *ms /* [RC_STAGE_COUNT] */, int64_t *launches /* [RC_STAGE_COUNT] */, int reset);
+
+/* Developer aid: when non-NULL, CTA 0 of the fused layer-1/2 kernel writes a
+ * globaltimer event timeline (5 roles x 8 tiles x 64 chunks, uint64) into this
+ * device buffer on every launch.  NULL disables it (the default). */
+int rc_debug_timeline(void *device_buffer);
 
 /* Number of kernel launches the last rc_* call on this thread enqueued. */
 int64_t rc_last_launch_count(void);

@@ -59,6 +59,9 @@ EXPORTS = {
     "rc_step": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(rc_cells), C.c_void_p, C.c_size_t, C.c_void_p]),
     "rc_partition": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "rc_last_launch_count": (C.c_int64, []),
+    "rc_profile_enable": (C.c_int, [C.c_int]),
+    "rc_profile_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+    "rc_debug_timeline": (C.c_int, [C.c_void_p]),
     "rc_last_error": (C.c_char_p, []),
     "rc_version": (C.c_char_p, []),
 }
@@ -188,3 +191,18 @@ def rc_step(mech, mlp, cells, ws, stream=None):
 
 def rc_last_launch_count():
     return int(lib().rc_last_launch_count())
+
+
+STAGES = ["thermo", "transport", "prologue", "L1", "L2", "L3", "epilogue", "finalize"]
+
+
+def rc_profile_enable(on=True):
+    return check(lib().rc_profile_enable(1 if on else 0))
+
+
+def rc_profile_read(reset=True):
+    """{stage: (total_ms, launches)} since the last reset (waits for the events)."""
+    ms = np.zeros(len(STAGES), dtype=np.float64)
+    cnt = np.zeros(len(STAGES), dtype=np.int64)
+    check(lib().rc_profile_read(ms.ctypes.data, cnt.ctypes.data, 1 if reset else 0))
+    return {s: (float(ms[i]), int(cnt[i])) for i, s in enumerate(STAGES)}

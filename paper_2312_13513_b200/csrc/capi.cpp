@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 
 #include "rc_internal.h"
 
@@ -21,6 +22,76 @@ int rc_fail(int code, const char *fmt, ...) {
 }
 void rc_count_launch(int n) { g_launches += n; }
 void rc_reset_launches() { g_launches = 0; }
+
+// ---------------------------------------------------------------------------
+// per-stage profiling
+// ---------------------------------------------------------------------------
+namespace {
+struct ProfRec {
+  int stage;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;      // recorded, not yet read
+std::vector<cudaEvent_t> g_pool;  // free events
+cudaEvent_t prof_event() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+ProfScope::ProfScope(int st, cudaStream_t str) : stage(st), s(str), slot(-1) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  if (!g_prof_on) return;
+  ProfRec r{st, prof_event(), prof_event()};
+  cudaEventRecord(r.a, s);
+  slot = (int)g_prof.size();
+  g_prof.push_back(r);
+}
+ProfScope::~ProfScope() {
+  if (slot < 0) return;
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  cudaEventRecord(g_prof[slot].b, s);
+}
+
+extern "C" int rc_profile_enable(int on) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_on = on != 0;
+  return RC_OK;
+}
+
+extern "C" int rc_profile_read(double *ms, int64_t *launches, int reset) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  if (ms) for (int i = 0; i < RC_STAGE_COUNT; ++i) ms[i] = 0.0;
+  if (launches) for (int i = 0; i < RC_STAGE_COUNT; ++i) launches[i] = 0;
+  for (auto &r : g_prof) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return rc_fail(RC_ECUDA, "rc_profile_read: event sync failed");
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    if (r.stage >= 0 && r.stage < RC_STAGE_COUNT) {
+      if (ms) ms[r.stage] += t;
+      if (launches) launches[r.stage] += 1;
+    }
+  }
+  if (reset) {
+    for (auto &r : g_prof) { g_pool.push_back(r.a); g_pool.push_back(r.b); }
+    g_prof.clear();
+  }
+  return RC_OK;
+}
+
+extern unsigned long long *g_l12_dbg;
+extern "C" int rc_debug_timeline(void *buf) {
+  g_l12_dbg = static_cast<unsigned long long *>(buf);
+  return RC_OK;
+}
 
 extern "C" const char *rc_last_error(void) { return g_err; }
 extern "C" const char *rc_version(void) { return "rc-b200 0.1 (sm_100a)"; }
@@ -169,8 +240,8 @@ extern "C" int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *d, rc_mlp **ou
     return rc_fail(RC_EINVAL, "rc_mlp_create: NULL array");
   if (d->n_nets < 1 || d->n_nets > m->ns) return rc_fail(RC_EINVAL, "rc_mlp_create: n_nets=%d", d->n_nets);
   const int h1 = d->hidden[0], h2 = d->hidden[1], h3 = d->hidden[2];
-  if (h1 < 16 || h2 < 16 || h3 < 16 || h1 % 32 || h2 % 16 || h3 % 16 || h1 > 4096 || h2 > 4096 || h3 > 4096)
-    return rc_fail(RC_EUNSUPPORTED, "rc_mlp_create: hidden (%d,%d,%d) must be multiples of (32,16,16)", h1, h2, h3);
+  if (h1 < 64 || h2 < 16 || h3 < 16 || h1 % 64 || h2 % 16 || h3 % 16 || h1 > 4096 || h2 > 4096 || h3 > 4096)
+    return rc_fail(RC_EUNSUPPORTED, "rc_mlp_create: hidden (%d,%d,%d) must be multiples of (64,16,16)", h1, h2, h3);
   if (d->precision != RC_BF16 && d->precision != RC_TF32)
     return rc_fail(RC_EINVAL, "rc_mlp_create: unknown precision %d", d->precision);
   if (!(d->lambda_bc > 0.0) || !(d->dt > 0.0)) return rc_fail(RC_EINVAL, "rc_mlp_create: lambda and dt must be > 0");
@@ -179,8 +250,8 @@ extern "C" int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *d, rc_mlp **ou
   if (std::fabs(inv - invi) > 1e-9 * inv || invi < 1 || invi > 16)
     return rc_fail(RC_EUNSUPPORTED, "rc_mlp_create: 1/lambda_bc must be an integer in [1,16]");
   const int d_in = m->ns + 2;
-  if (d_in > (d->precision == RC_BF16 ? 64 : 32))
-    return rc_fail(RC_EUNSUPPORTED, "rc_mlp_create: d_in=%d too large for the layer-1 tile", d_in);
+  if (d_in + 2 > 32)  // z row: d_in inputs + two bias columns, padded to 16 or 32
+    return rc_fail(RC_EUNSUPPORTED, "rc_mlp_create: d_in=%d too large for the layer-1 tile (ns <= 28)", d_in);
   for (int i = 0; i < d->n_nets; ++i) {
     int s = d->species_of_net[i];
     if (s < 0 || s >= m->ns) return rc_fail(RC_EINVAL, "species_of_net[%d]=%d out of range", i, s);
@@ -196,7 +267,7 @@ extern "C" int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *d, rc_mlp **ou
   n->lambda_bc = d->lambda_bc;
   n->inv_lambda = invi;
   n->dt = d->dt;
-  n->kpad1 = d->precision == RC_BF16 ? 64 : 32;
+  n->kpad1 = d_in + 2 <= 16 ? 16 : 32;
   n->species_of_net.assign(d->species_of_net, d->species_of_net + d->n_nets);
   cudaGetDevice(&n->device);
   int rc = mlp_upload(n, d);

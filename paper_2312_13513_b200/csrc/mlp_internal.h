@@ -1,0 +1,18 @@
+// mlp_internal.h -- shared declarations of the MLP kernels (mlp_sm100.cu, mlp_l12_sm100.cu)
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "rc_internal.h"
+
+struct L12Args {
+  int m_tiles, passes, nets, chunks, h2, cap, stages;
+  const float *b2;         // [nets][h2]
+  __nv_bfloat16 *h2out;    // [nets][cap][h2]
+  unsigned long long *dbg; // optional event timeline of CTA 0 (debug builds of the bench only)
+};
+
+int mlp_num_sms();
+int l12_pass_width(int h2);
+int launch_l12(int NP, int KZ, const CUtensorMap &Z, const CUtensorMap &W1, const CUtensorMap &W2, const L12Args &a,
+               cudaStream_t s);

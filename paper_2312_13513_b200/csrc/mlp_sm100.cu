@@ -23,8 +23,11 @@
 #include <cstring>
 #include <mutex>
 
+#include "mlp_internal.h"
 #include "ptx.cuh"
 #include "rc_internal.h"
+
+unsigned long long *g_l12_dbg = nullptr;  // set by rc_debug_l12_timeline (tools only)
 
 namespace {
 
@@ -108,11 +111,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer (single thread)
-      constexpr uint32_t idesc = rcx::make_idesc(1u, BM, BN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
       for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+        const int n_blk = tile % g.n_tiles;
+        const int n_eff = min(BN, g.N - n_blk * BN);  // ragged last tile: multiple of 16
+        const uint32_t idesc = rcx::make_idesc(1u, BM, (uint32_t)n_eff);
         const int as = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         rcx::mbar_wait(&tempty[as], aphase ^ 1);
@@ -135,7 +140,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else {  // ---------------- epilogue warps 2..9
     const int q = warp & 3;            // TMEM lane quadrant this warp may access
     const int grp = (warp - 2) >> 2;   // column-chunk group 0/1
-    constexpr int NCH = BN / 16;
     int it = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
       const int n_blk = tile % g.n_tiles, rest = tile / g.n_tiles;
@@ -145,6 +149,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       rcx::mbar_wait(&tfull[as], aphase);
       rcx::tc_fence_after();
       const int row = m_blk * BM + q * 32 + lane;
+      const int NCH = min(BN, g.N - n_blk * BN) / 16;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
       const float *bias = g.bias + (size_t)net * g.N + n_blk * BN;
       float dot = 0.f;
@@ -186,33 +191,38 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // ------------------------------------------------------------------ prologue (a3)
 struct ProArgs {
   int64_t c0;       // first global cell of the chunk
-  int rows, rows_pad, d_in, ns;
+  int rows, rows_pad, d_in, ns, kz;
   float lambda, inv_lambda;
   const float *xmean, *xinvstd;
-  __nv_bfloat16 *z;  // [cap][64]
+  __nv_bfloat16 *z;  // [cap][kz]: z-scored inputs, then two 1.0 columns (b1 hi/lo), then zeros
 };
 
 __global__ void __launch_bounds__(256) prologue_kernel(ProArgs a, CellsDev c) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= a.rows_pad) return;
-  float x[64];
+  float x[32];
 #pragma unroll
-  for (int j = 0; j < 64; ++j) x[j] = 0.f;
+  for (int j = 0; j < 32; ++j) x[j] = 0.f;
   if (r < a.rows) {
     const int64_t i = a.c0 + r;
-    x[0] = (float)c.T[i];
-    x[1] = (float)c.p[i];
-    for (int k = 0; k < a.ns; ++k) {
-      float y = (float)c.Y[k * c.ld + i];
-      y = y > 0.f ? y : 0.f;                                       // Y^ = max(Y, 0)
-      float b = y > 0.f ? exp2f(a.lambda * log2f(y)) : 0.f;        // Y^^lambda
-      x[2 + k] = (b - 1.f) * a.inv_lambda;                         // Box-Cox
-    }
-    for (int j = 0; j < a.d_in; ++j) x[j] = (x[j] - a.xmean[j]) * a.xinvstd[j];
-  }
-  uint4 *dst = reinterpret_cast<uint4 *>(a.z + (size_t)r * 64);
+    x[0] = ((float)c.T[i] - a.xmean[0]) * a.xinvstd[0];
+    x[1] = ((float)c.p[i] - a.xmean[1]) * a.xinvstd[1];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
+    for (int k = 0; k < 30; ++k)
+      if (k < a.ns) {
+        float y = (float)c.Y[k * c.ld + i];
+        y = y > 0.f ? y : 0.f;                                       // Y^ = max(Y, 0)
+        float b = y > 0.f ? exp2f(a.lambda * log2f(y)) : 0.f;        // Y^^lambda
+        x[2 + k] = ((b - 1.f) * a.inv_lambda - a.xmean[2 + k]) * a.xinvstd[2 + k];  // Box-Cox, z-score
+      }
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j == a.d_in || j == a.d_in + 1) x[j] = 1.f;
+  }
+  uint4 *dst = reinterpret_cast<uint4 *>(a.z + (size_t)r * a.kz);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (q * 8 >= a.kz) break;
     uint32_t pk[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -382,29 +392,42 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
-// 3D bf16 map over [d2][d1][d0] (d0 contiguous), box {64, box1, 1}, 128-byte swizzle
-int make_map(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t box1) {
+// 3D bf16 map over [d2][d1][d0] (d0 contiguous), box {box0, box1, 1}; the swizzle
+// width equals the box row (box0 * 2 bytes: 32, 64 or 128)
+int make_map(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t box1,
+             uint32_t box0 = BK) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return rc_fail(RC_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {d0 * 2, d0 * d1 * 2};
-  cuuint32_t box[3] = {(cuuint32_t)BK, box1, 1};
+  cuuint32_t box[3] = {box0, box1, 1};
+  const CUtensorMapSwizzle sw = box0 * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : box0 * 2 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return rc_fail(RC_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return RC_OK;
 }
 
+// N-tile width: split N into ceil(N/208) near-equal tiles rounded up to 16
+// (the UMMA N granularity); the last tile may be narrower (runtime N in the
+// instruction descriptor, TMA zero-fills the rows past N).  Wide tiles keep the
+// shared-memory operand traffic per MMA under the 128 B/clk SMEM port.
 int pick_bn(int N) {
-  const int c[] = {160, 128, 96, 80, 64, 48, 32, 16};
+  if (N % 16) return 0;
+  const int nt = (N + 207) / 208;
+  int bn = ((N + nt - 1) / nt + 15) / 16 * 16;
+  const int c[] = {16, 32, 48, 64, 96, 128, 160, 208};
   for (int b : c)
-    if (N % b == 0) return b;
+    if (b >= bn) return b;
   return 0;
 }
+int n_tiles_of(int N) { return (N + pick_bn(N) - 1) / pick_bn(N); }
 
-int num_sms() {
+}  // namespace
+int mlp_num_sms() {
   static int n = 0;
   if (!n) {
     int dev = 0;
@@ -414,9 +437,11 @@ int num_sms() {
   }
   return n;
 }
+namespace {
+int num_sms() { return mlp_num_sms(); }
 
 template <int BN, int MODE>
-int launch_gemm_t(const CUtensorMap &A, const CUtensorMap &B, GemmArgs g, cudaStream_t s) {
+int launch_gemm_t(const CUtensorMap &A, const CUtensorMap &B, GemmArgs g, cudaStream_t s, int stage) {
   const size_t stage_bytes = (size_t)BM * BK * 2 + (size_t)BN * BK * 2;
   int stages = (int)((220 * 1024) / stage_bytes);
   if (stages > 8) stages = 8;
@@ -429,24 +454,26 @@ int launch_gemm_t(const CUtensorMap &A, const CUtensorMap &B, GemmArgs g, cudaSt
   }
   const int total = g.m_tiles * g.n_tiles * g.nets;
   int grid = total < num_sms() ? total : num_sms();
+  ProfScope prof(stage, s);
   gemm_kernel<BN, MODE><<<grid, GEMM_THREADS, smem, s>>>(A, B, g);
   RC_LAUNCH_CHECK();
   return RC_OK;
 }
 
-int launch_gemm(int BN, int MODE, const CUtensorMap &A, const CUtensorMap &B, const GemmArgs &g, cudaStream_t s) {
+int launch_gemm(int BN, int MODE, const CUtensorMap &A, const CUtensorMap &B, const GemmArgs &g, cudaStream_t s,
+                int stage) {
 #define RC_GEMM_CASE(bn)                                                   \
   case bn:                                                                 \
-    return MODE == 0 ? launch_gemm_t<bn, 0>(A, B, g, s) : launch_gemm_t<bn, 1>(A, B, g, s);
+    return MODE == 0 ? launch_gemm_t<bn, 0>(A, B, g, s, stage) : launch_gemm_t<bn, 1>(A, B, g, s, stage);
   switch (BN) {
     RC_GEMM_CASE(16)
     RC_GEMM_CASE(32)
     RC_GEMM_CASE(48)
     RC_GEMM_CASE(64)
-    RC_GEMM_CASE(80)
     RC_GEMM_CASE(96)
     RC_GEMM_CASE(128)
     RC_GEMM_CASE(160)
+    RC_GEMM_CASE(208)
     default:
       return rc_fail(RC_EUNSUPPORTED, "no GEMM tile for BN=%d", BN);
   }
@@ -464,10 +491,10 @@ WsLayout ws_layout(const rc_mlp *n, int cap) {
   L.cap = cap;
   size_t o = 0;
   L.qpart = o; o = al(o + QPART_BLOCKS * 8);
-  L.z = o; o = al(o + (size_t)cap * 64 * 2);
-  L.h1 = o; o = al(o + (size_t)n->n_nets * cap * n->h1 * 2);
+  L.z = o; o = al(o + (size_t)cap * n->kpad1 * 2);
+  L.h1 = o;  // layer-1 activations never leave the SM (fused L1/L2 kernel)
   L.h2 = o; o = al(o + (size_t)n->n_nets * cap * n->h2 * 2);
-  const int np3 = 2 * (n->h3 / pick_bn(n->h3));
+  const int np3 = 2 * n_tiles_of(n->h3);
   L.opart = o; o = al(o + (size_t)n->n_nets * np3 * cap * 4);
   L.total = o;
   return L;
@@ -492,19 +519,27 @@ size_t chem_workspace_bytes(const rc_mech *, const rc_mlp *n, int64_t ncells) {
 
 int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
   if (n->precision != RC_BF16) return rc_fail(RC_EUNSUPPORTED, "TF32 MLP variant not built yet");
-  if (!pick_bn(n->h1) || !pick_bn(n->h2) || !pick_bn(n->h3))
-    return rc_fail(RC_EUNSUPPORTED, "hidden widths need a divisor in {16..160}");
+  if (n->h1 % 64 || !l12_pass_width(n->h2) || !pick_bn(n->h3))
+    return rc_fail(RC_EUNSUPPORTED, "hidden widths (%d,%d,%d) not supported by the fused kernels", n->h1, n->h2, n->h3);
   const int nets = n->n_nets, din = n->d_in, h1 = n->h1, h2 = n->h2, h3 = n->h3, kp = n->kpad1;
   const size_t P = (size_t)h1 * din + h1 + (size_t)h2 * h1 + h2 + (size_t)h3 * h2 + h3 + h3 + 1;
   std::vector<uint16_t> W1((size_t)nets * h1 * kp, 0), W2((size_t)nets * h2 * h1), W3((size_t)nets * h3 * h2);
   std::vector<float> b1((size_t)nets * h1), b2((size_t)nets * h2), b3((size_t)nets * h3), w4((size_t)nets * h3), b4(nets);
   for (int i = 0; i < nets; ++i) {
     const double *p = d->params + i * P;
-    for (int r = 0; r < h1; ++r)
+    const double *pb1 = p + (size_t)h1 * din;
+    for (int r = 0; r < h1; ++r) {
       for (int k = 0; k < din; ++k) W1[((size_t)i * h1 + r) * kp + k] = f2bf((float)p[(size_t)r * din + k]);
-    p += (size_t)h1 * din;
-    for (int r = 0; r < h1; ++r) b1[(size_t)i * h1 + r] = (float)p[r];
-    p += h1;
+      // b1 folded into the layer-1 MMA: z carries 1.0 in columns din and din+1
+      const uint16_t hi = f2bf((float)pb1[r]);
+      uint32_t hb = (uint32_t)hi << 16;
+      float hf;
+      std::memcpy(&hf, &hb, 4);
+      W1[((size_t)i * h1 + r) * kp + din] = hi;
+      W1[((size_t)i * h1 + r) * kp + din + 1] = f2bf((float)(pb1[r] - (double)hf));
+      b1[(size_t)i * h1 + r] = (float)pb1[r];
+    }
+    p += (size_t)h1 * din + h1;
     for (size_t e = 0; e < (size_t)h2 * h1; ++e) W2[(size_t)i * h2 * h1 + e] = f2bf((float)p[e]);
     p += (size_t)h2 * h1;
     for (int r = 0; r < h2; ++r) b2[(size_t)i * h2 + r] = (float)p[r];
@@ -545,38 +580,40 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   if (L.total > ws_bytes) return rc_fail(RC_EINVAL, "workspace too small (%zu < %zu)", ws_bytes, L.total);
   uint8_t *w = static_cast<uint8_t *>(ws);
   auto *z = reinterpret_cast<__nv_bfloat16 *>(w + L.z);
-  auto *h1 = reinterpret_cast<__nv_bfloat16 *>(w + L.h1);
   auto *h2 = reinterpret_cast<__nv_bfloat16 *>(w + L.h2);
   auto *opart = reinterpret_cast<float *>(w + L.opart);
   auto *qpart = reinterpret_cast<double *>(w + L.qpart);
   const int nets = n->n_nets;
-  const int bn1 = pick_bn(n->h1), bn2 = pick_bn(n->h2), bn3 = pick_bn(n->h3);
-  CUtensorMap mz, mh1, mh2, mw1, mw2, mw3;
+  const int bn3 = pick_bn(n->h3), NP = l12_pass_width(n->h2), KZ = n->kpad1;
+  CUtensorMap mz, mh2, mw1, mw2, mw3;
   int rc;
-  if ((rc = make_map(&mz, z, 64, cap, 1, BM)) || (rc = make_map(&mh1, h1, n->h1, cap, nets, BM)) ||
-      (rc = make_map(&mh2, h2, n->h2, cap, nets, BM)) || (rc = make_map(&mw1, n->d_W1, 64, n->h1, nets, bn1)) ||
-      (rc = make_map(&mw2, n->d_W2, n->h1, n->h2, nets, bn2)) || (rc = make_map(&mw3, n->d_W3, n->h2, n->h3, nets, bn3)))
+  if ((rc = make_map(&mz, z, KZ, cap, 1, BM, KZ)) || (rc = make_map(&mh2, h2, n->h2, cap, nets, BM)) ||
+      (rc = make_map(&mw1, n->d_W1, KZ, n->h1, nets, 64, KZ)) ||
+      (rc = make_map(&mw2, n->d_W2, n->h1, n->h2, nets, NP > 256 ? NP / 2 : NP)) ||
+      (rc = make_map(&mw3, n->d_W3, n->h2, n->h3, nets, bn3)))
     return rc;
   RC_CUDA_TRY(cudaMemsetAsync(qpart, 0, QPART_BLOCKS * 8, s));
   int64_t launches = 1;
   for (int64_t c0 = 0; c0 < c.n; c0 += cap) {
     const int rows = (int)std::min<int64_t>(cap, c.n - c0);
     const int mt = (rows + BM - 1) / BM;
-    ProArgs pa{c0, rows, mt * BM, n->d_in, n->ns, (float)n->lambda_bc, (float)(1.0 / n->lambda_bc), n->d_xmean,
+    ProArgs pa{c0, rows, mt * BM, n->d_in, n->ns, KZ, (float)n->lambda_bc, (float)(1.0 / n->lambda_bc), n->d_xmean,
                n->d_xinvstd, z};
-    prologue_kernel<<<(mt * BM + 255) / 256, 256, 0, s>>>(pa, c);
-    RC_LAUNCH_CHECK();
-    GemmArgs g1{mt, n->h1 / bn1, nets, 1, 1, n->h1, cap, 0, n->d_b1, h1, nullptr, nullptr};
-    if ((rc = launch_gemm(bn1, 0, mz, mw1, g1, s))) return rc;
-    GemmArgs g2{mt, n->h2 / bn2, nets, (n->h1 + BK - 1) / BK, 0, n->h2, cap, 0, n->d_b2, h2, nullptr, nullptr};
-    if ((rc = launch_gemm(bn2, 0, mh1, mw2, g2, s))) return rc;
-    GemmArgs g3{mt, n->h3 / bn3, nets, (n->h2 + BK - 1) / BK, 0, n->h3, cap, 0, n->d_b3, nullptr, n->d_w4, opart};
-    if ((rc = launch_gemm(bn3, 1, mh2, mw3, g3, s))) return rc;
-    EpiArgs ea{c0, rows, cap, nets, 2 * (n->h3 / bn3), n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt, opart,
+    {
+      ProfScope prof(RC_STAGE_PROLOGUE, s);
+      prologue_kernel<<<(mt * BM + 255) / 256, 256, 0, s>>>(pa, c);
+      RC_LAUNCH_CHECK();
+    }
+    L12Args la{mt, n->h2 / NP, nets, n->h1 / 64, n->h2, cap, 0, n->d_b2, h2, g_l12_dbg};
+    if ((rc = launch_l12(NP, KZ, mz, mw1, mw2, la, s))) return rc;
+    GemmArgs g3{mt, n_tiles_of(n->h3), nets, (n->h2 + BK - 1) / BK, 0, n->h3, cap, 0, n->d_b3, nullptr, n->d_w4, opart};
+    if ((rc = launch_gemm(bn3, 1, mh2, mw3, g3, s, RC_STAGE_L3))) return rc;
+    EpiArgs ea{c0, rows, cap, nets, 2 * n_tiles_of(n->h3), n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt, opart,
                n->d_b4, n->d_ymean, n->d_ystd, m->d_P, m->d_thermo, n->d_species, qpart};
     const size_t esm = (size_t)ThermoSeg::size(m->ns) * 8 + (size_t)((m->ns * m->ns + 1) & ~1) * 8;
     int eblocks = (rows + 255) / 256;
     if (eblocks > QPART_BLOCKS) eblocks = QPART_BLOCKS;
+    ProfScope prof(RC_STAGE_EPILOGUE, s);
     if (m->ns == 9)
       chem_epilogue_kernel<9><<<eblocks, 256, esm, s>>>(ea, c);
     else if (m->ns == 20)
@@ -587,6 +624,7 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
     launches += 5;
   }
   if (c.red) {
+    ProfScope prof(RC_STAGE_FINALIZE, s);
     qdot_finalize_kernel<<<1, 32, 0, s>>>(qpart, QPART_BLOCKS, c.red);
     RC_LAUNCH_CHECK();
   }

@@ -78,6 +78,15 @@ struct rc_mlp {
 int rc_fail(int code, const char *fmt, ...);
 void rc_count_launch(int n = 1);
 void rc_reset_launches();
+// per-stage CUDA-event timing (rc_profile_*); no-op unless enabled
+struct ProfScope {
+  int stage;
+  cudaStream_t s;
+  int slot;
+  ProfScope(int stage, cudaStream_t s);
+  ~ProfScope();
+};
+
 #define RC_CUDA_TRY(x)                                                                    \
   do {                                                                                    \
     cudaError_t e_ = (x);                                                                 \

@@ -152,6 +152,7 @@ int launch_thermo(const rc_mech *m, const CellsDev &c, cudaStream_t s) {
   if (blocks > 148 * 16) blocks = 148 * 16;
   const size_t smem = (size_t)ThermoSeg::size(m->ns) * 8;
   const bool u = m->uniform_tmid;
+  ProfScope prof(RC_STAGE_THERMO, s);
   if (m->ns == 9 && u)
     thermo_kernel<9, true><<<(unsigned)blocks, threads, smem, s>>>(m->d_thermo, m->ns, c);
   else if (m->ns == 20 && u)

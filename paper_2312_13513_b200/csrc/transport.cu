@@ -128,6 +128,7 @@ int launch_transport(const rc_mech *m, const CellsDev &c, cudaStream_t s) {
   int64_t blocks = (c.n + threads - 1) / threads;
   if (blocks > 148 * 32) blocks = 148 * 32;
   const size_t smem = (size_t)TransportSeg::size(m->ns) * 8;
+  ProfScope prof(RC_STAGE_TRANSPORT, s);
   if (m->ns == 9)
     transport_kernel<9><<<(unsigned)blocks, threads, smem, s>>>(m->d_transport, m->ns, c);
   else if (m->ns == 20) {

@@ -1,0 +1,20 @@
+#!/bin/bash
+# One GPU pass: smoke, parity tests, bench, ncu launch list, ncu full captures.
+# usage (under gpurun): bash tools/gpu_round.sh [tag]
+set -u
+TAG=${1:-r01}
+O=gpurun_out
+mkdir -p $O
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke_$TAG.log 2>&1; echo "smoke rc=$?"
+tail -2 $O/smoke_$TAG.log
+timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?"
+tail -3 $O/pytest_gpu_$TAG.log
+timeout 900 python bench.py > $O/bench_$TAG.json 2> $O/bench_$TAG.err; echo "bench rc=$?"
+cat $O/bench_$TAG.json; tail -3 $O/bench_$TAG.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_$TAG.csv \
+  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "ncu list rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 4 -c 3 \
+  -o $O/prof_gemm_$TAG -f python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_gemm_$TAG.log 2>&1; echo "ncu gemm rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"thermo_kernel|transport_kernel|chem_epilogue|prologue" -s 2 -c 4 \
+  -o $O/prof_fp64_$TAG -f python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_fp64_$TAG.log 2>&1; echo "ncu fp64 rc=$?"
+ls -la $O
