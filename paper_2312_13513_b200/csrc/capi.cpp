@@ -88,6 +88,11 @@ extern "C" int rc_profile_read(double *ms, int64_t *launches, int reset) {
 }
 
 extern unsigned long long *g_l12_dbg;
+extern int g_l12_flags;
+extern "C" int rc_debug_flags(int flags) {
+  g_l12_flags = flags;
+  return RC_OK;
+}
 extern "C" int rc_debug_timeline(void *buf) {
   g_l12_dbg = static_cast<unsigned long long *>(buf);
   return RC_OK;

@@ -27,7 +27,8 @@
 #include "ptx.cuh"
 #include "rc_internal.h"
 
-unsigned long long *g_l12_dbg = nullptr;  // set by rc_debug_l12_timeline (tools only)
+unsigned long long *g_l12_dbg = nullptr;  // set by rc_debug_timeline (developer tool)
+int g_l12_flags = 0;                      // set by rc_debug_flags (developer tool)
 
 namespace {
 
@@ -511,9 +512,9 @@ uint16_t f2bf(float f) {  // round-to-nearest-even float -> bf16 bits
 }  // namespace
 
 size_t chem_workspace_bytes(const rc_mech *, const rc_mlp *n, int64_t ncells) {
-  int64_t cap = (ncells + 127) / 128 * 128;
+  int64_t cap = (ncells + 255) / 256 * 256;  // chunks of CTA-pair (256-row) tiles
   if (cap > MAX_CAP) cap = MAX_CAP;
-  if (cap < 128) cap = 128;
+  if (cap < 256) cap = 256;
   return ws_layout(n, (int)cap).total;
 }
 
@@ -574,8 +575,8 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
 int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, size_t ws_bytes, cudaStream_t s) {
   if (c.n == 0) return RC_OK;
   // chunk capacity: largest multiple of 128 (<= MAX_CAP, <= n rounded up) whose layout fits the workspace
-  int cap = (int)std::min<int64_t>((c.n + 127) / 128 * 128, MAX_CAP);
-  while (cap > 128 && ws_layout(n, cap).total > ws_bytes) cap -= 128;
+  int cap = (int)std::min<int64_t>((c.n + 255) / 256 * 256, MAX_CAP);
+  while (cap > 256 && ws_layout(n, cap).total > ws_bytes) cap -= 256;
   WsLayout L = ws_layout(n, cap);
   if (L.total > ws_bytes) return rc_fail(RC_EINVAL, "workspace too small (%zu < %zu)", ws_bytes, L.total);
   uint8_t *w = static_cast<uint8_t *>(ws);
@@ -585,18 +586,21 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   auto *qpart = reinterpret_cast<double *>(w + L.qpart);
   const int nets = n->n_nets;
   const int bn3 = pick_bn(n->h3), NP = l12_pass_width(n->h2), KZ = n->kpad1;
-  CUtensorMap mz, mh2, mw1, mw2, mw3;
+  const int P1 = NP > 256 ? 256 : NP, P2 = NP - P1;
+  CUtensorMap mz, mh2, mh2st, mw1, mw2a, mw2b, mw3;
   int rc;
   if ((rc = make_map(&mz, z, KZ, cap, 1, BM, KZ)) || (rc = make_map(&mh2, h2, n->h2, cap, nets, BM)) ||
-      (rc = make_map(&mw1, n->d_W1, KZ, n->h1, nets, 64, KZ)) ||
-      (rc = make_map(&mw2, n->d_W2, n->h1, n->h2, nets, NP > 256 ? NP / 2 : NP)) ||
-      (rc = make_map(&mw3, n->d_W3, n->h2, n->h3, nets, bn3)))
+      (rc = make_map(&mw1, n->d_W1, KZ, n->h1, nets, 32, KZ)) ||
+      (rc = make_map(&mw2a, n->d_W2, n->h1, n->h2, nets, P1 / 2)) ||
+      (rc = make_map(&mw2b, n->d_W2, n->h1, n->h2, nets, P2 > 0 ? P2 / 2 : P1 / 2)) ||
+      (rc = make_map(&mw3, n->d_W3, n->h2, n->h3, nets, bn3)) ||
+      (rc = make_map(&mh2st, h2, n->h2, cap, nets, 32, 16)))  // h2 TMA stores: 32 rows x 16 cols
     return rc;
   RC_CUDA_TRY(cudaMemsetAsync(qpart, 0, QPART_BLOCKS * 8, s));
   int64_t launches = 1;
   for (int64_t c0 = 0; c0 < c.n; c0 += cap) {
     const int rows = (int)std::min<int64_t>(cap, c.n - c0);
-    const int mt = (rows + BM - 1) / BM;
+    const int mt = (rows + 2 * BM - 1) / (2 * BM) * 2;  // even: CTA pairs of 128-row tiles
     ProArgs pa{c0, rows, mt * BM, n->d_in, n->ns, KZ, (float)n->lambda_bc, (float)(1.0 / n->lambda_bc), n->d_xmean,
                n->d_xinvstd, z};
     {
@@ -604,8 +608,8 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
       prologue_kernel<<<(mt * BM + 255) / 256, 256, 0, s>>>(pa, c);
       RC_LAUNCH_CHECK();
     }
-    L12Args la{mt, n->h2 / NP, nets, n->h1 / 64, n->h2, cap, 0, n->d_b2, h2, g_l12_dbg};
-    if ((rc = launch_l12(NP, KZ, mz, mw1, mw2, la, s))) return rc;
+    L12Args la{mt, n->h2 / NP, nets, n->h1 / 64, n->h2, cap, 0, n->d_b2, h2, g_l12_dbg, g_l12_flags};
+    if ((rc = launch_l12_pair(NP, KZ, mz, mw1, mw2a, mw2b, mh2st, la, s))) return rc;
     GemmArgs g3{mt, n_tiles_of(n->h3), nets, (n->h2 + BK - 1) / BK, 0, n->h3, cap, 0, n->d_b3, nullptr, n->d_w4, opart};
     if ((rc = launch_gemm(bn3, 1, mh2, mw3, g3, s, RC_STAGE_L3))) return rc;
     EpiArgs ea{c0, rows, cap, nets, 2 * n_tiles_of(n->h3), n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt, opart,

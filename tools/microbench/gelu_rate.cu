@@ -1,0 +1,57 @@
+// Throughput of the GELU building blocks on B200: tanh.approx.{f32,bf16x2},
+// fma.rn.bf16x2, and the full packed-bf16x2 GELU vs the fp32 one.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+__device__ __forceinline__ uint32_t tanh2(uint32_t x) { uint32_t r; asm volatile("tanh.approx.bf16x2 %0, %1;" : "=r"(r) : "r"(x)); return r; }
+__device__ __forceinline__ float tanh1(float x) { float r; asm volatile("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
+__device__ __forceinline__ uint32_t fma2(uint32_t a, uint32_t b, uint32_t c) { uint32_t r; asm volatile("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c)); return r; }
+__device__ __forceinline__ uint32_t gelu2(uint32_t x) {
+  const uint32_t c0 = 0x3F4C3F4Cu, c1 = 0x3D123D12u, hf = 0x3F003F00u; uint32_t xx, t, u, th, hx, r;
+  asm("mul.rn.bf16x2 %0, %1, %1;" : "=r"(xx) : "r"(x)); asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(t) : "r"(xx), "r"(c1), "r"(c0));
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(u) : "r"(t), "r"(x)); asm("tanh.approx.bf16x2 %0, %1;" : "=r"(th) : "r"(u));
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(hx) : "r"(x), "r"(hf)); asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(hx), "r"(th), "r"(hx));
+  return r;
+}
+__device__ __forceinline__ float gelu1(float x) { float u = x * fmaf(0.0356774081f, x * x, 0.7978845608f); float hx = 0.5f * x; return fmaf(hx, tanh1(u), hx); }
+
+template <int MODE>
+__global__ void k(int iters, uint32_t *out) {
+  uint32_t v[8]; float f[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { v[i] = 0x3E003E00u + threadIdx.x + i; f[i] = 0.1f * i + threadIdx.x * 1e-4f; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (MODE == 0) v[i] = tanh2(v[i]);
+      if (MODE == 1) f[i] = tanh1(f[i]);
+      if (MODE == 2) v[i] = fma2(v[i], 0x3F803F80u, 0x00010001u);
+      if (MODE == 3) v[i] = gelu2(v[i]);
+      if (MODE == 4) f[i] = gelu1(f[i]);
+    }
+  }
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s ^= v[i] ^ __float_as_uint(f[i]);
+  if (s == 0x12345678) out[0] = s;
+}
+int main() {
+  uint32_t *d; cudaMalloc(&d, 4);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const char *names[] = {"tanh.approx.bf16x2 (elements)", "tanh.approx.f32", "fma.rn.bf16x2 (elements)", "gelu bf16x2 (elements)", "gelu f32"};
+  for (int warps : {4, 8, 16}) {
+    for (int m = 0; m < 5; ++m) {
+      int iters = 4096; dim3 g(148), b(32 * warps);
+      auto launch = [&]() { switch (m) { case 0: k<0><<<g, b>>>(iters, d); break; case 1: k<1><<<g, b>>>(iters, d); break;
+        case 2: k<2><<<g, b>>>(iters, d); break; case 3: k<3><<<g, b>>>(iters, d); break; case 4: k<4><<<g, b>>>(iters, d); break; } };
+      launch(); cudaDeviceSynchronize();
+      cudaEventRecord(e0); launch(); cudaEventRecord(e1); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      double elems = 8.0 * iters * g.x * b.x * ((m == 0 || m == 2 || m == 3) ? 2 : 1);
+      printf("warps/SM=%2d %-32s %8.1f Gelem/s = %6.1f elem/clk/SM @1.9GHz\n", warps, names[m], elems / ms / 1e6, elems / ms / 1e6 / 148 / 1.9);
+    }
+  }
+  return 0;
+}
