@@ -186,15 +186,6 @@ enum {
 int rc_profile_enable(int on);
 int rc_profile_read(double *ms /* [RC_STAGE_COUNT] */, int64_t *launches /* [RC_STAGE_COUNT] */, int reset);
 
-/* Developer aid: when non-NULL, CTA 0 of the fused layer-1/2 kernel writes a
- * globaltimer event timeline (10 roles x 8 tiles x 64 chunks, uint64) into this
- * device buffer on every launch.  NULL disables it (the default). */
-int rc_debug_timeline(void *device_buffer);
-/* Developer aid: diagnostic switches of the fused layer-1/2 kernel that break
- * its results (bit 0: MMA ignores h1-chunk readiness, bit 1: no weight loads).
- * Must be 0 (the default) for any real use. */
-int rc_debug_flags(int flags);
-
 /* Number of kernel launches the last rc_* call on this thread enqueued. */
 int64_t rc_last_launch_count(void);
 

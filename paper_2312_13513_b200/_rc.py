@@ -61,8 +61,6 @@ EXPORTS = {
     "rc_last_launch_count": (C.c_int64, []),
     "rc_profile_enable": (C.c_int, [C.c_int]),
     "rc_profile_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
-    "rc_debug_timeline": (C.c_int, [C.c_void_p]),
-    "rc_debug_flags": (C.c_int, [C.c_int]),
     "rc_last_error": (C.c_char_p, []),
     "rc_version": (C.c_char_p, []),
 }

@@ -87,17 +87,6 @@ extern "C" int rc_profile_read(double *ms, int64_t *launches, int reset) {
   return RC_OK;
 }
 
-extern unsigned long long *g_l12_dbg;
-extern int g_l12_flags;
-extern "C" int rc_debug_flags(int flags) {
-  g_l12_flags = flags;
-  return RC_OK;
-}
-extern "C" int rc_debug_timeline(void *buf) {
-  g_l12_dbg = static_cast<unsigned long long *>(buf);
-  return RC_OK;
-}
-
 extern "C" const char *rc_last_error(void) { return g_err; }
 extern "C" const char *rc_version(void) { return "rc-b200 0.1 (sm_100a)"; }
 extern "C" int64_t rc_last_launch_count(void) { return g_launches; }
@@ -272,7 +261,7 @@ extern "C" int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *d, rc_mlp **ou
   n->lambda_bc = d->lambda_bc;
   n->inv_lambda = invi;
   n->dt = d->dt;
-  n->kpad1 = d_in + 2 <= 16 ? 16 : 32;
+  n->kpad1 = d_in + 2 <= 16 ? 16 : 32;  // z row: d_in inputs, two constant-1 bias columns, zero padding
   n->species_of_net.assign(d->species_of_net, d->species_of_net + d->n_nets);
   cudaGetDevice(&n->device);
   int rc = mlp_upload(n, d);

@@ -1,0 +1,95 @@
+// mlp_common.cuh -- device helpers shared by the MLP kernels (mlp_l1/l2/sm100.cu):
+// packed-bf16x2 GELU, fp32->bf16x2 packing, UMMA descriptors, TMA stores and
+// the 128-byte-swizzled staging layout the TMA store/load maps use.
+#pragma once
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace rcm {
+
+// GELU, tanh form, packed bf16x2 on the FMA pipe + one MUFU op per pair:
+// 0.5 x (1 + tanh(x (c0 + c1 x^2))), c0 = sqrt(2/pi), c1 = 0.044715 c0.  Its
+// deviation from the oracle's exact-erf GELU (< 1e-3 absolute) is of the order
+// of the bf16 rounding of the activations it produces (MLP numerics).
+__device__ __forceinline__ uint32_t gelu_bf16x2(uint32_t x) {
+  const uint32_t c0 = 0x3F4C3F4Cu;  // bf16(0.7978846) x2
+  const uint32_t c1 = 0x3D123D12u;  // bf16(0.0356774) x2
+  const uint32_t hf = 0x3F003F00u;  // 0.5 x2
+  uint32_t xx, t, u, th, hx, r;
+  asm("mul.rn.bf16x2 %0, %1, %1;" : "=r"(xx) : "r"(x));
+  asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(t) : "r"(xx), "r"(c1), "r"(c0));
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(u) : "r"(t), "r"(x));
+  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(th) : "r"(u));
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(hx) : "r"(x), "r"(hf));
+  asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(hx), "r"(th), "r"(hx));
+  return r;
+}
+// The same GELU applied to y = x/2 (the layer-1 weights are stored halved, which is
+// exact in bf16): x (c0 + c1 x^2) = y (2 c0 + 8 c1 y^2) and 0.5 x (1 + t) = y + y t,
+// so the result equals gelu_bf16x2(2y) bit for bit with one multiply fewer.
+__device__ __forceinline__ uint32_t gelu_half_bf16x2(uint32_t y) {
+  const uint32_t c0 = 0x3FCC3FCCu;  // 2 bf16(0.7978846) x2
+  const uint32_t c1 = 0x3E923E92u;  // 8 bf16(0.0356774) x2
+  uint32_t yy, t, u, th, r;
+  asm("mul.rn.bf16x2 %0, %1, %1;" : "=r"(yy) : "r"(y));
+  asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(t) : "r"(yy), "r"(c1), "r"(c0));
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(u) : "r"(t), "r"(y));
+  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(th) : "r"(u));
+  asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(y), "r"(th), "r"(y));
+  return r;
+}
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ float bf_lo(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+
+// UMMA K-major descriptor for a 32/64/128-byte swizzled tile (8-row atoms, SBO = 8 rows)
+template <int ROW_BYTES>
+__device__ __forceinline__ uint64_t desc_sw(const void *smem) {
+  constexpr uint64_t layout = ROW_BYTES == 128 ? 2 : ROW_BYTES == 64 ? 4 : 6;
+  uint64_t d = (uint64_t)((rcx::smem_u32(smem) & 0x3FFFF) >> 4);
+  d |= (uint64_t)((8 * ROW_BYTES) >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= layout << 61;
+  return d;
+}
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, const void *src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+               "r"(rcx::smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// named barrier over the first `n` threads of the CTA (id 1; id 0 is __syncthreads)
+__device__ __forceinline__ void bar_sync_1(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+// 16 bf16 columns (32 B) of row `row` into a [rows][64] bf16 staging block laid out
+// as the TMA 128-byte swizzle expects (16-byte unit u of row r at r*128 + ((u ^ r%8) * 16));
+// `unit0` = the even 16-byte unit (0, 2, 4, 6) the 16 columns start at.
+__device__ __forceinline__ void stage_sw128(uint8_t *blk, int row, int unit0, const uint32_t (&pk)[8]) {
+  uint8_t *r = blk + row * 128;
+  const int x = row & 7;
+  *reinterpret_cast<uint4 *>(r + ((unit0 ^ x) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  *reinterpret_cast<uint4 *>(r + (((unit0 + 1) ^ x) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+}
+
+}  // namespace rcm

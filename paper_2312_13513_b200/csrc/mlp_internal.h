@@ -1,19 +1,28 @@
-// mlp_internal.h -- shared declarations of the MLP kernels (mlp_sm100.cu, mlp_l12_sm100.cu)
+// mlp_internal.h -- shared declarations of the MLP kernels (mlp_sm100.cu, mlp_l2_sm100.cu)
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
 
 #include "rc_internal.h"
 
-struct L12Args {
-  int m_tiles, passes, nets, chunks, h2, cap, stages;
-  const float *b2;         // [nets][h2]
-  __nv_bfloat16 *h2out;    // [nets][cap][h2]
-  unsigned long long *dbg; // optional event timeline of CTA 0 (developer tool)
-  int flags;               // developer diagnostics (0 in production): bit0 skip a2full, bit1 skip weight loads
-};
-
 int mlp_num_sms();
-int l12_pass_width(int h2);
-int launch_l12_pair(int NP, int KZ, const CUtensorMap &Z, const CUtensorMap &W1, const CUtensorMap &W2a,
-                    const CUtensorMap &W2b, const CUtensorMap &H2, const L12Args &a, cudaStream_t s);
+
+// layer 1 (mlp_l1_sm100.cu): h1 = GELU(z W1^T) with W1 stored halved, 128 x 256 tiles
+// (W1 boxes of l1_box_rows() rows), h1 TMA-stored through `Out` (64-column x 32-row boxes,
+// 128-byte swizzle) into [nets][cap][N] bf16
+struct L1Args {
+  int m_tiles, n_tiles, nets, N, stages, cap;
+  __nv_bfloat16 *h1;
+};
+int l1_tile_n();
+int l1_box_rows();
+int launch_l1(int KZ, const CUtensorMap &Z, const CUtensorMap &W, const CUtensorMap &Out, const L1Args &a,
+              cudaStream_t s);
+int l2_pass_width(int h2);
+
+struct L2Args {
+  int m_tiles, passes, nets, chunks, N, stages;
+  const float *bias;       // [nets][N]
+};
+int launch_l2_pair(int NP, const CUtensorMap &A, const CUtensorMap &Ba, const CUtensorMap &Bb, const CUtensorMap &Out,
+                   const L2Args &a, cudaStream_t s);

@@ -1,0 +1,259 @@
+// mlp_l2_sm100.cu -- layer 2 of the per-species MLP (1600 -> 800,
+// GELU) as a persistent CTA-pair tcgen05 GEMM:
+//
+//   h2[:, pass] = GELU( h1 W2[pass]^T + b2 )        (bf16 in, fp32 accumulate, bf16 out)
+//
+// Each CTA pair (cluster of 2) owns a 256-cell x NP tile (NP = 400: one of two
+// passes over the 800 outputs).  The even CTA issues M=256 cta_group::2 MMAs
+// whose A rows (h1, loaded by TMA) are split 128/128 between the two CTAs and
+// whose B operand (a 64-wide K chunk of W2[pass]) is split by N, so each SM
+// stages half of every weight chunk.  The NP outputs are two MMA pieces
+// (N = 256 + 144) that alternate in the instruction stream: back-to-back MMAs
+// into one accumulator stall on the accumulator dependency, alternating two
+// accumulators runs at the nominal rate (tools/microbench/mma_rate.cu).
+// The only barrier the MMA thread waits on per K chunk is the TMA "full"
+// barrier (extra waits between MMAs cost ~70 clk of tensor-pipe bubble each).
+// Sixteen epilogue warps (four per TMEM lane quadrant) drain acc2: b2 + GELU
+// (packed bf16x2, tanh form) -> swizzled smem staging -> TMA bulk tensor store.
+//
+// Warps: 0..15 epilogue, 16 TMA producer, 17 MMA issuer (the scheduler favours
+// higher warp ids, so the single-thread roles get the highest ids).
+#include <cuda_bf16.h>
+
+#include "mlp_common.cuh"
+#include "mlp_internal.h"
+
+namespace {
+
+constexpr int NEPI = 16;
+constexpr int L2_THREADS = 32 * NEPI + 64;
+constexpr int KC = 64;  // K chunk (one 128-byte swizzle row of bf16)
+
+using rcm::bulk_commit;
+using rcm::bulk_wait_all;
+using rcm::bulk_wait_read1;
+using rcm::cvt_bf16x2;
+using rcm::fence_async_smem;
+using rcm::gelu_bf16x2;
+using rcm::tma_store_3d;
+using rcm::tmem_ld32;
+__device__ __forceinline__ uint64_t desc_sw128(const void *smem) { return rcm::desc_sw<128>(smem); }
+
+template <int NP>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
+    l2_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBa,
+                   const __grid_constant__ CUtensorMap mapBb, const __grid_constant__ CUtensorMap mapOut, L2Args a) {
+  static_assert(NP % 16 == 0 && NP <= 512, "pass width");
+  constexpr int P1 = NP > 256 ? 256 : NP, P2 = NP - P1;
+  constexpr int H1 = P1 / 2, H2 = P2 / 2;  // B rows per CTA of each piece
+  static_assert(H1 % 8 == 0 && H2 % 8 == 0, "8-row swizzle atoms");
+  constexpr uint32_t A_BYTES = 128 * KC * 2, B_BYTES = (NP / 2) * KC * 2;
+  constexpr uint32_t STAGE = (A_BYTES + B_BYTES + 1023u) & ~1023u;
+  constexpr int W_TMA = NEPI, W_MMA = NEPI + 1;
+
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = rcx::smem_u32(smem_raw);
+  uint8_t *smem = smem_raw + (((base_u32 + 1023u) & ~1023u) - base_u32);
+  const int S = a.stages;
+  uint8_t *sW = smem;                                   // S x [A tile | B half]
+  uint8_t *sST = sW + S * STAGE;                        // NEPI x 2 x 1 KB store staging
+  float *sB2 = reinterpret_cast<float *>(sST + NEPI * 2 * 1024);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sB2 + 2 * NP);
+  uint64_t *full = bar, *empty = full + S, *c2full = empty + S, *c2empty = c2full + 1, *bfull = c2empty + 1,
+           *bempty = bfull + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = rcx::cluster_rank();
+  const bool leader = rank == 0;
+  if (warp == W_TMA && lane == 0) {
+    rcx::prefetch_tmap(&mapA);
+    rcx::prefetch_tmap(&mapBa);
+    if (P2 > 0) rcx::prefetch_tmap(&mapBb);
+    rcx::prefetch_tmap(&mapOut);
+    for (int s = 0; s < S; ++s) { rcx::mbar_init(&full[s], 2); rcx::mbar_init(&empty[s], 1); }
+    rcx::mbar_init(c2full, 1);
+    rcx::mbar_init(c2empty, 2 * NEPI);
+    for (int z = 0; z < 2; ++z) { rcx::mbar_init(&bfull[z], 1); rcx::mbar_init(&bempty[z], NEPI); }
+    rcx::fence_mbar_init();
+  }
+  if (warp == W_MMA) rcx::tmem_alloc_pair(tmem_slot, 512);
+  rcx::tc_fence_before();
+  rcx::cluster_sync();
+  rcx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int C = a.chunks;
+  const int pairs = a.m_tiles / 2;
+  const int total = a.nets * pairs * a.passes;
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == W_TMA) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer (both CTAs)
+      const uint32_t full0 = rcx::map_cta(full, 0);
+      int s = 0;
+      uint32_t ph = 0;
+      int it = 0;
+      for (int tile = cl; tile < total; tile += ncl, ++it) {
+        const int pass = tile % a.passes, rest = tile / a.passes;
+        const int mp = rest % pairs, net = rest / pairs;
+        const int zb = it & 1;
+        rcx::mbar_wait(&bempty[zb], ((it >> 1) & 1) ^ 1);  // b2 slice for this CTA's drain
+        rcx::mbar_arrive_expect_tx(&bfull[zb], NP * 4);
+        rcx::bulk_g2s(sB2 + zb * NP, a.bias + (size_t)net * a.N + pass * NP, NP * 4, &bfull[zb]);
+        for (int c = 0; c < C; ++c) {
+          rcx::mbar_wait(&empty[s], ph ^ 1);
+          rcx::mbar_arrive_expect_tx_cluster(full0 + s * 8, A_BYTES + B_BYTES);
+          uint8_t *st = sW + s * STAGE;
+          rcx::tma_load_3d_pair(st, &mapA, &full[s], c * KC, mp * 256 + rank * 128, net);
+          rcx::tma_load_3d_pair(st + A_BYTES, &mapBa, &full[s], c * KC, pass * NP + rank * H1, net);
+          if (P2 > 0)
+            rcx::tma_load_3d_pair(st + A_BYTES + H1 * 128, &mapBb, &full[s], c * KC, pass * NP + P1 + rank * H2, net);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == W_MMA) {
+    if (lane == 0 && leader) {  // ------------------------------------- MMA issuer (even CTA)
+      constexpr uint32_t idp1 = rcx::make_idesc(1u, 256, P1);
+      constexpr uint32_t idp2 = rcx::make_idesc(1u, 256, P2 > 0 ? P2 : 16);
+      int s = 0;
+      uint32_t ph = 0;
+      int it = 0;
+      for (int tile = cl; tile < total; tile += ncl, ++it) {
+        rcx::mbar_wait(c2empty, (it & 1) ^ 1);  // previous tile drained
+        rcx::tc_fence_after();
+        for (int c = 0; c < C; ++c) {
+          rcx::mbar_wait(&full[s], ph);
+          rcx::tc_fence_after();
+          const uint64_t da = desc_sw128(sW + s * STAGE);
+          const uint64_t db = desc_sw128(sW + s * STAGE + A_BYTES);
+#pragma unroll
+          for (int k = 0; k < KC / 16; ++k) {
+            rcx::mma_bf16_pair(tmem, da + 2 * k, db + 2 * k, idp1, (c | k) != 0);
+            if (P2 > 0)
+              rcx::mma_bf16_pair(tmem + P1, da + 2 * k, db + (uint64_t)((H1 * 128) >> 4) + 2 * k, idp2, (c | k) != 0);
+          }
+          rcx::mma_commit_pair(&empty[s]);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+        rcx::mma_commit_pair(c2full);
+      }
+    }
+  } else {  // ------------------------------------------------------ epilogue warps 0..15 (both CTAs)
+    const int q = warp & 3, sub = warp >> 2;
+    const uint32_t tq = (uint32_t)(q * 32) << 16;
+    constexpr int NCH = NP / 16;
+    const int ch_lo = (NCH * sub) / 4, ch_hi = (NCH * (sub + 1)) / 4;
+    const uint32_t c2empty0 = rcx::map_cta(c2empty, 0);
+    uint8_t *stg_base = sST + warp * 2 * 1024;
+    uint32_t nst = 0;
+    int it = 0;
+    for (int tile = cl; tile < total; tile += ncl, ++it) {
+      const int pass = tile % a.passes, rest = tile / a.passes;
+      const int mp = rest % pairs, net = rest / pairs;
+      rcx::mbar_wait(c2full, it & 1);
+      rcx::mbar_wait(&bfull[it & 1], (it >> 1) & 1);
+      rcx::tc_fence_after();
+      const float *b2 = sB2 + (it & 1) * NP;
+      const int grow = mp * 256 + rank * 128 + q * 32;  // first global row of this warp's 32 rows
+      for (int cc = ch_lo; cc < ch_hi; cc += 2) {
+        uint32_t v[32];
+        const bool two = cc + 1 < ch_hi;
+        if (two)
+          tmem_ld32(tmem + tq + cc * 16, v);
+        else
+          rcx::tmem_ld16(tmem + tq + cc * 16, *reinterpret_cast<uint32_t(*)[16]>(v));
+        rcx::tmem_ld_wait();
+        if (cc + 2 >= ch_hi) {  // this warp's last acc columns are in registers: release the accumulator
+          rcx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1 && !two) break;
+          const int col = (cc + h) * 16;
+          const float4 *bb = reinterpret_cast<const float4 *>(b2 + col);
+          uint32_t pk[8];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 b = bb[j];
+            pk[2 * j] = gelu_bf16x2(cvt_bf16x2(__uint_as_float(v[16 * h + 4 * j]) + b.x,
+                                               __uint_as_float(v[16 * h + 4 * j + 1]) + b.y));
+            pk[2 * j + 1] = gelu_bf16x2(cvt_bf16x2(__uint_as_float(v[16 * h + 4 * j + 2]) + b.z,
+                                                   __uint_as_float(v[16 * h + 4 * j + 3]) + b.w));
+          }
+          uint8_t *stg = stg_base + (nst & 1) * 1024;  // [32 rows][32 B], 32-byte TMA swizzle
+          if (lane == 0) bulk_wait_read1();            // the store that last used this buffer has read it
+          __syncwarp();
+          *reinterpret_cast<uint4 *>(stg + lane * 32 + ((0 ^ ((lane >> 2) & 1)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4 *>(stg + lane * 32 + ((1 ^ ((lane >> 2) & 1)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&mapOut, stg, pass * NP + col, grow, net);
+            bulk_commit();
+          }
+          ++nst;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) rcx::mbar_arrive(&bempty[it & 1]);
+    }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
+  }
+  rcx::tc_fence_before();
+  rcx::cluster_sync();
+  if (warp == W_MMA) {
+    rcx::tc_fence_after();
+    rcx::tmem_dealloc_pair(tmem, 512);
+  }
+}
+
+template <int NP>
+int launch_l2_pair_t(const CUtensorMap &A, const CUtensorMap &Ba, const CUtensorMap &Bb, const CUtensorMap &Out,
+                     L2Args a, cudaStream_t s) {
+  constexpr size_t STAGE = ((128 * KC * 2 + (NP / 2) * KC * 2) + 1023) & ~(size_t)1023;
+  const size_t fixed = 1024 + NEPI * 2 * 1024 + 2 * NP * 4 + 512;
+  int stages = (int)((232448 - fixed) / STAGE);
+  if (stages > 8) stages = 8;
+  if (stages < 2) return rc_fail(RC_EUNSUPPORTED, "layer-2 GEMM: pass width %d does not fit", NP);
+  a.stages = stages;
+  const size_t smem = fixed + stages * STAGE;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(l2_pair_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    attr = true;
+  }
+  const int total = a.nets * (a.m_tiles / 2) * a.passes;
+  int clusters = mlp_num_sms() / 2;
+  if (clusters > total) clusters = total;
+  l2_pair_kernel<NP><<<2 * clusters, L2_THREADS, smem, s>>>(A, Ba, Bb, Out, a);
+  RC_LAUNCH_CHECK();
+  return RC_OK;
+}
+
+}  // namespace
+
+// pass width: the widest NP <= 400 (TMEM: one pass accumulator) that divides h2 into equal passes
+int l2_pass_width(int h2) {
+  for (int p = 1; p <= h2 / 16; ++p)
+    if (h2 % p == 0 && (h2 / p) % 16 == 0 && h2 / p <= 400 && (h2 / p <= 256 || (h2 / p / 2) % 8 == 0)) return h2 / p;
+  return 0;
+}
+
+int launch_l2_pair(int NP, const CUtensorMap &A, const CUtensorMap &Ba, const CUtensorMap &Bb, const CUtensorMap &Out,
+                   const L2Args &a, cudaStream_t s) {
+  ProfScope prof(RC_STAGE_L2, s);
+#define RC_L2P(np) \
+  if (NP == np) return launch_l2_pair_t<np>(A, Ba, Bb, Out, a, s);
+  RC_L2P(400)
+  RC_L2P(256)
+  RC_L2P(208)
+  RC_L2P(128)
+  RC_L2P(64)
+  RC_L2P(32)
+#undef RC_L2P
+  return rc_fail(RC_EUNSUPPORTED, "layer-2 GEMM: no instance for pass width %d", NP);
+}

@@ -27,10 +27,23 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t phase) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, p;\n}"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+// try_wait with a suspend-time hint: a waiting thread is parked by the hardware
+// (no issue slots spent spinning) until the phase completes or ~`ns` pass.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t *bar, uint32_t phase, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase), "r"(ns)
       : "memory");
   return ok != 0;
 }
@@ -46,6 +59,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
   if (mbar_try_wait(bar, phase)) return;
   const uint64_t t0 = global_ns();
   while (!mbar_try_wait(bar, phase)) {
+    if (global_ns() - t0 > 20000000000ull) __trap();
+  }
+}
+// the same for single-thread roles that wait most of the time (producer, MMA, store issuer)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t phase) {
+  if (mbar_try_wait(bar, phase)) return;
+  const uint64_t t0 = global_ns();
+  while (!mbar_try_wait_sleep(bar, phase, 100000u)) {
     if (global_ns() - t0 > 20000000000ull) __trap();
   }
 }

@@ -30,6 +30,11 @@ __global__ void k(int iters, uint32_t *out) {
       if (MODE == 2) v[i] = fma2(v[i], 0x3F803F80u, 0x00010001u);
       if (MODE == 3) v[i] = gelu2(v[i]);
       if (MODE == 4) f[i] = gelu1(f[i]);
+      if (MODE == 5) {  // fp32 accumulator pair -> cvt.rn.bf16x2 -> packed GELU (the epilogue's per-pair work)
+        uint32_t p; asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(f[i]), "f"(f[(i + 1) & 7]));
+        p = gelu2(p); f[i] = __uint_as_float(p) * 1e-3f + f[i];
+      }
+      if (MODE == 6) { uint32_t p; asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(f[i]), "f"(f[(i + 1) & 7])); f[i] = __uint_as_float(p) + f[i]; }
     }
   }
   uint32_t s = 0;
@@ -40,16 +45,16 @@ __global__ void k(int iters, uint32_t *out) {
 int main() {
   uint32_t *d; cudaMalloc(&d, 4);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const char *names[] = {"tanh.approx.bf16x2 (elements)", "tanh.approx.f32", "fma.rn.bf16x2 (elements)", "gelu bf16x2 (elements)", "gelu f32"};
-  for (int warps : {4, 8, 16}) {
-    for (int m = 0; m < 5; ++m) {
+  const char *names[] = {"tanh.approx.bf16x2 (elements)", "tanh.approx.f32", "fma.rn.bf16x2 (elements)", "gelu bf16x2 (elements)", "gelu f32", "cvt+gelu bf16x2 (elements)", "cvt.rn.bf16x2.f32 (elements)"};
+  for (int warps : {16}) {
+    for (int m = 0; m < 7; ++m) {
       int iters = 4096; dim3 g(148), b(32 * warps);
       auto launch = [&]() { switch (m) { case 0: k<0><<<g, b>>>(iters, d); break; case 1: k<1><<<g, b>>>(iters, d); break;
-        case 2: k<2><<<g, b>>>(iters, d); break; case 3: k<3><<<g, b>>>(iters, d); break; case 4: k<4><<<g, b>>>(iters, d); break; } };
+        case 2: k<2><<<g, b>>>(iters, d); break; case 3: k<3><<<g, b>>>(iters, d); break; case 4: k<4><<<g, b>>>(iters, d); break; case 5: k<5><<<g, b>>>(iters, d); break; case 6: k<6><<<g, b>>>(iters, d); break; } };
       launch(); cudaDeviceSynchronize();
       cudaEventRecord(e0); launch(); cudaEventRecord(e1); cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
-      double elems = 8.0 * iters * g.x * b.x * ((m == 0 || m == 2 || m == 3) ? 2 : 1);
+      double elems = 8.0 * iters * g.x * b.x * ((m == 0 || m == 2 || m == 3 || m == 5 || m == 6) ? 2 : 1);
       printf("warps/SM=%2d %-32s %8.1f Gelem/s = %6.1f elem/clk/SM @1.9GHz\n", warps, names[m], elems / ms / 1e6, elems / ms / 1e6 / 148 / 1.9);
     }
   }
