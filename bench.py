@@ -34,7 +34,7 @@ SUSTAINED = "bf16_tflops_sustained"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
@@ -64,46 +64,73 @@ def fp64_peak():
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock / throttle-reason sampler running during the timed region (B200_PROFILING.md
+    clocks line).  NVML polled from a thread every 5 ms (nvidia-smi's start-up latency would
+    miss most of a ~1 s timed region); falls back to nvidia-smi -lms if NVML is unavailable."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index):
         self.index = index
-        self.p = None
+        self.rows = []  # (sm_mhz, max_mhz, reasons bitmask)
+        self._stop = None
+
+    def _handle(self, nv):
+        """NVML handle of this process's CUDA device, matched by PCI bus id (CUDA and NVML
+        enumerate devices differently when CUDA_VISIBLE_DEVICES is set)."""
+        nv.nvmlInit()
+        want = None
+        try:
+            import torch
+            want = str(torch.cuda.get_device_properties(self.index).pci_bus_id).lower()
+        except Exception:
+            pass
+        n = nv.nvmlDeviceGetCount()
+        for i in range(n):
+            h = nv.nvmlDeviceGetHandleByIndex(i)
+            bid = nv.nvmlDeviceGetPciInfo(h).busId
+            bid = (bid.decode() if isinstance(bid, bytes) else str(bid)).lower()
+            if want and (bid.endswith(want) or want.endswith(bid[-12:])):
+                return h
+        return nv.nvmlDeviceGetHandleByIndex(self.index if self.index < n else 0)
 
     def __enter__(self):
+        import threading
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
-                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.p = None
+            import pynvml as nv
+            h = self._handle(nv)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        except Exception:
+            return self
+        self._stop = threading.Event()
+
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((float(sm), float(mx), int(r)))
+                except Exception:
+                    pass
+                time.sleep(0.005)
+
+        self._t = threading.Thread(target=loop, daemon=True)
+        self._t.start()
         return self
 
     def __exit__(self, *a):
-        self.rows = []
-        if self.p is None:
-            return
-        self.p.terminate()
-        out, _ = self.p.communicate(timeout=10)
-        for line in out.strip().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) >= 9:
-                self.rows.append(f)
+        if self._stop is not None:
+            self._stop.set()
+            self._t.join(timeout=2)
 
     def summary(self):
-        rows = getattr(self, "rows", [])
-        if not rows:
+        if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({k for r in self.rows for k, bit in self.REASONS.items() if r[2] & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": float(min(sm)), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(self.rows), "source": "NVML, 5 ms polling during the timed steps"}
 
 
 def local_cells(cfg, rank, world, strong):

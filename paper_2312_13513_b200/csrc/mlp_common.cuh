@@ -39,6 +39,15 @@ __device__ __forceinline__ uint32_t gelu_half_bf16x2(uint32_t y) {
   asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(y), "r"(th), "r"(y));
   return r;
 }
+// fp32 GELU (same tanh form, MUFU tanh.approx.f32): used where the activation
+// feeds an fp32 reduction directly (layer 3 -> the folded layer-4 dot)
+__device__ __forceinline__ float gelu_f32(float x) {
+  float t;
+  const float u = x * fmaf(0.0356774081f, x * x, 0.7978845608f);
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+  const float hx = 0.5f * x;
+  return fmaf(hx, t, hx);
+}
 __device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));

@@ -178,12 +178,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const float4 b = __ldg(bb + j);
             float4 w = __ldg(ww + j);
             if (!on) w = make_float4(0.f, 0.f, 0.f, 0.f);
+#ifdef L3_BF16_GELU
             const uint32_t p0 = gelu_bf16x2(cvt_bf16x2(__uint_as_float(v[c][4 * j]) + b.x, __uint_as_float(v[c][4 * j + 1]) + b.y));
             const uint32_t p1 = gelu_bf16x2(cvt_bf16x2(__uint_as_float(v[c][4 * j + 2]) + b.z, __uint_as_float(v[c][4 * j + 3]) + b.w));
             dot = fmaf(bf_lo(p0), w.x, dot);
             dot = fmaf(bf_hi(p0), w.y, dot);
             dot = fmaf(bf_lo(p1), w.z, dot);
             dot = fmaf(bf_hi(p1), w.w, dot);
+#else
+            // h3 never leaves the SM: GELU and the layer-4 dot stay in fp32
+            dot = fmaf(rcm::gelu_f32(__uint_as_float(v[c][4 * j]) + b.x), w.x, dot);
+            dot = fmaf(rcm::gelu_f32(__uint_as_float(v[c][4 * j + 1]) + b.y), w.y, dot);
+            dot = fmaf(rcm::gelu_f32(__uint_as_float(v[c][4 * j + 2]) + b.z), w.z, dot);
+            dot = fmaf(rcm::gelu_f32(__uint_as_float(v[c][4 * j + 3]) + b.w), w.w, dot);
+#endif
           }
         }
         g.opart[((size_t)net * g.n_tiles * 4 + n_blk * 4 + sub) * g.cap + m_blk * BM + q * 32 + lane] = dot;

@@ -2,7 +2,7 @@
 the C ABI (include/rc.h).  Gates (BASELINE.json north_star):
   fp64 thermo/transport (T, cp, rho, mu, lambda, D_k)  |g - o| <= 1e-10 |o|
   bf16 MLP output o ("relative 2e-2 of the output norm")   ||g - o|| / ||o|| <= 2e-2
-  bf16 wdot, qdot, sum qdot (derived, R17)        ||g - o|| / ||o|| <= 5e-2
+  bf16 wdot, qdot, sum qdot (SURVEY.md §8(c) gates)     ||g - o|| / ||o|| <= 2e-2
   T_max                                                 1e-10
   GPU wdot conserves mass and elements                  1e-12 of sum |wdot|
   sharded == unsharded                                  bitwise
@@ -18,8 +18,8 @@ pytestmark = pytest.mark.gpu
 
 FP64_TOL = 1e-10
 BF16_TOL = 2e-2        # on the MLP output o (north_star)
-BF16_DERIVED_TOL = 5e-2  # on wdot / qdot: bf16 weight rounding of the nets with the smallest |o|
-                         # (e.g. O2, |o| ~ 0.01 with random init) dominates wdot (R17)
+BF16_DERIVED_TOL = 2e-2  # on wdot / qdot / sum qdot: the same gate (SURVEY.md §8(c) "measured on o
+                         # and on wdot"); met since layer 3 + the folded layer 4 run in fp32 (R17)
 
 
 @pytest.fixture(scope="module", autouse=True)

@@ -13,8 +13,11 @@ timeout 900 python bench.py > $O/bench_$TAG.json 2> $O/bench_$TAG.err; echo "ben
 cat $O/bench_$TAG.json; tail -3 $O/bench_$TAG.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_$TAG.csv \
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "ncu list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 4 -c 3 \
-  -o $O/prof_gemm_$TAG -f python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_gemm_$TAG.log 2>&1; echo "ncu gemm rc=$?"
+for K in l2_pair_kernel l1_kernel l3_kernel; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 2 -c 1 \
+    -o $O/prof_${K}_$TAG -f python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_${K}_$TAG.log 2>&1
+  echo "ncu $K rc=$?"
+done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"thermo_kernel|transport_kernel|chem_epilogue|prologue" -s 2 -c 4 \
   -o $O/prof_fp64_$TAG -f python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_fp64_$TAG.log 2>&1; echo "ncu fp64 rc=$?"
-ls -la $O
+ls -la $O | tail -20
