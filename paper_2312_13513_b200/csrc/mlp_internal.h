@@ -23,6 +23,9 @@ int l2_pass_width(int h2);
 struct L2Args {
   int m_tiles, passes, nets, chunks, N, stages;
   const float *bias;       // [nets][N]
+  const float *w4;         // layer-3 mode (nullptr: layer 2): [nets][N], layer 4 folded into the epilogue
+  float *opart;            // layer-3 mode: [nets][passes*4][cap] partial dots
+  int cap;
 };
 int launch_l2_pair(int NP, const CUtensorMap &A, const CUtensorMap &Ba, const CUtensorMap &Bb, const CUtensorMap &Out,
                    const L2Args &a, cudaStream_t s);

@@ -18,6 +18,17 @@
 //
 // Warps: 0..15 epilogue, 16 TMA producer, 17 MMA issuer (the scheduler favours
 // higher warp ids, so the single-thread roles get the highest ids).
+//
+// DOT = true runs layer 3 (800 -> 400) with layer 4 folded in: the epilogue
+// computes GELU(acc + b3) . w4 in fp32 over each warp's columns and writes one
+// partial per (row, column quarter); the chem epilogue sums the four.
+//
+// The accumulator is drained after the last K chunk (MUFU-bound, ~3 K clk per
+// tile) while the tensor pipe idles.  Overlapping the drain with the next
+// tile's MMAs (piece 2 trailing piece 1 by D chunks) measured slower: an MMA
+// chain into one accumulator runs at one K16 step per ~220 clk whatever N
+// (tools/microbench/mma_rate.cu), so the full rate needs ~400+ accumulator
+// columns in flight, which leaves no TMEM to drain from.
 #include <cuda_bf16.h>
 
 #include "mlp_common.cuh"
@@ -39,7 +50,7 @@ using rcm::tma_store_3d;
 using rcm::tmem_ld32;
 __device__ __forceinline__ uint64_t desc_sw128(const void *smem) { return rcm::desc_sw<128>(smem); }
 
-template <int NP>
+template <int NP, bool DOT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     l2_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBa,
                    const __grid_constant__ CUtensorMap mapBb, const __grid_constant__ CUtensorMap mapOut, L2Args a) {
@@ -57,8 +68,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
   const int S = a.stages;
   uint8_t *sW = smem;                                   // S x [A tile | B half]
   uint8_t *sST = sW + S * STAGE;                        // NEPI x 2 x 1 KB store staging
-  float *sB2 = reinterpret_cast<float *>(sST + NEPI * 2 * 1024);
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sB2 + 2 * NP);
+  float *sB2 = reinterpret_cast<float *>(sST + NEPI * 2 * 1024);  // 2 x [b | w4 (DOT)] slices
+  constexpr int VEC = DOT ? 2 * NP : NP;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sB2 + 2 * VEC);
   uint64_t *full = bar, *empty = full + S, *c2full = empty + S, *c2empty = c2full + 1, *bfull = c2empty + 1,
            *bempty = bfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bempty + 2);
@@ -70,7 +82,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     rcx::prefetch_tmap(&mapA);
     rcx::prefetch_tmap(&mapBa);
     if (P2 > 0) rcx::prefetch_tmap(&mapBb);
-    rcx::prefetch_tmap(&mapOut);
+    if (!DOT) rcx::prefetch_tmap(&mapOut);
     for (int s = 0; s < S; ++s) { rcx::mbar_init(&full[s], 2); rcx::mbar_init(&empty[s], 1); }
     rcx::mbar_init(c2full, 1);
     rcx::mbar_init(c2empty, 2 * NEPI);
@@ -98,8 +110,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
         const int mp = rest % pairs, net = rest / pairs;
         const int zb = it & 1;
         rcx::mbar_wait(&bempty[zb], ((it >> 1) & 1) ^ 1);  // b2 slice for this CTA's drain
-        rcx::mbar_arrive_expect_tx(&bfull[zb], NP * 4);
-        rcx::bulk_g2s(sB2 + zb * NP, a.bias + (size_t)net * a.N + pass * NP, NP * 4, &bfull[zb]);
+        rcx::mbar_arrive_expect_tx(&bfull[zb], VEC * 4);
+        rcx::bulk_g2s(sB2 + zb * VEC, a.bias + (size_t)net * a.N + pass * NP, NP * 4, &bfull[zb]);
+        if (DOT) rcx::bulk_g2s(sB2 + zb * VEC + NP, a.w4 + (size_t)net * a.N + pass * NP, NP * 4, &bfull[zb]);
         for (int c = 0; c < C; ++c) {
           rcx::mbar_wait(&empty[s], ph ^ 1);
           rcx::mbar_arrive_expect_tx_cluster(full0 + s * 8, A_BYTES + B_BYTES);
@@ -154,53 +167,93 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
       rcx::mbar_wait(c2full, it & 1);
       rcx::mbar_wait(&bfull[it & 1], (it >> 1) & 1);
       rcx::tc_fence_after();
-      const float *b2 = sB2 + (it & 1) * NP;
+      if (ch_lo == ch_hi) {  // narrow pass (NP < 64): this warp owns no columns but must still release
+        rcx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
+      }
+      const float *b2 = sB2 + (it & 1) * VEC;
       const int grow = mp * 256 + rank * 128 + q * 32;  // first global row of this warp's 32 rows
-      for (int cc = ch_lo; cc < ch_hi; cc += 2) {
-        uint32_t v[32];
-        const bool two = cc + 1 < ch_hi;
-        if (two)
-          tmem_ld32(tmem + tq + cc * 16, v);
-        else
-          rcx::tmem_ld16(tmem + tq + cc * 16, *reinterpret_cast<uint32_t(*)[16]>(v));
-        rcx::tmem_ld_wait();
-        if (cc + 2 >= ch_hi) {  // this warp's last acc columns are in registers: release the accumulator
-          rcx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
+      if constexpr (DOT) {
+        const float *w4s = b2 + NP;
+        float dot = 0.f;
+        for (int cc = ch_lo; cc < ch_hi; cc += 2) {
+          uint32_t v[32];
+          const bool two = cc + 1 < ch_hi;
+          if (two)
+            tmem_ld32(tmem + tq + cc * 16, v);
+          else
+            rcx::tmem_ld16(tmem + tq + cc * 16, *reinterpret_cast<uint32_t(*)[16]>(v));
+          rcx::tmem_ld_wait();
+          if (cc + 2 >= ch_hi) {  // this warp's last acc columns are in registers: release the accumulator
+            rcx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !two) break;
+            const int col = (cc + h) * 16;
+            const float4 *bb = reinterpret_cast<const float4 *>(b2 + col);
+            const float4 *ww = reinterpret_cast<const float4 *>(w4s + col);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 b = bb[j], w = ww[j];
+              dot = fmaf(rcm::gelu_f32(__uint_as_float(v[16 * h + 4 * j]) + b.x), w.x, dot);
+              dot = fmaf(rcm::gelu_f32(__uint_as_float(v[16 * h + 4 * j + 1]) + b.y), w.y, dot);
+              dot = fmaf(rcm::gelu_f32(__uint_as_float(v[16 * h + 4 * j + 2]) + b.z), w.z, dot);
+              dot = fmaf(rcm::gelu_f32(__uint_as_float(v[16 * h + 4 * j + 3]) + b.w), w.w, dot);
+            }
+          }
         }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (h == 1 && !two) break;
-          const int col = (cc + h) * 16;
-          const float4 *bb = reinterpret_cast<const float4 *>(b2 + col);
-          uint32_t pk[8];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 b = bb[j];
-            pk[2 * j] = gelu_bf16x2(cvt_bf16x2(__uint_as_float(v[16 * h + 4 * j]) + b.x,
-                                               __uint_as_float(v[16 * h + 4 * j + 1]) + b.y));
-            pk[2 * j + 1] = gelu_bf16x2(cvt_bf16x2(__uint_as_float(v[16 * h + 4 * j + 2]) + b.z,
-                                                   __uint_as_float(v[16 * h + 4 * j + 3]) + b.w));
+        a.opart[((size_t)(net * a.passes + pass) * 4 + sub) * a.cap + grow + lane] = dot;
+      } else {
+        for (int cc = ch_lo; cc < ch_hi; cc += 2) {
+          uint32_t v[32];
+          const bool two = cc + 1 < ch_hi;
+          if (two)
+            tmem_ld32(tmem + tq + cc * 16, v);
+          else
+            rcx::tmem_ld16(tmem + tq + cc * 16, *reinterpret_cast<uint32_t(*)[16]>(v));
+          rcx::tmem_ld_wait();
+          if (cc + 2 >= ch_hi) {  // this warp's last acc columns are in registers: release the accumulator
+            rcx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
           }
-          uint8_t *stg = stg_base + (nst & 1) * 1024;  // [32 rows][32 B], 32-byte TMA swizzle
-          if (lane == 0) bulk_wait_read1();            // the store that last used this buffer has read it
-          __syncwarp();
-          *reinterpret_cast<uint4 *>(stg + lane * 32 + ((0 ^ ((lane >> 2) & 1)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          *reinterpret_cast<uint4 *>(stg + lane * 32 + ((1 ^ ((lane >> 2) & 1)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_3d(&mapOut, stg, pass * NP + col, grow, net);
-            bulk_commit();
+  #pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !two) break;
+            const int col = (cc + h) * 16;
+            const float4 *bb = reinterpret_cast<const float4 *>(b2 + col);
+            uint32_t pk[8];
+  #pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 b = bb[j];
+              pk[2 * j] = gelu_bf16x2(cvt_bf16x2(__uint_as_float(v[16 * h + 4 * j]) + b.x,
+                                                 __uint_as_float(v[16 * h + 4 * j + 1]) + b.y));
+              pk[2 * j + 1] = gelu_bf16x2(cvt_bf16x2(__uint_as_float(v[16 * h + 4 * j + 2]) + b.z,
+                                                     __uint_as_float(v[16 * h + 4 * j + 3]) + b.w));
+            }
+            uint8_t *stg = stg_base + (nst & 1) * 1024;  // [32 rows][32 B], 32-byte TMA swizzle
+            if (lane == 0) bulk_wait_read1();            // the store that last used this buffer has read it
+            __syncwarp();
+            *reinterpret_cast<uint4 *>(stg + lane * 32 + ((0 ^ ((lane >> 2) & 1)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            *reinterpret_cast<uint4 *>(stg + lane * 32 + ((1 ^ ((lane >> 2) & 1)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(&mapOut, stg, pass * NP + col, grow, net);
+              bulk_commit();
+            }
+            ++nst;
           }
-          ++nst;
         }
       }
       __syncwarp();
       if (lane == 0) rcx::mbar_arrive(&bempty[it & 1]);
     }
-    if (lane == 0) bulk_wait_all();
+    if (!DOT && lane == 0) bulk_wait_all();
     __syncwarp();
   }
   rcx::tc_fence_before();
@@ -211,11 +264,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
   }
 }
 
-template <int NP>
+template <int NP, bool DOT>
 int launch_l2_pair_t(const CUtensorMap &A, const CUtensorMap &Ba, const CUtensorMap &Bb, const CUtensorMap &Out,
                      L2Args a, cudaStream_t s) {
   constexpr size_t STAGE = ((128 * KC * 2 + (NP / 2) * KC * 2) + 1023) & ~(size_t)1023;
-  const size_t fixed = 1024 + NEPI * 2 * 1024 + 2 * NP * 4 + 512;
+  const size_t fixed = 1024 + NEPI * 2 * 1024 + 2 * (DOT ? 2 : 1) * NP * 4 + 512;
   int stages = (int)((232448 - fixed) / STAGE);
   if (stages > 8) stages = 8;
   if (stages < 2) return rc_fail(RC_EUNSUPPORTED, "layer-2 GEMM: pass width %d does not fit", NP);
@@ -223,13 +276,13 @@ int launch_l2_pair_t(const CUtensorMap &A, const CUtensorMap &Ba, const CUtensor
   const size_t smem = fixed + stages * STAGE;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(l2_pair_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaFuncSetAttribute(l2_pair_kernel<NP, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     attr = true;
   }
   const int total = a.nets * (a.m_tiles / 2) * a.passes;
   int clusters = mlp_num_sms() / 2;
   if (clusters > total) clusters = total;
-  l2_pair_kernel<NP><<<2 * clusters, L2_THREADS, smem, s>>>(A, Ba, Bb, Out, a);
+  l2_pair_kernel<NP, DOT><<<2 * clusters, L2_THREADS, smem, s>>>(A, Ba, Bb, Out, a);
   RC_LAUNCH_CHECK();
   return RC_OK;
 }
@@ -245,15 +298,18 @@ int l2_pass_width(int h2) {
 
 int launch_l2_pair(int NP, const CUtensorMap &A, const CUtensorMap &Ba, const CUtensorMap &Bb, const CUtensorMap &Out,
                    const L2Args &a, cudaStream_t s) {
-  ProfScope prof(RC_STAGE_L2, s);
-#define RC_L2P(np) \
-  if (NP == np) return launch_l2_pair_t<np>(A, Ba, Bb, Out, a, s);
+  ProfScope prof(a.w4 ? RC_STAGE_L3 : RC_STAGE_L2, s);
+#define RC_L2P(np)                                                                     \
+  if (NP == np)                                                                        \
+    return a.w4 ? launch_l2_pair_t<np, true>(A, Ba, Bb, Out, a, s)                      \
+                : launch_l2_pair_t<np, false>(A, Ba, Bb, Out, a, s);
   RC_L2P(400)
   RC_L2P(256)
   RC_L2P(208)
   RC_L2P(128)
   RC_L2P(64)
   RC_L2P(32)
+  RC_L2P(16)
 #undef RC_L2P
   return rc_fail(RC_EUNSUPPORTED, "layer-2 GEMM: no instance for pass width %d", NP);
 }

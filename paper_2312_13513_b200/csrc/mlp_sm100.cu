@@ -11,13 +11,11 @@
 //   prologue      T,p,Y (fp64 SoA) -> z [cap][kz] bf16 (K-major A operand, two 1-columns for b1)
 //   l1_kernel     h1 = GELU(z W1^T)                  [nets][cap][h1] bf16   (mlp_l1_sm100.cu)
 //   l2_pair       h2 = GELU(h1 W2^T + b2)            [nets][cap][h2] bf16   (mlp_l2_sm100.cu)
-//   l3_kernel     o_part = GELU(h2 W3^T + b3) . w4   (layer 4 folded into the epilogue)
+//   l2_pair<dot>  o_part = GELU(h2 W3^T + b3) . w4   (layer 3, layer 4 folded into the epilogue)
 //   chem_epilogue o = b4 + sum(o_part) -> dY -> P dY -> wdot, qdot, sum qdot partials
-// The layer-3 GEMM is a persistent, warp-specialised kernel: one warp issues
-// TMA loads into a multi-stage shared-memory ring (128-byte swizzle), one
-// issues tcgen05.mma (M=128, N=BN, K=16) into a double-buffered TMEM
-// accumulator, sixteen drain TMEM with tcgen05.ld, add b3, apply GELU and
-// reduce against w4.
+// The GEMMs are persistent warp-specialised tcgen05 kernels (TMA producer warp,
+// single-thread MMA issuer, sixteen TMEM-draining epilogue warps); this file
+// holds the prologue, the fp64 chem epilogue, the weight upload and the driver.
 #include <cuda_bf16.h>
 
 #include <cmath>
@@ -34,176 +32,9 @@ namespace {
 
 constexpr int BM = 128;       // UMMA M (one CTA, cta_group::1)
 constexpr int BK = 64;        // K elements per pipeline stage (128 B of bf16 = one swizzle row)
-constexpr int GEMM_NEPI = 16;                      // epilogue warps: 4 per TMEM lane quadrant
-constexpr int GEMM_THREADS = 32 * GEMM_NEPI + 64;  // + TMA producer warp + MMA issuer warp
 constexpr int MAX_CAP = 32768;     // cells per chunk (activation working set)
 constexpr int QPART_BLOCKS = 148 * 4;
 
-using rcm::bf_hi;
-using rcm::bf_lo;
-using rcm::cvt_bf16x2;
-using rcm::desc_sw;
-using rcm::gelu_bf16x2;
-
-struct GemmArgs {
-  int m_tiles, n_tiles, nets, k_blocks, a_shared, N, cap, stages;
-  const float *bias;   // [nets][N] or nullptr (bias folded into the MMA)
-  const float *w4;     // MODE 1: [nets][N]
-  float *opart;        // MODE 1: [nets][n_tiles*4][cap]
-};
-
-// Persistent warp-specialised tcgen05 GEMM, M = 128 per CTA, N tile BN
-// (runtime-narrower last tile), K chunks of 64, double-buffered TMEM
-// accumulator so the epilogue of tile i overlaps the MMAs of tile i+1.
-// opart = GELU(A B^T + bias) . w4 per row and column quarter (layer 3 with
-// layer 4 folded in).
-template <int BN, int KB = BK>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
-    l3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, GemmArgs g) {
-  static_assert(KB == 16 || KB == 32 || KB == 64, "K atom: 32/64/128-byte swizzle rows");
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t base_u32 = rcx::smem_u32(smem_raw);
-  uint8_t *smem = smem_raw + (((base_u32 + 1023u) & ~1023u) - base_u32);
-  constexpr uint32_t A_BYTES = BM * KB * 2, B_BYTES = BN * KB * 2;
-  constexpr int W_TMA = GEMM_NEPI, W_MMA = GEMM_NEPI + 1;
-  const int S = g.stages;
-  uint8_t *sA = smem, *sB = smem + S * A_BYTES;
-  uint64_t *full = reinterpret_cast<uint64_t *>(sB + S * B_BYTES);
-  uint64_t *empty = full + S, *tfull = empty + S, *tempty = tfull + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-  constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == W_TMA && lane == 0) {
-    rcx::prefetch_tmap(&mapA);
-    rcx::prefetch_tmap(&mapB);
-    for (int s = 0; s < S; ++s) {
-      rcx::mbar_init(&full[s], 1);
-      rcx::mbar_init(&empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      rcx::mbar_init(&tfull[a], 1);
-      rcx::mbar_init(&tempty[a], GEMM_NEPI);
-    }
-    rcx::fence_mbar_init();
-  }
-  if (warp == W_MMA) rcx::tmem_alloc(tmem_slot, TMEM_COLS);
-  rcx::tc_fence_before();
-  __syncthreads();
-  rcx::tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  const int total = g.m_tiles * g.n_tiles * g.nets;
-
-  if (warp == W_TMA) {
-    if (lane == 0) {  // ---------------- TMA producer
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        const int n_blk = tile % g.n_tiles, rest = tile / g.n_tiles;
-        const int m_blk = rest % g.m_tiles, net = rest / g.m_tiles;
-        for (int kb = 0; kb < g.k_blocks; ++kb) {
-          rcx::mbar_wait(&empty[stage], phase ^ 1);
-          rcx::mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
-          rcx::tma_load_3d(sA + stage * A_BYTES, &mapA, &full[stage], kb * KB, m_blk * BM, g.a_shared ? 0 : net);
-          rcx::tma_load_3d(sB + stage * B_BYTES, &mapB, &full[stage], kb * KB, n_blk * BN, net);
-          if (++stage == S) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == W_MMA) {
-    if (lane == 0) {  // ---------------- MMA issuer (single thread)
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
-        const int n_blk = tile % g.n_tiles;
-        const int n_eff = min(BN, g.N - n_blk * BN);  // ragged last tile: multiple of 16
-        const uint32_t idesc = rcx::make_idesc(1u, BM, (uint32_t)n_eff);
-        const int as = it & 1;
-        const uint32_t aphase = (it >> 1) & 1;
-        rcx::mbar_wait(&tempty[as], aphase ^ 1);
-        rcx::tc_fence_after();
-        const uint32_t d = tmem_base + as * BN;
-        for (int kb = 0; kb < g.k_blocks; ++kb) {
-          rcx::mbar_wait(&full[stage], phase);
-          rcx::tc_fence_after();
-          const uint64_t ad = desc_sw<KB * 2>(sA + stage * A_BYTES);
-          const uint64_t bd = desc_sw<KB * 2>(sB + stage * B_BYTES);
-#pragma unroll
-          for (int k = 0; k < KB / 16; ++k)
-            rcx::mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-          rcx::mma_commit(&empty[stage]);
-          if (++stage == S) { stage = 0; phase ^= 1; }
-        }
-        rcx::mma_commit(&tfull[as]);
-      }
-    }
-  } else {  // ---------------- epilogue warps 0..15: four per TMEM lane quadrant, each a quarter of the columns
-    const int q = warp & 3;     // TMEM lane quadrant this warp may access
-    const int sub = warp >> 2;  // column quarter 0..3
-    constexpr int MAXC = (BN / 16 + 3) / 4;  // 16-column chunks per warp (<= 4 for BN <= 256)
-    int it = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
-      const int n_blk = tile % g.n_tiles, rest = tile / g.n_tiles;
-      const int m_blk = rest % g.m_tiles, net = rest / g.m_tiles;
-      const int as = it & 1;
-      const uint32_t aphase = (it >> 1) & 1;
-      const int NCH = min(BN, g.N - n_blk * BN) / 16;
-      const int ch_lo = (NCH * sub) / 4, nch = (NCH * (sub + 1)) / 4 - ch_lo;  // warp-uniform
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + ch_lo * 16;
-      rcx::mbar_wait(&tfull[as], aphase);
-      rcx::tc_fence_after();
-      // all of this warp's accumulator columns -> registers, one wait, release the TMEM buffer.
-      // Always MAXC chunks (branch-free, so the GELU chains of all chunks interleave); chunks past
-      // this warp's range read valid but unused TMEM columns and are never stored.
-      uint32_t v[MAXC][16];
-#pragma unroll
-      for (int c = 0; c < MAXC; ++c) rcx::tmem_ld16(tbase + c * 16, v[c]);
-      rcx::tmem_ld_wait();
-      rcx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) rcx::mbar_arrive(&tempty[as]);
-      const size_t col0 = (size_t)net * g.N + n_blk * BN + ch_lo * 16;
-      {
-        // GELU(acc + b3) . w4 over this warp's columns (layer 4 folded into layer 3)
-        float dot = 0.f;
-#pragma unroll
-        for (int c = 0; c < MAXC; ++c) {
-          // chunks past this warp's range contribute with weight 0
-          const bool on = c < nch;
-          const float4 *bb = reinterpret_cast<const float4 *>(g.bias + col0 + (on ? c * 16 : 0));
-          const float4 *ww = reinterpret_cast<const float4 *>(g.w4 + col0 + (on ? c * 16 : 0));
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 b = __ldg(bb + j);
-            float4 w = __ldg(ww + j);
-            if (!on) w = make_float4(0.f, 0.f, 0.f, 0.f);
-#ifdef L3_BF16_GELU
-            const uint32_t p0 = gelu_bf16x2(cvt_bf16x2(__uint_as_float(v[c][4 * j]) + b.x, __uint_as_float(v[c][4 * j + 1]) + b.y));
-            const uint32_t p1 = gelu_bf16x2(cvt_bf16x2(__uint_as_float(v[c][4 * j + 2]) + b.z, __uint_as_float(v[c][4 * j + 3]) + b.w));
-            dot = fmaf(bf_lo(p0), w.x, dot);
-            dot = fmaf(bf_hi(p0), w.y, dot);
-            dot = fmaf(bf_lo(p1), w.z, dot);
-            dot = fmaf(bf_hi(p1), w.w, dot);
-#else
-            // h3 never leaves the SM: GELU and the layer-4 dot stay in fp32
-            dot = fmaf(rcm::gelu_f32(__uint_as_float(v[c][4 * j]) + b.x), w.x, dot);
-            dot = fmaf(rcm::gelu_f32(__uint_as_float(v[c][4 * j + 1]) + b.y), w.y, dot);
-            dot = fmaf(rcm::gelu_f32(__uint_as_float(v[c][4 * j + 2]) + b.z), w.z, dot);
-            dot = fmaf(rcm::gelu_f32(__uint_as_float(v[c][4 * j + 3]) + b.w), w.w, dot);
-#endif
-          }
-        }
-        g.opart[((size_t)net * g.n_tiles * 4 + n_blk * 4 + sub) * g.cap + m_blk * BM + q * 32 + lane] = dot;
-      }
-    }
-  }
-  __syncthreads();
-  if (warp == W_MMA) {
-    rcx::tc_fence_after();
-    rcx::tmem_dealloc(tmem_base, TMEM_COLS);
-  }
-}
 
 // ------------------------------------------------------------------ prologue (a3)
 struct ProArgs {
@@ -432,17 +263,6 @@ int make_map(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint64_
 // (the UMMA N granularity); the last tile may be narrower (runtime N in the
 // instruction descriptor, TMA zero-fills the rows past N).  Wide tiles keep the
 // shared-memory operand traffic per MMA under the 128 B/clk SMEM port.
-int pick_bn(int N) {
-  if (N % 16) return 0;
-  const int nt = (N + 207) / 208;
-  int bn = ((N + nt - 1) / nt + 15) / 16 * 16;
-  const int c[] = {16, 32, 48, 64, 96, 128, 160, 208};
-  for (int b : c)
-    if (b >= bn) return b;
-  return 0;
-}
-int n_tiles_of(int N) { return (N + pick_bn(N) - 1) / pick_bn(N); }
-
 }  // namespace
 int mlp_num_sms() {
   static int n = 0;
@@ -456,47 +276,6 @@ int mlp_num_sms() {
 }
 namespace {
 int num_sms() { return mlp_num_sms(); }
-
-template <int BN>
-int launch_l3_t(const CUtensorMap &A, const CUtensorMap &B, GemmArgs g, cudaStream_t s) {
-  const size_t stage_bytes = (size_t)BM * BK * 2 + (size_t)BN * BK * 2;
-  const size_t fixed = 1024 + 256;
-  int stages = (int)((232448 - fixed) / stage_bytes);
-  if (stages > 8) stages = 8;
-  g.stages = stages;
-  const size_t smem = fixed + stages * stage_bytes;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(l3_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    attr_set = true;
-  }
-  const int total = g.m_tiles * g.n_tiles * g.nets;
-  int grid = total < num_sms() ? total : num_sms();
-  ProfScope prof(RC_STAGE_L3, s);
-  l3_kernel<BN><<<grid, GEMM_THREADS, smem, s>>>(A, B, g);
-  RC_LAUNCH_CHECK();
-  return RC_OK;
-}
-
-// layer 3 (+ layer 4 folded into its epilogue)
-int launch_l3(int BN, const CUtensorMap &A, const CUtensorMap &B, const GemmArgs &g, cudaStream_t s) {
-#define RC_GEMM_CASE(bn) \
-  case bn:               \
-    return launch_l3_t<bn>(A, B, g, s);
-  switch (BN) {
-    RC_GEMM_CASE(16)
-    RC_GEMM_CASE(32)
-    RC_GEMM_CASE(48)
-    RC_GEMM_CASE(64)
-    RC_GEMM_CASE(96)
-    RC_GEMM_CASE(128)
-    RC_GEMM_CASE(160)
-    RC_GEMM_CASE(208)
-    default:
-      return rc_fail(RC_EUNSUPPORTED, "no layer-3 GEMM tile for BN=%d", BN);
-  }
-#undef RC_GEMM_CASE
-}
 
 struct WsLayout {
   size_t z, h1, h2, opart, qpart, total;
@@ -512,7 +291,7 @@ WsLayout ws_layout(const rc_mlp *n, int cap) {
   L.z = o; o = al(o + (size_t)cap * n->kpad1 * 2);
   L.h1 = o; o = al(o + (size_t)n->n_nets * cap * n->h1 * 2);
   L.h2 = o; o = al(o + (size_t)n->n_nets * cap * n->h2 * 2);
-  const int np3 = 4 * n_tiles_of(n->h3);
+  const int np3 = 4 * (n->h3 / l2_pass_width(n->h3));  // partial dots per row: 4 column quarters per pass
   L.opart = o; o = al(o + (size_t)n->n_nets * np3 * cap * 4);
   L.total = o;
   return L;
@@ -537,7 +316,7 @@ size_t chem_workspace_bytes(const rc_mech *, const rc_mlp *n, int64_t ncells) {
 
 int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
   if (n->precision != RC_BF16) return rc_fail(RC_EUNSUPPORTED, "TF32 MLP variant not built yet");
-  if (n->h1 % 64 || !l2_pass_width(n->h2) || !pick_bn(n->h3))
+  if (n->h1 % 64 || !l2_pass_width(n->h2) || !l2_pass_width(n->h3))
     return rc_fail(RC_EUNSUPPORTED, "hidden widths (%d,%d,%d) not supported by the fused kernels", n->h1, n->h2, n->h3);
   const int nets = n->n_nets, din = n->d_in, h1 = n->h1, h2 = n->h2, h3 = n->h3, kp = n->kpad1;
   const size_t P = (size_t)h1 * din + h1 + (size_t)h2 * h1 + h2 + (size_t)h3 * h2 + h3 + h3 + 1;
@@ -604,16 +383,18 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   auto *opart = reinterpret_cast<float *>(w + L.opart);
   auto *qpart = reinterpret_cast<double *>(w + L.qpart);
   const int nets = n->n_nets;
-  const int bn1 = l1_tile_n(), bn3 = pick_bn(n->h3), NP = l2_pass_width(n->h2), KZ = n->kpad1;
+  const int bn1 = l1_tile_n(), NP = l2_pass_width(n->h2), NP3 = l2_pass_width(n->h3), KZ = n->kpad1;
   const int P1 = NP > 256 ? 256 : NP, P2 = NP - P1;
-  CUtensorMap mz, mh1, mh1st, mh2, mh2st, mw1, mw2a, mw2b, mw3;
+  const int Q1 = NP3 > 256 ? 256 : NP3, Q2 = NP3 - Q1;
+  CUtensorMap mz, mh1, mh1st, mh2, mh2st, mw1, mw2a, mw2b, mw3a, mw3b;
   int rc;
   if ((rc = make_map(&mz, z, KZ, cap, 1, BM, KZ)) || (rc = make_map(&mw1, n->d_W1, KZ, n->h1, nets, l1_box_rows(), KZ)) ||
       (rc = make_map(&mh1, h1, n->h1, cap, nets, BM)) || (rc = make_map(&mh1st, h1, n->h1, cap, nets, 32)) ||
       (rc = make_map(&mw2a, n->d_W2, n->h1, n->h2, nets, P1 / 2)) ||
       (rc = make_map(&mw2b, n->d_W2, n->h1, n->h2, nets, P2 > 0 ? P2 / 2 : P1 / 2)) ||
       (rc = make_map(&mh2, h2, n->h2, cap, nets, BM)) || (rc = make_map(&mh2st, h2, n->h2, cap, nets, 32, 16)) ||
-      (rc = make_map(&mw3, n->d_W3, n->h2, n->h3, nets, bn3)))
+      (rc = make_map(&mw3a, n->d_W3, n->h2, n->h3, nets, Q1 / 2)) ||
+      (rc = make_map(&mw3b, n->d_W3, n->h2, n->h3, nets, Q2 > 0 ? Q2 / 2 : Q1 / 2)))
     return rc;
   RC_CUDA_TRY(cudaMemsetAsync(qpart, 0, QPART_BLOCKS * 8, s));
   int64_t launches = 1;
@@ -631,11 +412,12 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
     L1Args g1{mt, (n->h1 + bn1 - 1) / bn1, nets, n->h1, 0, cap, h1};
     if ((rc = launch_l1(KZ, mz, mw1, mh1st, g1, s))) return rc;
     // layer 2: h2 = GELU(h1 W2^T + b2), CTA-pair GEMM
-    L2Args la{mt, n->h2 / NP, nets, n->h1 / 64, n->h2, 0, n->d_b2};
+    L2Args la{mt, n->h2 / NP, nets, n->h1 / 64, n->h2, 0, n->d_b2, nullptr, nullptr, cap};
     if ((rc = launch_l2_pair(NP, mh1, mw2a, mw2b, mh2st, la, s))) return rc;
-    GemmArgs g3{mt, n_tiles_of(n->h3), nets, (n->h2 + BK - 1) / BK, 0, n->h3, cap, 0, n->d_b3, n->d_w4, opart};
-    if ((rc = launch_l3(bn3, mh2, mw3, g3, s))) return rc;
-    EpiArgs ea{c0, rows, cap, nets, 4 * n_tiles_of(n->h3), n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt, opart,
+    // layer 3 + folded layer 4: the same CTA-pair GEMM with the dot epilogue (K = h2, zero-filled to 64s)
+    L2Args l3{mt, n->h3 / NP3, nets, (n->h2 + 63) / 64, n->h3, 0, n->d_b3, n->d_w4, opart, cap};
+    if ((rc = launch_l2_pair(NP3, mh2, mw3a, mw3b, mh2st, l3, s))) return rc;
+    EpiArgs ea{c0, rows, cap, nets, 4 * (n->h3 / NP3), n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt, opart,
                n->d_b4, n->d_ymean, n->d_ystd, m->d_P, m->d_thermo, n->d_species, qpart};
     const size_t esm = (size_t)ThermoSeg::size(m->ns) * 8 + (size_t)((m->ns * m->ns + 1) & ~1) * 8;
     int eblocks = (rows + 255) / 256;

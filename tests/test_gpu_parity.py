@@ -106,6 +106,18 @@ def test_full_size_sampled(cfg):
     assert np.all(np.abs(g["wdot"].sum(axis=0)) <= 1e-12 * tot)
 
 
+def test_small_mlp_many_tiles_per_cta():
+    """C1's narrow MLP (64/32/16: pass widths below one 64-column block) on 65,536 C2
+    cells, so every persistent CTA pair runs several tiles (accumulator reuse, warps
+    with no columns still releasing the accumulator); every cell checked."""
+    c = inputs("C2", begin=0, end=65536)
+    o = run_oracle("C1", c)
+    g = Gpu("C1").run(c)
+    check_fp64(g, o)
+    eo, ew, eq = check_chem(g, o, mech("h2_9sp"))
+    print(f"small MLP x 65536 cells bf16 errors: o {eo:.2e} wdot {ew:.2e} qdot {eq:.2e}")
+
+
 def test_ch4_paper_shape_sample():
     """C4 (CH4/air, 20 species, 19 nets, d_in 22): parity on a hashed sample."""
     cols = _sample("C4", 256)

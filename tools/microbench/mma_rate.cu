@@ -76,7 +76,7 @@ int main() {
   cudaFuncSetAttribute(mma_loop<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(mma_loop<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  struct C { int pair, n1, n2, l1; } cs[] = {{1, 256, 144, 0}, {1, 256, 144, 11}, {1, 256, 144, 13}, {1, 256, 144, 21}, {1, 256, 144, 23}, {1, 256, 144, 32}, {1, 256, 144, 34}, {1, 256, 144, 1}};
+  struct C { int pair, n1, n2, l1; } cs[] = {{1, 256, 144, 0}, {1, 256, 0, 0}, {1, 144, 0, 0}, {1, 128, 128, 0}, {1, 128, 0, 0}, {1, 256, 144, 11}, {1, 256, 144, 21}, {1, 256, 0, 11}};
   for (auto c : cs) {
     int iters = 2000;
     cudaLaunchConfig_t cfg = {};
