@@ -23,8 +23,11 @@
 // computes GELU(acc + b3) . w4 in fp32 over each warp's columns and writes one
 // partial per (row, column quarter); the chem epilogue sums the four.
 //
-// The accumulator is drained after the last K chunk (MUFU-bound, ~3 K clk per
-// tile) while the tensor pipe idles.  Overlapping the drain with the next
+// The accumulator is drained in two phases: each warp first copies all its
+// columns out of TMEM as 16-bit (acc + bias) pairs (no MUFU work, ~1 K clk)
+// and releases it, then applies GELU and stores while the next tile's MMAs run
+// (tools/l2trace.py: releasing after the GELU of all but the last columns kept
+// the tensor pipe idle ~7 K of ~27 K clk per layer-2 tile).  Overlapping the drain with the next
 // tile's MMAs (piece 2 trailing piece 1 by D chunks) measured slower: an MMA
 // chain into one accumulator runs at one K16 step per ~220 clk whatever N
 // (tools/microbench/mma_rate.cu), so the full rate needs ~400+ accumulator
@@ -49,6 +52,30 @@ using rcm::gelu_bf16x2;
 using rcm::tma_store_3d;
 using rcm::tmem_ld32;
 __device__ __forceinline__ uint64_t desc_sw128(const void *smem) { return rcm::desc_sw<128>(smem); }
+__device__ __forceinline__ uint32_t cvt_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ float2 f16x2_to_f2(uint32_t v) {
+  float lo, hi;
+  asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n}"
+      : "=f"(lo), "=f"(hi) : "r"(v));
+  return make_float2(lo, hi);
+}
+
+#ifdef L2TRACE  // timing experiment: per-tile clock64 stamps of cluster 0 (tools/l2trace.py)
+constexpr int TR_TILES = 40;
+__device__ long long g_l2trace[2][20][TR_TILES][4];  // [DOT][warp][tile][event]
+#define TRACE(w, it, k)                                                                                  \
+  do {                                                                                                   \
+    if (blockIdx.x == 0 && (it) < TR_TILES && lane == 0) g_l2trace[DOT ? 1 : 0][w][it][k] = clock64(); \
+  } while (0)
+#else
+#define TRACE(w, it, k) \
+  do {                  \
+  } while (0)
+#endif
 
 template <int NP, bool DOT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
@@ -133,7 +160,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
       uint32_t ph = 0;
       int it = 0;
       for (int tile = cl; tile < total; tile += ncl, ++it) {
+        TRACE(W_MMA, it, 0);
         rcx::mbar_wait(c2empty, (it & 1) ^ 1);  // previous tile drained
+        TRACE(W_MMA, it, 1);
         rcx::tc_fence_after();
         for (int c = 0; c < C; ++c) {
           rcx::mbar_wait(&full[s], ph);
@@ -150,12 +179,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
           if (++s == S) { s = 0; ph ^= 1; }
         }
         rcx::mma_commit_pair(c2full);
+        TRACE(W_MMA, it, 2);
       }
     }
   } else {  // ------------------------------------------------------ epilogue warps 0..15 (both CTAs)
     const int q = warp & 3, sub = warp >> 2;
     const uint32_t tq = (uint32_t)(q * 32) << 16;
     constexpr int NCH = NP / 16;
+    constexpr int MAXCH = (NCH + 3) / 4;  // 16-column chunks per warp (7 at NP = 400)
     const int ch_lo = (NCH * sub) / 4, ch_hi = (NCH * (sub + 1)) / 4;
     const uint32_t c2empty0 = rcx::map_cta(c2empty, 0);
     uint8_t *stg_base = sST + warp * 2 * 1024;
@@ -164,86 +195,76 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     for (int tile = cl; tile < total; tile += ncl, ++it) {
       const int pass = tile % a.passes, rest = tile / a.passes;
       const int mp = rest % pairs, net = rest / pairs;
+      TRACE(warp, it, 0);
       rcx::mbar_wait(c2full, it & 1);
+      TRACE(warp, it, 1);
       rcx::mbar_wait(&bfull[it & 1], (it >> 1) & 1);
       rcx::tc_fence_after();
-      if (ch_lo == ch_hi) {  // narrow pass (NP < 64): this warp owns no columns but must still release
-        rcx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
-      }
       const float *b2 = sB2 + (it & 1) * VEC;
       const int grow = mp * 256 + rank * 128 + q * 32;  // first global row of this warp's 32 rows
-      if constexpr (DOT) {
+      const int nch = ch_hi - ch_lo;
+      // Phase A (no MUFU): every accumulator column of this warp -> registers as 16-bit pairs of
+      // (acc + bias): bf16 for layer 2 (the GELU input was bf16 anyway: bit-identical), f16 for the
+      // fp32 layer-3 GELU.  Then release the accumulator, so the next tile's MMAs run under phase B.
+      uint32_t pk[MAXCH][8];
+#pragma unroll
+      for (int c = 0; c < MAXCH; ++c) {
+        if (c < nch) {
+          uint32_t v[16];
+          rcx::tmem_ld16(tmem + tq + (ch_lo + c) * 16, v);
+          rcx::tmem_ld_wait();
+          const float4 *bb = reinterpret_cast<const float4 *>(b2 + (ch_lo + c) * 16);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 b = bb[j];
+            const float x0 = __uint_as_float(v[4 * j]) + b.x, x1 = __uint_as_float(v[4 * j + 1]) + b.y;
+            const float x2 = __uint_as_float(v[4 * j + 2]) + b.z, x3 = __uint_as_float(v[4 * j + 3]) + b.w;
+            pk[c][2 * j] = DOT ? cvt_f16x2(x0, x1) : cvt_bf16x2(x0, x1);
+            pk[c][2 * j + 1] = DOT ? cvt_f16x2(x2, x3) : cvt_bf16x2(x2, x3);
+          }
+        }
+      }
+      rcx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
+      TRACE(warp, it, 2);
+      // Phase B: GELU (MUFU) and the layer's output path
+      if constexpr (DOT) {  // layer 3: GELU(acc + b3) . w4 in fp32
         const float *w4s = b2 + NP;
         float dot = 0.f;
-        for (int cc = ch_lo; cc < ch_hi; cc += 2) {
-          uint32_t v[32];
-          const bool two = cc + 1 < ch_hi;
-          if (two)
-            tmem_ld32(tmem + tq + cc * 16, v);
-          else
-            rcx::tmem_ld16(tmem + tq + cc * 16, *reinterpret_cast<uint32_t(*)[16]>(v));
-          rcx::tmem_ld_wait();
-          if (cc + 2 >= ch_hi) {  // this warp's last acc columns are in registers: release the accumulator
-            rcx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
-          }
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            if (h == 1 && !two) break;
-            const int col = (cc + h) * 16;
-            const float4 *bb = reinterpret_cast<const float4 *>(b2 + col);
-            const float4 *ww = reinterpret_cast<const float4 *>(w4s + col);
+        for (int c = 0; c < MAXCH; ++c) {
+          if (c < nch) {
+            const float4 *ww = reinterpret_cast<const float4 *>(w4s + (ch_lo + c) * 16);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const float4 b = bb[j], w = ww[j];
-              dot = fmaf(rcm::gelu_f32(__uint_as_float(v[16 * h + 4 * j]) + b.x), w.x, dot);
-              dot = fmaf(rcm::gelu_f32(__uint_as_float(v[16 * h + 4 * j + 1]) + b.y), w.y, dot);
-              dot = fmaf(rcm::gelu_f32(__uint_as_float(v[16 * h + 4 * j + 2]) + b.z), w.z, dot);
-              dot = fmaf(rcm::gelu_f32(__uint_as_float(v[16 * h + 4 * j + 3]) + b.w), w.w, dot);
+              const float4 w = ww[j];
+              const float2 a01 = f16x2_to_f2(pk[c][2 * j]), a23 = f16x2_to_f2(pk[c][2 * j + 1]);
+              dot = fmaf(rcm::gelu_f32(a01.x), w.x, dot);
+              dot = fmaf(rcm::gelu_f32(a01.y), w.y, dot);
+              dot = fmaf(rcm::gelu_f32(a23.x), w.z, dot);
+              dot = fmaf(rcm::gelu_f32(a23.y), w.w, dot);
             }
           }
         }
         a.opart[((size_t)(net * a.passes + pass) * 4 + sub) * a.cap + grow + lane] = dot;
-      } else {
-        for (int cc = ch_lo; cc < ch_hi; cc += 2) {
-          uint32_t v[32];
-          const bool two = cc + 1 < ch_hi;
-          if (two)
-            tmem_ld32(tmem + tq + cc * 16, v);
-          else
-            rcx::tmem_ld16(tmem + tq + cc * 16, *reinterpret_cast<uint32_t(*)[16]>(v));
-          rcx::tmem_ld_wait();
-          if (cc + 2 >= ch_hi) {  // this warp's last acc columns are in registers: release the accumulator
-            rcx::tc_fence_before();
+      } else {  // layer 2: bf16 GELU -> [32 rows][32 B] staging (32-byte TMA swizzle) -> TMA store
+#pragma unroll
+        for (int c = 0; c < MAXCH; ++c) {
+          if (c < nch) {
+            uint32_t g[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) g[j] = gelu_bf16x2(pk[c][j]);
+            uint8_t *stg = stg_base + (nst & 1) * 1024;
+            if (lane == 0) bulk_wait_read1();  // the store that last used this buffer has read it
             __syncwarp();
-            if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
-          }
-  #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            if (h == 1 && !two) break;
-            const int col = (cc + h) * 16;
-            const float4 *bb = reinterpret_cast<const float4 *>(b2 + col);
-            uint32_t pk[8];
-  #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float4 b = bb[j];
-              pk[2 * j] = gelu_bf16x2(cvt_bf16x2(__uint_as_float(v[16 * h + 4 * j]) + b.x,
-                                                 __uint_as_float(v[16 * h + 4 * j + 1]) + b.y));
-              pk[2 * j + 1] = gelu_bf16x2(cvt_bf16x2(__uint_as_float(v[16 * h + 4 * j + 2]) + b.z,
-                                                     __uint_as_float(v[16 * h + 4 * j + 3]) + b.w));
-            }
-            uint8_t *stg = stg_base + (nst & 1) * 1024;  // [32 rows][32 B], 32-byte TMA swizzle
-            if (lane == 0) bulk_wait_read1();            // the store that last used this buffer has read it
-            __syncwarp();
-            *reinterpret_cast<uint4 *>(stg + lane * 32 + ((0 ^ ((lane >> 2) & 1)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            *reinterpret_cast<uint4 *>(stg + lane * 32 + ((1 ^ ((lane >> 2) & 1)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            const int sw = (lane >> 2) & 1;
+            *reinterpret_cast<uint4 *>(stg + lane * 32 + (sw << 4)) = make_uint4(g[0], g[1], g[2], g[3]);
+            *reinterpret_cast<uint4 *>(stg + lane * 32 + ((sw ^ 1) << 4)) = make_uint4(g[4], g[5], g[6], g[7]);
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_3d(&mapOut, stg, pass * NP + col, grow, net);
+              tma_store_3d(&mapOut, stg, pass * NP + (ch_lo + c) * 16, grow, net);
               bulk_commit();
             }
             ++nst;
@@ -251,6 +272,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
         }
       }
       __syncwarp();
+      TRACE(warp, it, 3);
       if (lane == 0) rcx::mbar_arrive(&bempty[it & 1]);
     }
     if (!DOT && lane == 0) bulk_wait_all();
@@ -288,6 +310,12 @@ int launch_l2_pair_t(const CUtensorMap &A, const CUtensorMap &Ba, const CUtensor
 }
 
 }  // namespace
+
+#ifdef L2TRACE
+extern "C" __attribute__((visibility("default"))) int rc_debug_l2trace(void *host) {
+  return (int)cudaMemcpyFromSymbol(host, g_l2trace, sizeof(g_l2trace));
+}
+#endif
 
 // pass width: the widest NP <= 400 (TMEM: one pass accumulator) that divides h2 into equal passes
 int l2_pass_width(int h2) {
