@@ -111,7 +111,10 @@ typedef struct {
   const double *y_mean, *y_std;   /* [n_nets] output de-normalisation (R2) */
   double lambda_bc;               /* Box-Cox lambda (R3; 0.1) -- must satisfy 1/lambda integer <= 16 */
   double dt;                      /* training dt of the bundle, s (R7) */
-  int32_t precision;              /* RC_BF16 (bf16 x bf16 -> fp32) | RC_TF32 */
+  int32_t precision;              /* RC_BF16: bf16 operands and activations, fp32 accumulate, tanh-form
+                                     GELU (north_star gate 2e-2 on o);
+                                     RC_TF32: tf32-rounded fp32 operands and activations, fp32
+                                     accumulate, exact-erf GELU (gate 1e-3 on o) */
 } rc_mlp_desc;
 
 int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *desc, rc_mlp **out);

@@ -48,6 +48,32 @@ __device__ __forceinline__ float gelu_f32(float x) {
   const float hx = 0.5f * x;
   return fmaf(hx, t, hx);
 }
+// exact-erf GELU in fp32 (the oracle's form, R5) for the TF32 precision mode
+__device__ __forceinline__ float gelu_erf_f32(float x) { return 0.5f * x * (1.0f + erff(x * 0.7071067811865476f)); }
+// round-to-nearest fp32 -> tf32 (the value the tensor core multiplies; low 13 mantissa bits zero)
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// element-type traits of the MLP GEMMs: bf16 (kind::f16, K16 atoms) or tf32 (kind::tf32, K8 atoms);
+// one MMA K atom is 32 bytes of a K-major operand row in both cases
+template <bool TF32>
+struct Elem {
+  static constexpr int BYTES = TF32 ? 4 : 2;
+  static constexpr int KATOM = TF32 ? 8 : 16;
+  static constexpr uint32_t FMT = TF32 ? 2u : 1u;  // instruction-descriptor a/b format
+};
+template <bool TF32>
+__device__ __forceinline__ void mma_cta(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (TF32) rcx::mma_tf32(d, a, b, idesc, acc); else rcx::mma_bf16(d, a, b, idesc, acc);
+}
+template <bool TF32>
+__device__ __forceinline__ void mma_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (TF32) rcx::mma_tf32_pair(d, a, b, idesc, acc); else rcx::mma_bf16_pair(d, a, b, idesc, acc);
+}
+
 __device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));

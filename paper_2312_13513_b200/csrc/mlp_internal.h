@@ -7,16 +7,15 @@
 
 int mlp_num_sms();
 
-// layer 1 (mlp_l1_sm100.cu): h1 = GELU(z W1^T) with W1 stored halved, 128 x 256 tiles
-// (W1 boxes of l1_box_rows() rows), h1 TMA-stored through `Out` (64-column x 32-row boxes,
-// 128-byte swizzle) into [nets][cap][N] bf16
+// layer 1 (mlp_l1_sm100.cu): h1 = GELU(z W1^T), 128 x 256 tiles (W1 boxes of l1_box_rows() rows),
+// h1 TMA-stored through `Out` (128-byte-swizzled 32-row boxes: 64 bf16 or 32 fp32 columns) into
+// [nets][cap][N]; bf16 (W1 stored halved) or tf32 (fp32 storage, tf32-rounded) precision
 struct L1Args {
   int m_tiles, n_tiles, nets, N, stages, cap;
-  __nv_bfloat16 *h1;
 };
 int l1_tile_n();
 int l1_box_rows();
-int launch_l1(int KZ, const CUtensorMap &Z, const CUtensorMap &W, const CUtensorMap &Out, const L1Args &a,
+int launch_l1(int KZ, bool tf32, const CUtensorMap &Z, const CUtensorMap &W, const CUtensorMap &Out, const L1Args &a,
               cudaStream_t s);
 int l2_pass_width(int h2);
 
@@ -27,5 +26,5 @@ struct L2Args {
   float *opart;            // layer-3 mode: [nets][passes*4][cap] partial dots
   int cap;
 };
-int launch_l2_pair(int NP, const CUtensorMap &A, const CUtensorMap &Ba, const CUtensorMap &Bb, const CUtensorMap &Out,
+int launch_l2_pair(int NP, bool tf32, const CUtensorMap &A, const CUtensorMap &Ba, const CUtensorMap &Bb, const CUtensorMap &Out,
                    const L2Args &a, cudaStream_t s);

@@ -18,6 +18,9 @@
 //  capped the store path at ~3.5 TB/s; a per-tile named barrier across the warps,
 //  one store-issuing thread fed through mbarriers, and coalesced STG stores from
 //  the warps were all slower.
+// TF32 precision mode (RC_TF32): fp32 z/W1 (tf32-rounded) with kind::tf32 MMAs,
+// exact-erf GELU in fp32, fp32 h1 rounded to tf32; each warp's 32 x 64 block is
+// staged as two 32 x 32 fp32 swizzled blocks (one 8 KB slot per warp).
 // Warps: 0..15 epilogue, 16 TMA producer, 17 MMA issuer.
 #include <cuda_bf16.h>
 
@@ -30,7 +33,12 @@ constexpr int BM = 128, BN = 256;
 constexpr int NEPI = 16;
 constexpr int W_TMA = NEPI, W_MMA = NEPI + 1;
 constexpr int L1_THREADS = 32 * (NEPI + 2);
-constexpr uint32_t STG_WARP = 32 * 128;  // [32 rows][64 bf16] swizzled staging slot (4 KB)
+// per-warp staging: [32 rows][64 cols] = 4 KB bf16 (2 slots) or 8 KB fp32 (1 slot)
+template <bool TF32>
+struct L1Stg {
+  static constexpr uint32_t SLOT = 32 * 64 * (TF32 ? 4 : 2);
+  static constexpr int NSLOT = TF32 ? 1 : 2;
+};
 #ifdef L1TRACE  // timing experiment: per-tile clock64 stamps of CTA 0 (tools/l1trace.py)
 constexpr int TR_TILES = 96;
 __device__ long long g_l1trace[24][TR_TILES][8];
@@ -55,19 +63,23 @@ __device__ __forceinline__ void wait(uint64_t *bar, uint32_t phase) {
     rcx::mbar_wait(bar, phase);
 }
 
-template <int KZ>
+template <int KZ, bool TF32>
 __global__ void __launch_bounds__(L1_THREADS, 1)
     l1_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapW,
               const __grid_constant__ CUtensorMap mapOut, L1Args a) {
-  static_assert(KZ == 16 || KZ == 32, "K atom: 32/64-byte swizzle rows");
-  constexpr uint32_t A_BYTES = BM * KZ * 2, B_BYTES = BN * KZ * 2;
+  static_assert(KZ == 16 || KZ == 32, "z row of 16 or 32 elements");
+  using E = rcm::Elem<TF32>;
+  constexpr int ROWB = KZ * E::BYTES;  // 32, 64 or 128-byte swizzled operand rows
+  constexpr uint32_t SLOT = L1Stg<TF32>::SLOT;
+  constexpr int NSLOT = L1Stg<TF32>::NSLOT;
+  constexpr uint32_t A_BYTES = BM * ROWB, B_BYTES = BN * ROWB;
   constexpr uint32_t STAGE = (A_BYTES + B_BYTES + 1023u) & ~1023u;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = rcx::smem_u32(smem_raw);
   uint8_t *smem = smem_raw + (((base_u32 + 1023u) & ~1023u) - base_u32);
   const int S = a.stages;
-  uint8_t *sST = smem;                       // NEPI x 2 slots x STG_WARP
-  uint8_t *sW = sST + NEPI * 2 * STG_WARP;   // S x [z tile | W1 tile]
+  uint8_t *sST = smem;                       // NEPI x NSLOT x SLOT
+  uint8_t *sW = sST + NEPI * NSLOT * SLOT;   // S x [z tile | W1 tile]
   uint64_t *full = reinterpret_cast<uint64_t *>(sW + S * STAGE);
   uint64_t *empty = full + S, *tfull = empty + S, *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
@@ -116,7 +128,7 @@ __global__ void __launch_bounds__(L1_THREADS, 1)
       for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
         const int nb = tile % a.n_tiles;
         const int n_eff = min(BN, a.N - nb * BN);  // multiple of 64
-        const uint32_t idesc = rcx::make_idesc(1u, BM, (uint32_t)n_eff);
+        const uint32_t idesc = rcx::make_idesc(E::FMT, BM, (uint32_t)n_eff);
         const int as = it & 1;
         TRACE(W_MMA, it, 0);
         wait<2>(&tempty[as], ((it >> 1) & 1) ^ 1);
@@ -124,10 +136,11 @@ __global__ void __launch_bounds__(L1_THREADS, 1)
         wait<2>(&full[s], ph);
         TRACE(W_MMA, it, 2);
         rcx::tc_fence_after();
-        const uint64_t ad = rcm::desc_sw<KZ * 2>(sW + s * STAGE);
-        const uint64_t bd = rcm::desc_sw<KZ * 2>(sW + s * STAGE + A_BYTES);
+        const uint64_t ad = rcm::desc_sw<ROWB>(sW + s * STAGE);
+        const uint64_t bd = rcm::desc_sw<ROWB>(sW + s * STAGE + A_BYTES);
 #pragma unroll
-        for (int k = 0; k < KZ / 16; ++k) rcx::mma_bf16(tmem + as * BN, ad + 2 * k, bd + 2 * k, idesc, k != 0);
+        for (int k = 0; k < KZ / E::KATOM; ++k)  // one 32-byte K atom per MMA: descriptor start += 2
+          rcm::mma_cta<TF32>(tmem + as * BN, ad + 2 * k, bd + 2 * k, idesc, k != 0);
         rcx::mma_commit(&empty[s]);
         rcx::mma_commit(&tfull[as]);
         if (++s == S) { s = 0; ph ^= 1; }
@@ -135,7 +148,7 @@ __global__ void __launch_bounds__(L1_THREADS, 1)
     }
   } else {  // ---------------- epilogue warps 0..15: 32 rows (lane quadrant q) x 64 columns (block sub)
     const int q = warp & 3, sub = warp >> 2;
-    uint8_t *stg0 = sST + warp * 2 * STG_WARP;
+    uint8_t *stg0 = sST + warp * NSLOT * SLOT;
     int it = 0, nst = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
       const int nb = tile % a.n_tiles, rest = tile / a.n_tiles;
@@ -158,22 +171,44 @@ __global__ void __launch_bounds__(L1_THREADS, 1)
       if (lane == 0) rcx::mbar_arrive(&tempty[as]);
       TRACE(warp, it, 2);
       if (!mine) continue;
-      uint8_t *stg = stg0 + (nst & 1) * STG_WARP;
-      if (lane == 0) rcm::bulk_wait_read1();  // the store that last used this slot has read it
+      uint8_t *stg = stg0 + (nst % NSLOT) * SLOT;
+      if (lane == 0) {  // the store that last used this slot has read it
+        if constexpr (NSLOT == 2) rcm::bulk_wait_read1(); else rcm::bulk_wait_read0();
+      }
       __syncwarp();
+      if constexpr (TF32) {
+        // exact GELU in fp32, tf32-rounded; [32 rows][32 fp32] blocks, 128-byte swizzle
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t pk[8];
+        for (int c = 0; c < 4; ++c) {
+          float g[16];
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          pk[j] = rcm::gelu_half_bf16x2(rcm::cvt_bf16x2(__uint_as_float(v[c][2 * j]), __uint_as_float(v[c][2 * j + 1])));
-        rcm::stage_sw128(stg, lane, 2 * c, pk);
+          for (int j = 0; j < 16; ++j) g[j] = rcm::tf32_rn(rcm::gelu_erf_f32(__uint_as_float(v[c][j])));
+          uint8_t *r = stg + (c >> 1) * 4096 + lane * 128;
+          const int x = lane & 7, u0 = (c & 1) * 4;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<float4 *>(r + (((u0 + u) ^ x) << 4)) = make_float4(g[4 * u], g[4 * u + 1], g[4 * u + 2], g[4 * u + 3]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            pk[j] = rcm::gelu_half_bf16x2(rcm::cvt_bf16x2(__uint_as_float(v[c][2 * j]), __uint_as_float(v[c][2 * j + 1])));
+          rcm::stage_sw128(stg, lane, 2 * c, pk);
+        }
       }
       rcm::fence_async_smem();
       __syncwarp();
       TRACE(warp, it, 3);
       if (lane == 0) {
-        rcm::tma_store_3d(&mapOut, stg, nb * BN + sub * 64, mb * BM + q * 32, net);
+        if constexpr (TF32) {
+          rcm::tma_store_3d(&mapOut, stg, nb * BN + sub * 64, mb * BM + q * 32, net);
+          rcm::tma_store_3d(&mapOut, stg + 4096, nb * BN + sub * 64 + 32, mb * BM + q * 32, net);
+        } else {
+          rcm::tma_store_3d(&mapOut, stg, nb * BN + sub * 64, mb * BM + q * 32, net);
+        }
         rcm::bulk_commit();
       }
       ++nst;
@@ -188,22 +223,23 @@ __global__ void __launch_bounds__(L1_THREADS, 1)
   }
 }
 
-template <int KZ>
+template <int KZ, bool TF32>
 int launch_t(const CUtensorMap &Z, const CUtensorMap &W, const CUtensorMap &Out, L1Args a, cudaStream_t s) {
-  constexpr size_t STAGE = ((BM * KZ * 2 + BN * KZ * 2) + 1023) & ~(size_t)1023;
-  const size_t fixed = 1024 + NEPI * 2 * STG_WARP + 256;
+  constexpr int EB = rcm::Elem<TF32>::BYTES;
+  constexpr size_t STAGE = ((BM * KZ * EB + BN * KZ * EB) + 1023) & ~(size_t)1023;
+  const size_t fixed = 1024 + NEPI * L1Stg<TF32>::NSLOT * L1Stg<TF32>::SLOT + 256;
   int stages = (int)((232448 - fixed) / STAGE);
   if (stages > 8) stages = 8;
   a.stages = stages;
   const size_t smem = fixed + stages * STAGE;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(l1_kernel<KZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaFuncSetAttribute(l1_kernel<KZ, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     attr = true;
   }
   const int total = a.m_tiles * a.n_tiles * a.nets;
   const int grid = total < mlp_num_sms() ? total : mlp_num_sms();
-  l1_kernel<KZ><<<grid, L1_THREADS, smem, s>>>(Z, W, Out, a);
+  l1_kernel<KZ, TF32><<<grid, L1_THREADS, smem, s>>>(Z, W, Out, a);
   RC_LAUNCH_CHECK();
   return RC_OK;
 }
@@ -219,11 +255,11 @@ extern "C" __attribute__((visibility("default"))) int rc_debug_l1trace(void *hos
 }
 #endif
 
-int launch_l1(int KZ, const CUtensorMap &Z, const CUtensorMap &W, const CUtensorMap &Out, const L1Args &a,
+int launch_l1(int KZ, bool tf32, const CUtensorMap &Z, const CUtensorMap &W, const CUtensorMap &Out, const L1Args &a,
               cudaStream_t s) {
   ProfScope prof(RC_STAGE_L1, s);
   if (a.N % 64) return rc_fail(RC_EUNSUPPORTED, "layer-1 GEMM: h1 = %d is not a multiple of 64", a.N);
-  if (KZ == 16) return launch_t<16>(Z, W, Out, a, s);
-  if (KZ == 32) return launch_t<32>(Z, W, Out, a, s);
+  if (KZ == 16) return tf32 ? launch_t<16, true>(Z, W, Out, a, s) : launch_t<16, false>(Z, W, Out, a, s);
+  if (KZ == 32) return tf32 ? launch_t<32, true>(Z, W, Out, a, s) : launch_t<32, false>(Z, W, Out, a, s);
   return rc_fail(RC_EUNSUPPORTED, "layer-1 GEMM: no instance for K = %d", KZ);
 }

@@ -41,7 +41,12 @@ namespace {
 
 constexpr int NEPI = 16;
 constexpr int L2_THREADS = 32 * NEPI + 64;
-constexpr int KC = 64;  // K chunk (one 128-byte swizzle row of bf16)
+// K chunk = one 128-byte swizzle row: 64 bf16 or 32 fp32 (tf32) elements
+template <bool TF32>
+constexpr int kc() { return 128 / rcm::Elem<TF32>::BYTES; }
+// store staging per warp: [32 rows][16 cols] = 1 KB bf16 / 2 KB fp32, two slots
+template <bool TF32>
+constexpr uint32_t stg_bytes() { return 32 * 16 * rcm::Elem<TF32>::BYTES; }
 
 using rcm::bulk_commit;
 using rcm::bulk_wait_all;
@@ -77,7 +82,7 @@ __device__ long long g_l2trace[2][20][TR_TILES][4];  // [DOT][warp][tile][event]
   } while (0)
 #endif
 
-template <int NP, bool DOT>
+template <int NP, bool DOT, bool TF32>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     l2_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBa,
                    const __grid_constant__ CUtensorMap mapBb, const __grid_constant__ CUtensorMap mapOut, L2Args a) {
@@ -85,7 +90,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
   constexpr int P1 = NP > 256 ? 256 : NP, P2 = NP - P1;
   constexpr int H1 = P1 / 2, H2 = P2 / 2;  // B rows per CTA of each piece
   static_assert(H1 % 8 == 0 && H2 % 8 == 0, "8-row swizzle atoms");
-  constexpr uint32_t A_BYTES = 128 * KC * 2, B_BYTES = (NP / 2) * KC * 2;
+  using E = rcm::Elem<TF32>;
+  constexpr int KC = kc<TF32>();
+  constexpr uint32_t STG = stg_bytes<TF32>();
+  constexpr uint32_t A_BYTES = 128 * 128, B_BYTES = (NP / 2) * 128;  // 128-byte rows
   constexpr uint32_t STAGE = (A_BYTES + B_BYTES + 1023u) & ~1023u;
   constexpr int W_TMA = NEPI, W_MMA = NEPI + 1;
 
@@ -95,7 +103,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
   const int S = a.stages;
   uint8_t *sW = smem;                                   // S x [A tile | B half]
   uint8_t *sST = sW + S * STAGE;                        // NEPI x 2 x 1 KB store staging
-  float *sB2 = reinterpret_cast<float *>(sST + NEPI * 2 * 1024);  // 2 x [b | w4 (DOT)] slices
+  float *sB2 = reinterpret_cast<float *>(sST + NEPI * 2 * STG);  // 2 x [b | w4 (DOT)] slices
   constexpr int VEC = DOT ? 2 * NP : NP;
   uint64_t *bar = reinterpret_cast<uint64_t *>(sB2 + 2 * VEC);
   uint64_t *full = bar, *empty = full + S, *c2full = empty + S, *c2empty = c2full + 1, *bfull = c2empty + 1,
@@ -154,8 +162,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     }
   } else if (warp == W_MMA) {
     if (lane == 0 && leader) {  // ------------------------------------- MMA issuer (even CTA)
-      constexpr uint32_t idp1 = rcx::make_idesc(1u, 256, P1);
-      constexpr uint32_t idp2 = rcx::make_idesc(1u, 256, P2 > 0 ? P2 : 16);
+      constexpr uint32_t idp1 = rcx::make_idesc(E::FMT, 256, P1);
+      constexpr uint32_t idp2 = rcx::make_idesc(E::FMT, 256, P2 > 0 ? P2 : 16);
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
@@ -170,10 +178,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
           const uint64_t da = desc_sw128(sW + s * STAGE);
           const uint64_t db = desc_sw128(sW + s * STAGE + A_BYTES);
 #pragma unroll
-          for (int k = 0; k < KC / 16; ++k) {
-            rcx::mma_bf16_pair(tmem, da + 2 * k, db + 2 * k, idp1, (c | k) != 0);
+          for (int k = 0; k < KC / E::KATOM; ++k) {  // 32-byte K atoms: descriptor start += 2
+            rcm::mma_pair<TF32>(tmem, da + 2 * k, db + 2 * k, idp1, (c | k) != 0);
             if (P2 > 0)
-              rcx::mma_bf16_pair(tmem + P1, da + 2 * k, db + (uint64_t)((H1 * 128) >> 4) + 2 * k, idp2, (c | k) != 0);
+              rcm::mma_pair<TF32>(tmem + P1, da + 2 * k, db + (uint64_t)((H1 * 128) >> 4) + 2 * k, idp2, (c | k) != 0);
           }
           rcx::mma_commit_pair(&empty[s]);
           if (++s == S) { s = 0; ph ^= 1; }
@@ -189,7 +197,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     constexpr int MAXCH = (NCH + 3) / 4;  // 16-column chunks per warp (7 at NP = 400)
     const int ch_lo = (NCH * sub) / 4, ch_hi = (NCH * (sub + 1)) / 4;
     const uint32_t c2empty0 = rcx::map_cta(c2empty, 0);
-    uint8_t *stg_base = sST + warp * 2 * 1024;
+    uint8_t *stg_base = sST + warp * 2 * STG;
     uint32_t nst = 0;
     int it = 0;
     for (int tile = cl; tile < total; tile += ncl, ++it) {
@@ -202,72 +210,140 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
       rcx::tc_fence_after();
       const float *b2 = sB2 + (it & 1) * VEC;
       const int grow = mp * 256 + rank * 128 + q * 32;  // first global row of this warp's 32 rows
-      const int nch = ch_hi - ch_lo;
-      // Phase A (no MUFU): every accumulator column of this warp -> registers as 16-bit pairs of
-      // (acc + bias): bf16 for layer 2 (the GELU input was bf16 anyway: bit-identical), f16 for the
-      // fp32 layer-3 GELU.  Then release the accumulator, so the next tile's MMAs run under phase B.
-      uint32_t pk[MAXCH][8];
-#pragma unroll
-      for (int c = 0; c < MAXCH; ++c) {
-        if (c < nch) {
-          uint32_t v[16];
-          rcx::tmem_ld16(tmem + tq + (ch_lo + c) * 16, v);
-          rcx::tmem_ld_wait();
-          const float4 *bb = reinterpret_cast<const float4 *>(b2 + (ch_lo + c) * 16);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 b = bb[j];
-            const float x0 = __uint_as_float(v[4 * j]) + b.x, x1 = __uint_as_float(v[4 * j + 1]) + b.y;
-            const float x2 = __uint_as_float(v[4 * j + 2]) + b.z, x3 = __uint_as_float(v[4 * j + 3]) + b.w;
-            pk[c][2 * j] = DOT ? cvt_f16x2(x0, x1) : cvt_bf16x2(x0, x1);
-            pk[c][2 * j + 1] = DOT ? cvt_f16x2(x2, x3) : cvt_bf16x2(x2, x3);
-          }
-        }
-      }
-      rcx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
-      TRACE(warp, it, 2);
-      // Phase B: GELU (MUFU) and the layer's output path
-      if constexpr (DOT) {  // layer 3: GELU(acc + b3) . w4 in fp32
-        const float *w4s = b2 + NP;
+      if constexpr (TF32) {
+        // fp32 accumulators chunk pair by chunk pair; the accumulator is released after the last load
         float dot = 0.f;
+        if (ch_lo == ch_hi) {
+          rcx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
+        }
+        for (int cc = ch_lo; cc < ch_hi; cc += 2) {
+          uint32_t v[32];
+          const bool two = cc + 1 < ch_hi;
+          if (two)
+            tmem_ld32(tmem + tq + cc * 16, v);
+          else
+            rcx::tmem_ld16(tmem + tq + cc * 16, *reinterpret_cast<uint32_t(*)[16]>(v));
+          rcx::tmem_ld_wait();
+          if (cc + 2 >= ch_hi) {
+            rcx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
+            TRACE(warp, it, 2);
+          }
 #pragma unroll
-        for (int c = 0; c < MAXCH; ++c) {
-          if (c < nch) {
-            const float4 *ww = reinterpret_cast<const float4 *>(w4s + (ch_lo + c) * 16);
+          for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !two) break;
+            const int col = (cc + h) * 16;
+            const float4 *bb = reinterpret_cast<const float4 *>(b2 + col);
+            if constexpr (DOT) {  // layer 3: exact GELU(acc + b3) . w4
+              const float4 *ww = reinterpret_cast<const float4 *>(b2 + NP + col);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float4 w = ww[j];
-              const float2 a01 = f16x2_to_f2(pk[c][2 * j]), a23 = f16x2_to_f2(pk[c][2 * j + 1]);
-              dot = fmaf(rcm::gelu_f32(a01.x), w.x, dot);
-              dot = fmaf(rcm::gelu_f32(a01.y), w.y, dot);
-              dot = fmaf(rcm::gelu_f32(a23.x), w.z, dot);
-              dot = fmaf(rcm::gelu_f32(a23.y), w.w, dot);
+              for (int j = 0; j < 4; ++j) {
+                const float4 b = bb[j], w = ww[j];
+                dot = fmaf(rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j]) + b.x), w.x, dot);
+                dot = fmaf(rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j + 1]) + b.y), w.y, dot);
+                dot = fmaf(rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j + 2]) + b.z), w.z, dot);
+                dot = fmaf(rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j + 3]) + b.w), w.w, dot);
+              }
+            } else {  // layer 2: tf32-rounded exact GELU -> [32 rows][64 B] staging (64-byte swizzle) -> TMA store
+              float g[16];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float4 b = bb[j];
+                g[4 * j] = rcm::tf32_rn(rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j]) + b.x));
+                g[4 * j + 1] = rcm::tf32_rn(rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j + 1]) + b.y));
+                g[4 * j + 2] = rcm::tf32_rn(rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j + 2]) + b.z));
+                g[4 * j + 3] = rcm::tf32_rn(rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j + 3]) + b.w));
+              }
+              uint8_t *stg = stg_base + (nst & 1) * STG;
+              if (lane == 0) bulk_wait_read1();
+              __syncwarp();
+              const int x = (lane >> 1) & 3;
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                *reinterpret_cast<float4 *>(stg + lane * 64 + ((u ^ x) << 4)) =
+                    make_float4(g[4 * u], g[4 * u + 1], g[4 * u + 2], g[4 * u + 3]);
+              fence_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_3d(&mapOut, stg, pass * NP + col, grow, net);
+                bulk_commit();
+              }
+              ++nst;
             }
           }
         }
-        a.opart[((size_t)(net * a.passes + pass) * 4 + sub) * a.cap + grow + lane] = dot;
-      } else {  // layer 2: bf16 GELU -> [32 rows][32 B] staging (32-byte TMA swizzle) -> TMA store
-#pragma unroll
+        if constexpr (DOT) a.opart[((size_t)(net * a.passes + pass) * 4 + sub) * a.cap + grow + lane] = dot;
+      } else {
+        const int nch = ch_hi - ch_lo;
+        // Phase A (no MUFU): every accumulator column of this warp -> registers as 16-bit pairs of
+        // (acc + bias): bf16 for layer 2 (the GELU input was bf16 anyway: bit-identical), f16 for the
+        // fp32 layer-3 GELU.  Then release the accumulator, so the next tile's MMAs run under phase B.
+        uint32_t pk[MAXCH][8];
+  #pragma unroll
         for (int c = 0; c < MAXCH; ++c) {
           if (c < nch) {
-            uint32_t g[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) g[j] = gelu_bf16x2(pk[c][j]);
-            uint8_t *stg = stg_base + (nst & 1) * 1024;
-            if (lane == 0) bulk_wait_read1();  // the store that last used this buffer has read it
-            __syncwarp();
-            const int sw = (lane >> 2) & 1;
-            *reinterpret_cast<uint4 *>(stg + lane * 32 + (sw << 4)) = make_uint4(g[0], g[1], g[2], g[3]);
-            *reinterpret_cast<uint4 *>(stg + lane * 32 + ((sw ^ 1) << 4)) = make_uint4(g[4], g[5], g[6], g[7]);
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_3d(&mapOut, stg, pass * NP + (ch_lo + c) * 16, grow, net);
-              bulk_commit();
+            uint32_t v[16];
+            rcx::tmem_ld16(tmem + tq + (ch_lo + c) * 16, v);
+            rcx::tmem_ld_wait();
+            const float4 *bb = reinterpret_cast<const float4 *>(b2 + (ch_lo + c) * 16);
+  #pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 b = bb[j];
+              const float x0 = __uint_as_float(v[4 * j]) + b.x, x1 = __uint_as_float(v[4 * j + 1]) + b.y;
+              const float x2 = __uint_as_float(v[4 * j + 2]) + b.z, x3 = __uint_as_float(v[4 * j + 3]) + b.w;
+              pk[c][2 * j] = DOT ? cvt_f16x2(x0, x1) : cvt_bf16x2(x0, x1);
+              pk[c][2 * j + 1] = DOT ? cvt_f16x2(x2, x3) : cvt_bf16x2(x2, x3);
             }
-            ++nst;
+          }
+        }
+        rcx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
+        TRACE(warp, it, 2);
+        // Phase B: GELU (MUFU) and the layer's output path
+        if constexpr (DOT) {  // layer 3: GELU(acc + b3) . w4 in fp32
+          const float *w4s = b2 + NP;
+          float dot = 0.f;
+  #pragma unroll
+          for (int c = 0; c < MAXCH; ++c) {
+            if (c < nch) {
+              const float4 *ww = reinterpret_cast<const float4 *>(w4s + (ch_lo + c) * 16);
+  #pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float4 w = ww[j];
+                const float2 a01 = f16x2_to_f2(pk[c][2 * j]), a23 = f16x2_to_f2(pk[c][2 * j + 1]);
+                dot = fmaf(rcm::gelu_f32(a01.x), w.x, dot);
+                dot = fmaf(rcm::gelu_f32(a01.y), w.y, dot);
+                dot = fmaf(rcm::gelu_f32(a23.x), w.z, dot);
+                dot = fmaf(rcm::gelu_f32(a23.y), w.w, dot);
+              }
+            }
+          }
+          a.opart[((size_t)(net * a.passes + pass) * 4 + sub) * a.cap + grow + lane] = dot;
+        } else {  // layer 2: bf16 GELU -> [32 rows][32 B] staging (32-byte TMA swizzle) -> TMA store
+  #pragma unroll
+          for (int c = 0; c < MAXCH; ++c) {
+            if (c < nch) {
+              uint32_t g[8];
+  #pragma unroll
+              for (int j = 0; j < 8; ++j) g[j] = gelu_bf16x2(pk[c][j]);
+              uint8_t *stg = stg_base + (nst & 1) * 1024;
+              if (lane == 0) bulk_wait_read1();  // the store that last used this buffer has read it
+              __syncwarp();
+              const int sw = (lane >> 2) & 1;
+              *reinterpret_cast<uint4 *>(stg + lane * 32 + (sw << 4)) = make_uint4(g[0], g[1], g[2], g[3]);
+              *reinterpret_cast<uint4 *>(stg + lane * 32 + ((sw ^ 1) << 4)) = make_uint4(g[4], g[5], g[6], g[7]);
+              fence_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_3d(&mapOut, stg, pass * NP + (ch_lo + c) * 16, grow, net);
+                bulk_commit();
+              }
+              ++nst;
+            }
           }
         }
       }
@@ -286,11 +362,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
   }
 }
 
-template <int NP, bool DOT>
+template <int NP, bool DOT, bool TF32>
 int launch_l2_pair_t(const CUtensorMap &A, const CUtensorMap &Ba, const CUtensorMap &Bb, const CUtensorMap &Out,
                      L2Args a, cudaStream_t s) {
-  constexpr size_t STAGE = ((128 * KC * 2 + (NP / 2) * KC * 2) + 1023) & ~(size_t)1023;
-  const size_t fixed = 1024 + NEPI * 2 * 1024 + 2 * (DOT ? 2 : 1) * NP * 4 + 512;
+  constexpr size_t STAGE = ((128 * 128 + (NP / 2) * 128) + 1023) & ~(size_t)1023;
+  const size_t fixed = 1024 + NEPI * 2 * stg_bytes<TF32>() + 2 * (DOT ? 2 : 1) * NP * 4 + 512;
   int stages = (int)((232448 - fixed) / STAGE);
   if (stages > 8) stages = 8;
   if (stages < 2) return rc_fail(RC_EUNSUPPORTED, "layer-2 GEMM: pass width %d does not fit", NP);
@@ -298,13 +374,13 @@ int launch_l2_pair_t(const CUtensorMap &A, const CUtensorMap &Ba, const CUtensor
   const size_t smem = fixed + stages * STAGE;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(l2_pair_kernel<NP, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaFuncSetAttribute(l2_pair_kernel<NP, DOT, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     attr = true;
   }
   const int total = a.nets * (a.m_tiles / 2) * a.passes;
   int clusters = mlp_num_sms() / 2;
   if (clusters > total) clusters = total;
-  l2_pair_kernel<NP, DOT><<<2 * clusters, L2_THREADS, smem, s>>>(A, Ba, Bb, Out, a);
+  l2_pair_kernel<NP, DOT, TF32><<<2 * clusters, L2_THREADS, smem, s>>>(A, Ba, Bb, Out, a);
   RC_LAUNCH_CHECK();
   return RC_OK;
 }
@@ -324,13 +400,15 @@ int l2_pass_width(int h2) {
   return 0;
 }
 
-int launch_l2_pair(int NP, const CUtensorMap &A, const CUtensorMap &Ba, const CUtensorMap &Bb, const CUtensorMap &Out,
+int launch_l2_pair(int NP, bool tf32, const CUtensorMap &A, const CUtensorMap &Ba, const CUtensorMap &Bb, const CUtensorMap &Out,
                    const L2Args &a, cudaStream_t s) {
   ProfScope prof(a.w4 ? RC_STAGE_L3 : RC_STAGE_L2, s);
 #define RC_L2P(np)                                                                     \
   if (NP == np)                                                                        \
-    return a.w4 ? launch_l2_pair_t<np, true>(A, Ba, Bb, Out, a, s)                      \
-                : launch_l2_pair_t<np, false>(A, Ba, Bb, Out, a, s);
+    return a.w4 ? (tf32 ? launch_l2_pair_t<np, true, true>(A, Ba, Bb, Out, a, s)        \
+                        : launch_l2_pair_t<np, true, false>(A, Ba, Bb, Out, a, s))      \
+                : (tf32 ? launch_l2_pair_t<np, false, true>(A, Ba, Bb, Out, a, s)       \
+                        : launch_l2_pair_t<np, false, false>(A, Ba, Bb, Out, a, s));
   RC_L2P(400)
   RC_L2P(256)
   RC_L2P(208)

@@ -31,7 +31,6 @@
 namespace {
 
 constexpr int BM = 128;       // UMMA M (one CTA, cta_group::1)
-constexpr int BK = 64;        // K elements per pipeline stage (128 B of bf16 = one swizzle row)
 constexpr int MAX_CAP = 32768;     // cells per chunk (activation working set)
 constexpr int QPART_BLOCKS = 148 * 4;
 
@@ -42,7 +41,8 @@ struct ProArgs {
   int rows, rows_pad, d_in, ns, kz;
   float lambda, inv_lambda;
   const float *xmean, *xinvstd;
-  __nv_bfloat16 *z;  // [cap][kz]: z-scored inputs, then two 1.0 columns (b1 hi/lo), then zeros
+  void *z;  // [cap][kz] bf16 (or tf32-rounded fp32): z-scored inputs, two 1.0 columns (b1 hi/lo), zeros
+  int tf32;
 };
 
 __global__ void __launch_bounds__(256) prologue_kernel(ProArgs a, CellsDev c) {
@@ -67,7 +67,17 @@ __global__ void __launch_bounds__(256) prologue_kernel(ProArgs a, CellsDev c) {
     for (int j = 0; j < 32; ++j)
       if (j == a.d_in || j == a.d_in + 1) x[j] = 1.f;
   }
-  uint4 *dst = reinterpret_cast<uint4 *>(a.z + (size_t)r * a.kz);
+  if (a.tf32) {
+    float4 *dst = reinterpret_cast<float4 *>(static_cast<float *>(a.z) + (size_t)r * a.kz);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (q * 4 >= a.kz) break;
+      dst[q] = make_float4(rcm::tf32_rn(x[4 * q]), rcm::tf32_rn(x[4 * q + 1]), rcm::tf32_rn(x[4 * q + 2]),
+                           rcm::tf32_rn(x[4 * q + 3]));
+    }
+    return;
+  }
+  uint4 *dst = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(a.z) + (size_t)r * a.kz);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     if (q * 8 >= a.kz) break;
@@ -240,29 +250,27 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
-// 3D bf16 map over [d2][d1][d0] (d0 contiguous), box {box0, box1, 1}; the swizzle
-// width equals the box row (box0 * 2 bytes: 32, 64 or 128)
-int make_map(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t box1,
-             uint32_t box0 = BK) {
+// 3D map over [d2][d1][d0] (d0 contiguous) of bf16 (esize 2) or fp32 (esize 4) elements,
+// box {box0, box1, 1}; the swizzle width equals the box row (box0 * esize bytes: 32, 64 or 128)
+int make_map(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t box1, uint32_t box0,
+             int esize) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return rc_fail(RC_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {d0, d1, d2};
-  cuuint64_t strides[2] = {d0 * 2, d0 * d1 * 2};
+  cuuint64_t strides[2] = {d0 * esize, d0 * d1 * esize};
   cuuint32_t box[3] = {box0, box1, 1};
-  const CUtensorMapSwizzle sw = box0 * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                : box0 * 2 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+  const uint32_t rowb = box0 * esize;
+  const CUtensorMapSwizzle sw = rowb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : rowb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
+  CUresult r = enc(m, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                   const_cast<void *>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return rc_fail(RC_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return RC_OK;
 }
 
-// N-tile width: split N into ceil(N/208) near-equal tiles rounded up to 16
-// (the UMMA N granularity); the last tile may be narrower (runtime N in the
-// instruction descriptor, TMA zero-fills the rows past N).  Wide tiles keep the
-// shared-memory operand traffic per MMA under the 128 B/clk SMEM port.
 }  // namespace
 int mlp_num_sms() {
   static int n = 0;
@@ -275,7 +283,6 @@ int mlp_num_sms() {
   return n;
 }
 namespace {
-int num_sms() { return mlp_num_sms(); }
 
 struct WsLayout {
   size_t z, h1, h2, opart, qpart, total;
@@ -288,13 +295,23 @@ WsLayout ws_layout(const rc_mlp *n, int cap) {
   L.cap = cap;
   size_t o = 0;
   L.qpart = o; o = al(o + QPART_BLOCKS * 8);
-  L.z = o; o = al(o + (size_t)cap * n->kpad1 * 2);
-  L.h1 = o; o = al(o + (size_t)n->n_nets * cap * n->h1 * 2);
-  L.h2 = o; o = al(o + (size_t)n->n_nets * cap * n->h2 * 2);
+  const size_t eb = n->precision == RC_TF32 ? 4 : 2;  // activation element bytes
+  L.z = o; o = al(o + (size_t)cap * n->kpad1 * eb);
+  L.h1 = o; o = al(o + (size_t)n->n_nets * cap * n->h1 * eb);
+  L.h2 = o; o = al(o + (size_t)n->n_nets * cap * n->h2 * eb);
   const int np3 = 4 * (n->h3 / l2_pass_width(n->h3));  // partial dots per row: 4 column quarters per pass
   L.opart = o; o = al(o + (size_t)n->n_nets * np3 * cap * 4);
   L.total = o;
   return L;
+}
+
+float f2tf32(float f) {  // round-to-nearest (ties away, as cvt.rna.tf32.f32) float -> tf32 value
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & ~0x1FFFu;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
 }
 
 uint16_t f2bf(float f) {  // round-to-nearest-even float -> bf16 bits
@@ -315,34 +332,56 @@ size_t chem_workspace_bytes(const rc_mech *, const rc_mlp *n, int64_t ncells) {
 }
 
 int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
-  if (n->precision != RC_BF16) return rc_fail(RC_EUNSUPPORTED, "TF32 MLP variant not built yet");
   if (n->h1 % 64 || !l2_pass_width(n->h2) || !l2_pass_width(n->h3))
-    return rc_fail(RC_EUNSUPPORTED, "hidden widths (%d,%d,%d) not supported by the fused kernels", n->h1, n->h2, n->h3);
+    return rc_fail(RC_EUNSUPPORTED, "hidden widths (%d,%d,%d) not supported by the MLP kernels", n->h1, n->h2, n->h3);
+  const bool tf32 = n->precision == RC_TF32;
   const int nets = n->n_nets, din = n->d_in, h1 = n->h1, h2 = n->h2, h3 = n->h3, kp = n->kpad1;
   const size_t P = (size_t)h1 * din + h1 + (size_t)h2 * h1 + h2 + (size_t)h3 * h2 + h3 + h3 + 1;
+  // weights, K-major [net][out][in]: bf16 (RNE) or tf32-rounded fp32
   std::vector<uint16_t> W1((size_t)nets * h1 * kp, 0), W2((size_t)nets * h2 * h1), W3((size_t)nets * h3 * h2);
+  std::vector<float> F1, F2, F3;
+  if (tf32) {
+    F1.assign((size_t)nets * h1 * kp, 0.f);
+    F2.resize((size_t)nets * h2 * h1);
+    F3.resize((size_t)nets * h3 * h2);
+  }
   std::vector<float> b1((size_t)nets * h1), b2((size_t)nets * h2), b3((size_t)nets * h3), w4((size_t)nets * h3), b4(nets);
   for (int i = 0; i < nets; ++i) {
     const double *p = d->params + i * P;
     const double *pb1 = p + (size_t)h1 * din;
     for (int r = 0; r < h1; ++r) {
-      // W1 is stored halved (exact in bf16): the layer-1 epilogue evaluates GELU(2y) from y = x/2
-      for (int k = 0; k < din; ++k) W1[((size_t)i * h1 + r) * kp + k] = f2bf(0.5f * (float)p[(size_t)r * din + k]);
-      // b1 folded into the layer-1 MMA: z carries 1.0 in columns din and din+1
-      const uint16_t hi = f2bf(0.5f * (float)pb1[r]);
-      uint32_t hb = (uint32_t)hi << 16;
-      float hf;
-      std::memcpy(&hf, &hb, 4);
-      W1[((size_t)i * h1 + r) * kp + din] = hi;
-      W1[((size_t)i * h1 + r) * kp + din + 1] = f2bf((float)(0.5 * pb1[r] - (double)hf));
+      const size_t row = ((size_t)i * h1 + r) * kp;
+      if (tf32) {
+        for (int k = 0; k < din; ++k) F1[row + k] = f2tf32((float)p[(size_t)r * din + k]);
+        // b1 folded into the layer-1 MMA as tf32 hi + lo parts (z carries 1.0 in columns din, din+1)
+        const float hi = f2tf32((float)pb1[r]);
+        F1[row + din] = hi;
+        F1[row + din + 1] = f2tf32((float)(pb1[r] - (double)hi));
+      } else {
+        // W1 is stored halved (exact in bf16): the layer-1 epilogue evaluates GELU(2y) from y = x/2
+        for (int k = 0; k < din; ++k) W1[row + k] = f2bf(0.5f * (float)p[(size_t)r * din + k]);
+        // b1 folded into the layer-1 MMA: z carries 1.0 in columns din and din+1
+        const uint16_t hi = f2bf(0.5f * (float)pb1[r]);
+        uint32_t hb = (uint32_t)hi << 16;
+        float hf;
+        std::memcpy(&hf, &hb, 4);
+        W1[row + din] = hi;
+        W1[row + din + 1] = f2bf((float)(0.5 * pb1[r] - (double)hf));
+      }
       b1[(size_t)i * h1 + r] = (float)pb1[r];
     }
     p += (size_t)h1 * din + h1;
-    for (size_t e = 0; e < (size_t)h2 * h1; ++e) W2[(size_t)i * h2 * h1 + e] = f2bf((float)p[e]);
+    for (size_t e = 0; e < (size_t)h2 * h1; ++e) {
+      if (tf32) F2[(size_t)i * h2 * h1 + e] = f2tf32((float)p[e]);
+      else W2[(size_t)i * h2 * h1 + e] = f2bf((float)p[e]);
+    }
     p += (size_t)h2 * h1;
     for (int r = 0; r < h2; ++r) b2[(size_t)i * h2 + r] = (float)p[r];
     p += h2;
-    for (size_t e = 0; e < (size_t)h3 * h2; ++e) W3[(size_t)i * h3 * h2 + e] = f2bf((float)p[e]);
+    for (size_t e = 0; e < (size_t)h3 * h2; ++e) {
+      if (tf32) F3[(size_t)i * h3 * h2 + e] = f2tf32((float)p[e]);
+      else W3[(size_t)i * h3 * h2 + e] = f2bf((float)p[e]);
+    }
     p += (size_t)h3 * h2;
     for (int r = 0; r < h3; ++r) b3[(size_t)i * h3 + r] = (float)p[r];
     p += h3;
@@ -358,8 +397,11 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
   auto up = [](void **dst, const void *src, size_t bytes) -> bool {
     return cudaMalloc(dst, bytes) == cudaSuccess && cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
   };
-  bool ok = up(&n->d_W1, W1.data(), W1.size() * 2) && up(&n->d_W2, W2.data(), W2.size() * 2) &&
-            up(&n->d_W3, W3.data(), W3.size() * 2) && up((void **)&n->d_b1, b1.data(), b1.size() * 4) &&
+  bool ok = (tf32 ? up(&n->d_W1, F1.data(), F1.size() * 4) && up(&n->d_W2, F2.data(), F2.size() * 4) &&
+                        up(&n->d_W3, F3.data(), F3.size() * 4)
+                   : up(&n->d_W1, W1.data(), W1.size() * 2) && up(&n->d_W2, W2.data(), W2.size() * 2) &&
+                        up(&n->d_W3, W3.data(), W3.size() * 2)) &&
+            up((void **)&n->d_b1, b1.data(), b1.size() * 4) &&
             up((void **)&n->d_b2, b2.data(), b2.size() * 4) && up((void **)&n->d_b3, b3.data(), b3.size() * 4) &&
             up((void **)&n->d_w4, w4.data(), w4.size() * 4) && up((void **)&n->d_b4, b4.data(), b4.size() * 4) &&
             up((void **)&n->d_xmean, xm.data(), xm.size() * 4) && up((void **)&n->d_xinvstd, xi.data(), xi.size() * 4) &&
@@ -377,9 +419,9 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   WsLayout L = ws_layout(n, cap);
   if (L.total > ws_bytes) return rc_fail(RC_EINVAL, "workspace too small (%zu < %zu)", ws_bytes, L.total);
   uint8_t *w = static_cast<uint8_t *>(ws);
-  auto *z = reinterpret_cast<__nv_bfloat16 *>(w + L.z);
-  auto *h1 = reinterpret_cast<__nv_bfloat16 *>(w + L.h1);
-  auto *h2 = reinterpret_cast<__nv_bfloat16 *>(w + L.h2);
+  void *z = w + L.z, *h1 = w + L.h1, *h2 = w + L.h2;
+  const bool tf32 = n->precision == RC_TF32;
+  const int EB = tf32 ? 4 : 2, KC = 128 / EB;  // element bytes; K elements per 128-byte operand row
   auto *opart = reinterpret_cast<float *>(w + L.opart);
   auto *qpart = reinterpret_cast<double *>(w + L.qpart);
   const int nets = n->n_nets;
@@ -388,13 +430,17 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   const int Q1 = NP3 > 256 ? 256 : NP3, Q2 = NP3 - Q1;
   CUtensorMap mz, mh1, mh1st, mh2, mh2st, mw1, mw2a, mw2b, mw3a, mw3b;
   int rc;
-  if ((rc = make_map(&mz, z, KZ, cap, 1, BM, KZ)) || (rc = make_map(&mw1, n->d_W1, KZ, n->h1, nets, l1_box_rows(), KZ)) ||
-      (rc = make_map(&mh1, h1, n->h1, cap, nets, BM)) || (rc = make_map(&mh1st, h1, n->h1, cap, nets, 32)) ||
-      (rc = make_map(&mw2a, n->d_W2, n->h1, n->h2, nets, P1 / 2)) ||
-      (rc = make_map(&mw2b, n->d_W2, n->h1, n->h2, nets, P2 > 0 ? P2 / 2 : P1 / 2)) ||
-      (rc = make_map(&mh2, h2, n->h2, cap, nets, BM)) || (rc = make_map(&mh2st, h2, n->h2, cap, nets, 32, 16)) ||
-      (rc = make_map(&mw3a, n->d_W3, n->h2, n->h3, nets, Q1 / 2)) ||
-      (rc = make_map(&mw3b, n->d_W3, n->h2, n->h3, nets, Q2 > 0 ? Q2 / 2 : Q1 / 2)))
+  // operand maps: 128-byte rows (KC elements) except z/W1 (KZ elements); store maps: 32-row boxes
+  if ((rc = make_map(&mz, z, KZ, cap, 1, BM, KZ, EB)) ||
+      (rc = make_map(&mw1, n->d_W1, KZ, n->h1, nets, l1_box_rows(), KZ, EB)) ||
+      (rc = make_map(&mh1, h1, n->h1, cap, nets, BM, KC, EB)) ||
+      (rc = make_map(&mh1st, h1, n->h1, cap, nets, 32, KC, EB)) ||
+      (rc = make_map(&mw2a, n->d_W2, n->h1, n->h2, nets, P1 / 2, KC, EB)) ||
+      (rc = make_map(&mw2b, n->d_W2, n->h1, n->h2, nets, P2 > 0 ? P2 / 2 : P1 / 2, KC, EB)) ||
+      (rc = make_map(&mh2, h2, n->h2, cap, nets, BM, KC, EB)) ||
+      (rc = make_map(&mh2st, h2, n->h2, cap, nets, 32, 16, EB)) ||
+      (rc = make_map(&mw3a, n->d_W3, n->h2, n->h3, nets, Q1 / 2, KC, EB)) ||
+      (rc = make_map(&mw3b, n->d_W3, n->h2, n->h3, nets, Q2 > 0 ? Q2 / 2 : Q1 / 2, KC, EB)))
     return rc;
   RC_CUDA_TRY(cudaMemsetAsync(qpart, 0, QPART_BLOCKS * 8, s));
   int64_t launches = 1;
@@ -402,21 +448,21 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
     const int rows = (int)std::min<int64_t>(cap, c.n - c0);
     const int mt = (rows + 2 * BM - 1) / (2 * BM) * 2;  // even: CTA pairs of 128-row tiles
     ProArgs pa{c0, rows, mt * BM, n->d_in, n->ns, KZ, (float)n->lambda_bc, (float)(1.0 / n->lambda_bc), n->d_xmean,
-               n->d_xinvstd, z};
+               n->d_xinvstd, z, tf32 ? 1 : 0};
     {
       ProfScope prof(RC_STAGE_PROLOGUE, s);
       prologue_kernel<<<(mt * BM + 255) / 256, 256, 0, s>>>(pa, c);
       RC_LAUNCH_CHECK();
     }
     // layer 1: h1 = GELU(z W1^T) (b1 folded into z's constant-1 columns)
-    L1Args g1{mt, (n->h1 + bn1 - 1) / bn1, nets, n->h1, 0, cap, h1};
-    if ((rc = launch_l1(KZ, mz, mw1, mh1st, g1, s))) return rc;
+    L1Args g1{mt, (n->h1 + bn1 - 1) / bn1, nets, n->h1, 0, cap};
+    if ((rc = launch_l1(KZ, tf32, mz, mw1, mh1st, g1, s))) return rc;
     // layer 2: h2 = GELU(h1 W2^T + b2), CTA-pair GEMM
-    L2Args la{mt, n->h2 / NP, nets, n->h1 / 64, n->h2, 0, n->d_b2, nullptr, nullptr, cap};
-    if ((rc = launch_l2_pair(NP, mh1, mw2a, mw2b, mh2st, la, s))) return rc;
-    // layer 3 + folded layer 4: the same CTA-pair GEMM with the dot epilogue (K = h2, zero-filled to 64s)
-    L2Args l3{mt, n->h3 / NP3, nets, (n->h2 + 63) / 64, n->h3, 0, n->d_b3, n->d_w4, opart, cap};
-    if ((rc = launch_l2_pair(NP3, mh2, mw3a, mw3b, mh2st, l3, s))) return rc;
+    L2Args la{mt, n->h2 / NP, nets, (n->h1 + KC - 1) / KC, n->h2, 0, n->d_b2, nullptr, nullptr, cap};
+    if ((rc = launch_l2_pair(NP, tf32, mh1, mw2a, mw2b, mh2st, la, s))) return rc;
+    // layer 3 + folded layer 4: the same CTA-pair GEMM with the dot epilogue (K = h2, zero-filled to KC)
+    L2Args l3{mt, n->h3 / NP3, nets, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, n->d_w4, opart, cap};
+    if ((rc = launch_l2_pair(NP3, tf32, mh2, mw3a, mw3b, mh2st, l3, s))) return rc;
     EpiArgs ea{c0, rows, cap, nets, 4 * (n->h3 / NP3), n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt, opart,
                n->d_b4, n->d_ymean, n->d_ystd, m->d_P, m->d_thermo, n->d_species, qpart};
     const size_t esm = (size_t)ThermoSeg::size(m->ns) * 8 + (size_t)((m->ns * m->ns + 1) & ~1) * 8;
