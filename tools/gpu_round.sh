@@ -13,8 +13,10 @@ timeout 900 python bench.py > $O/bench_$TAG.json 2> $O/bench_$TAG.err; echo "ben
 cat $O/bench_$TAG.json; tail -3 $O/bench_$TAG.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_$TAG.csv \
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "ncu list rc=$?"
-for K in l2_pair_kernel l1_kernel l3_kernel; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 2 -c 1 \
+# l2_pair_kernel: -c 2 captures one layer-2 and one layer-3 (DOT) launch
+for K in l2_pair_kernel l1_kernel; do
+  C=1; [ $K = l2_pair_kernel ] && C=2
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 2 -c $C \
     -o $O/prof_${K}_$TAG -f python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_${K}_$TAG.log 2>&1
   echo "ncu $K rc=$?"
 done
