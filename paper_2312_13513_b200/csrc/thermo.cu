@@ -15,6 +15,13 @@
 
 namespace {
 
+// 16-byte shared load kept in program order (see the mixture-coefficient loop)
+__device__ __forceinline__ double2 lds_f64x2(const double *p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(rcx::smem_u32(p)));
+  return v;
+}
+
 __device__ __forceinline__ void warp_count_add(int64_t *dst, int v) {
   unsigned s = __reduce_add_sync(0xffffffffu, (unsigned)v);
   if ((threadIdx.x & 31) == 0 && s) atomicAdd((unsigned long long *)dst, (unsigned long long)s);
@@ -53,6 +60,9 @@ __global__ void __launch_bounds__(256) thermo_kernel(const double *__restrict__ 
   int n_bisect = 0, n_maxit = 0, n_neg = 0, n_bad = 0;
   double Tloc_max = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n; i += (int64_t)gridDim.x * blockDim.x) {
+    // mixture NASA coefficients per range and 1/W = sum Y_k / W_k.  All Y loads are issued
+    // up front; the table is read with volatile shared loads next to their use, because a
+    // fully unrolled loop would otherwise hoist the whole coefficient table into registers.
     double Y[CAP];
     bool neg = false;
 #pragma unroll UR
@@ -61,19 +71,21 @@ __global__ void __launch_bounds__(256) thermo_kernel(const double *__restrict__ 
         Y[k] = c.Y[k * c.ld + i];
         neg |= Y[k] < 0.0;
       }
-    const double p = c.p[i];
-    // mixture coefficients per range and 1/W = sum Y_k / W_k
     double Hl[6] = {0, 0, 0, 0, 0, 0}, Hh[6] = {0, 0, 0, 0, 0, 0}, sW = 0.0;
 #pragma unroll UR
     for (int k = 0; k < CAP; ++k)
       if (k < ns) {
 #pragma unroll
-        for (int j = 0; j < 6; ++j) {
-          Hl[j] = fma(Y[k], hlo[6 * k + j], Hl[j]);
-          Hh[j] = fma(Y[k], hhi[6 * k + j], Hh[j]);
+        for (int j = 0; j < 6; j += 2) {
+          const double2 lo = lds_f64x2(hlo + 6 * k + j), hi = lds_f64x2(hhi + 6 * k + j);
+          Hl[j] = fma(Y[k], lo.x, Hl[j]);
+          Hl[j + 1] = fma(Y[k], lo.y, Hl[j + 1]);
+          Hh[j] = fma(Y[k], hi.x, Hh[j]);
+          Hh[j + 1] = fma(Y[k], hi.y, Hh[j + 1]);
         }
         sW = fma(Y[k], invW[k], sW);
       }
+    const double p = c.p[i];
     auto eval = [&](double T, double &h, double &cp) {
       if constexpr (UNIFORM) {
         const bool lo = T <= Tmid;
@@ -101,9 +113,10 @@ __global__ void __launch_bounds__(256) thermo_kernel(const double *__restrict__ 
       T = fmin(fmax(T, Tmin), Tmax);
       int clamp_hits = 0;
       bool done = false;
+#pragma unroll 1
       for (int it = 1; it <= 50; ++it) {
         eval(T, hT, cpT);
-        double Tn = T + (hs - hT) / cpT;
+        double Tn = T + (hs - hT) * rcx::rcp_f64(cpT);
         bool clamped = false;
         if (Tn < Tmin) { Tn = Tmin; clamped = true; }
         if (Tn > Tmax) { Tn = Tmax; clamped = true; }
@@ -116,6 +129,7 @@ __global__ void __launch_bounds__(256) thermo_kernel(const double *__restrict__ 
       if (!done) {  // bisection on [Tmin, Tmax]; h increasing since cp > 0
         ++n_bisect;
         double lo = Tmin, hi = Tmax;
+#pragma unroll 1
         while (hi - lo > 1e-10 * (0.5 * (lo + hi))) {
           double mid = 0.5 * (lo + hi), hm, cm;
           eval(mid, hm, cm);

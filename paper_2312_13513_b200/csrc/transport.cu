@@ -15,8 +15,16 @@
 
 namespace {
 
+// Shared-memory table reads kept in program order: with the species loops fully
+// unrolled the compiler would otherwise hoist the whole coefficient table into
+// registers (255 registers and spills for 20 species).
+__device__ __forceinline__ double lds(const double *p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(rcx::smem_u32(p)));
+  return v;
+}
 __device__ __forceinline__ double poly5(const double *c, double L) {
-  return fma(L, fma(L, fma(L, fma(L, c[4], c[3]), c[2]), c[1]), c[0]);
+  return fma(L, fma(L, fma(L, fma(L, lds(c + 4), lds(c + 3)), lds(c + 2)), lds(c + 1)), lds(c));
 }
 
 template <int NS>
@@ -53,7 +61,7 @@ __global__ void __launch_bounds__(128) transport_kernel(const double *__restrict
         X[k] = c.Y[k * c.ld + i];
         sW = fma(X[k], invW[k], sW);
       }
-    const double Wbar = 1.0 / sW;
+    const double Wbar = rcx::rcp_f64(sW);
     const double L = log(T), sT = sqrt(T), qT = sqrt(sT), T15 = T * sT, pT = p / T15;
     double s1 = 0.0, s2 = 0.0, Wp = 0.0;
 #pragma unroll UR
@@ -62,10 +70,10 @@ __global__ void __launch_bounds__(128) transport_kernel(const double *__restrict
         double x = X[k] * Wbar * invW[k];
         X[k] = x > 0.0 ? x : 0.0;                 // X+ = max(X, 0)
         s[k] = qT * poly5(visc + 5 * k, L);       // sqrt(mu_k)
-        rs[k] = 1.0 / s[k];
+        rs[k] = rcx::rcp_f64(s[k]);
         double lam = sT * poly5(cond + 5 * k, L);
         s1 = fma(X[k], lam, s1);
-        s2 = fma(X[k], 1.0 / lam, s2);
+        s2 = fma(X[k], rcx::rcp_f64(lam), s2);
         Wp = fma(X[k], W[k], Wp);
         S[k] = 0.0;
       }
@@ -78,10 +86,10 @@ __global__ void __launch_bounds__(128) transport_kernel(const double *__restrict
 #pragma unroll UR
         for (int j = 0; j < CAP; ++j)
           if (j < ns) {
-            double t = fma(s[k] * rs[j], c1[k * ns + j], 1.0);
-            den = fma(X[j], t * t * c2[k * ns + j], den);
+            double t = fma(s[k] * rs[j], lds(c1 + k * ns + j), 1.0);
+            den = fma(X[j], t * t * lds(c2 + k * ns + j), den);
           }
-        if (den > 0.0) mu += X[k] * (s[k] * s[k]) / den;
+        if (den > 0.0) mu += X[k] * (s[k] * s[k]) * rcx::rcp_f64(den);
       }
     // mixture-averaged diffusion: S_k = sum_{j != k} X_j / D_jk, 1/D_jk = p / (T^1.5 R_jk(L))
 #pragma unroll UR
@@ -90,13 +98,13 @@ __global__ void __launch_bounds__(128) transport_kernel(const double *__restrict
 #pragma unroll UR
         for (int j = 0; j < CAP; ++j)
           if (j < k) {
-            double iD = pT / poly5(diff + 5 * (k * (k + 1) / 2 + j), L);
+            double iD = pT * rcx::rcp_f64(poly5(diff + 5 * (k * (k + 1) / 2 + j), L));
             S[k] = fma(X[j], iD, S[k]);
             S[j] = fma(X[k], iD, S[j]);
           }
       }
     if (c.mu) c.mu[i] = mu;
-    const double lam = 0.5 * (s1 + 1.0 / s2);
+    const double lam = 0.5 * (s1 + rcx::rcp_f64(s2));
     if (c.lambda) c.lambda[i] = lam;
     bool bad = !(isfinite(mu) && isfinite(lam));
     if (c.D) {
@@ -107,7 +115,8 @@ __global__ void __launch_bounds__(128) transport_kernel(const double *__restrict
 #pragma unroll UR
           for (int j = 0; j < CAP; ++j)
             if (j < ns && j != k) num = fma(X[j], W[j], num);
-          double Dk = (S[k] == 0.0) ? poly5(diff + 5 * (k * (k + 1) / 2 + k), L) / pT : num / (Wp * S[k]);
+          double Dk = (S[k] == 0.0) ? poly5(diff + 5 * (k * (k + 1) / 2 + k), L) * rcx::rcp_f64(pT)
+                                    : num * rcx::rcp_f64(Wp * S[k]);
           c.D[k * c.ld + i] = Dk;
           bad |= !isfinite(Dk);
         }
