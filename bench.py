@@ -294,7 +294,7 @@ def run_ours(a):
             "data": "synthetic (seeded manifold states, random-init paper-shape MLP weights)",
             "config": {"workload": f"{cfg.name}: {cfg.note}", "cells_per_gpu": int(n), "cells_total": int(total_cells),
                        "mech": cfg.mech, "hidden": list(cfg.hidden), "nets": nets, "parallelism": f"cells dp{world}",
-                       "l2": "working set > L2 (1M cells x 8 nets activations in 32768-cell chunks ~0.9 GB; "
+                       "l2": "working set > L2 (activations of 131072-cell chunks x 8 nets ~5 GB; "
                              "cell state 0.2 GB) - no flush needed",
                        "precision": a.precision},
             "roofline": {"kernel": "L2 GEMM (h1 1600 -> h2 800, tcgen05 bf16)", "bound": "tensor",

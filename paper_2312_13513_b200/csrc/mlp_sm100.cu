@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -31,7 +32,17 @@
 namespace {
 
 constexpr int BM = 128;       // UMMA M (one CTA, cta_group::1)
-constexpr int MAX_CAP = 32768;     // cells per chunk (activation working set)
+// cells per chunk (the activation working set: ~39 KB per cell for the paper MLP in bf16, 5 GB at
+// 131072 cells; larger chunks amortise the per-chunk prologue/epilogue launches and tails)
+int max_cap() {
+  static int v = [] {
+    const char *e = getenv("RC_MAX_CAP");  // experiments (tools/capvar.sh)
+    int x = e ? atoi(e) : 131072;
+    return x < 256 ? 256 : x / 256 * 256;
+  }();
+  return v;
+}
+#define MAX_CAP max_cap()
 constexpr int QPART_BLOCKS = 148 * 4;
 
 
