@@ -144,12 +144,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
         const int pass = tile % a.passes, rest = tile / a.passes;
         const int mp = rest % pairs, net = rest / pairs;
         const int zb = it & 1;
-        rcx::mbar_wait(&bempty[zb], ((it >> 1) & 1) ^ 1);  // b2 slice for this CTA's drain
+        rcx::mbar_wait_sleep(&bempty[zb], ((it >> 1) & 1) ^ 1);  // b2 slice for this CTA's drain
         rcx::mbar_arrive_expect_tx(&bfull[zb], VEC * 4);
         rcx::bulk_g2s(sB2 + zb * VEC, a.bias + (size_t)net * a.N + pass * NP, NP * 4, &bfull[zb]);
         if (DOT) rcx::bulk_g2s(sB2 + zb * VEC + NP, a.w4 + (size_t)net * a.N + pass * NP, NP * 4, &bfull[zb]);
         for (int c = 0; c < C; ++c) {
-          rcx::mbar_wait(&empty[s], ph ^ 1);
+          rcx::mbar_wait_sleep(&empty[s], ph ^ 1);
           rcx::mbar_arrive_expect_tx_cluster(full0 + s * 8, A_BYTES + B_BYTES);
           uint8_t *st = sW + s * STAGE;
           rcx::tma_load_3d_pair(st, &mapA, &full[s], c * KC, mp * 256 + rank * 128, net);
@@ -204,7 +204,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
       const int pass = tile % a.passes, rest = tile / a.passes;
       const int mp = rest % pairs, net = rest / pairs;
       TRACE(warp, it, 0);
+#ifdef L2_EPI_SPIN
       rcx::mbar_wait(c2full, it & 1);
+#else
+      rcx::mbar_wait_sleep(c2full, it & 1);  // parked for the whole mainloop: leave issue slots and power to the rest
+#endif
       TRACE(warp, it, 1);
       rcx::mbar_wait(&bfull[it & 1], (it >> 1) & 1);
       rcx::tc_fence_after();
