@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(L1_THREADS, 1)
     }
     for (int z = 0; z < 2; ++z) {
       rcx::mbar_init(&tfull[z], 1);
-      rcx::mbar_init(&tempty[z], NEPI);
+      rcx::mbar_init(&tempty[z], TF32 ? NEPI : NEPI / 2);  // bf16: one warp group per accumulator
     }
     rcx::fence_mbar_init();
   }
@@ -146,7 +146,64 @@ __global__ void __launch_bounds__(L1_THREADS, 1)
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
-  } else {  // ---------------- epilogue warps 0..15: 32 rows (lane quadrant q) x 64 columns (block sub)
+  } else if constexpr (!TF32) {
+    // ---------------- bf16 epilogue: two groups of eight warps take alternate tiles (group g drains
+    // accumulator g), so one group's TMA-store phase overlaps the other's GELU phase instead of all
+    // sixteen warps of an SM sub-partition pausing the MUFU pipe together.  In a group, warp
+    // (q, hb) converts rows q*32.. and columns hb*128.. as two 64-column blocks; it releases the
+    // accumulator after loading its second block.
+    const int g = warp >> 3, q = warp & 3, hb = (warp >> 2) & 1;
+    uint8_t *stg0 = sST + warp * NSLOT * SLOT;
+    int it = 0, nst = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+      if ((it & 1) != g) continue;
+      const int nb = tile % a.n_tiles, rest = tile / a.n_tiles;
+      const int mb = rest % a.m_tiles, net = rest / a.m_tiles;
+      const int n_eff = min(BN, a.N - nb * BN);
+      const int nblk = max(0, min(2, (n_eff - hb * 128) / 64));  // this warp's 64-column blocks: 0..2
+      wait<8>(&tfull[g], (it >> 1) & 1);
+      rcx::tc_fence_after();
+      if (nblk == 0) {
+        rcx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) rcx::mbar_arrive(&tempty[g]);
+        continue;
+      }
+#pragma unroll 1
+      for (int j = 0; j < nblk; ++j) {
+        uint32_t v[4][16];
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + g * BN + hb * 128 + j * 64;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) rcx::tmem_ld16(ta + c * 16, v[c]);
+        rcx::tmem_ld_wait();
+        if (j == nblk - 1) {  // all of this warp's columns are out of TMEM
+          rcx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) rcx::mbar_arrive(&tempty[g]);
+        }
+        uint8_t *stg = stg0 + (nst & 1) * SLOT;
+        if (lane == 0) rcm::bulk_wait_read1();  // the store that last used this slot has read it
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            pk[k] = rcm::gelu_half_bf16x2(rcm::cvt_bf16x2(__uint_as_float(v[c][2 * k]), __uint_as_float(v[c][2 * k + 1])));
+          rcm::stage_sw128(stg, lane, 2 * c, pk);
+        }
+        rcm::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          rcm::tma_store_3d(&mapOut, stg, nb * BN + hb * 128 + j * 64, mb * BM + q * 32, net);
+          rcm::bulk_commit();
+        }
+        ++nst;
+      }
+    }
+    if (lane == 0) rcm::bulk_wait_all();
+    __syncwarp();
+  } else {  // ---------------- TF32 epilogue, warps 0..15: 32 rows (lane quadrant q) x 64 columns (block sub)
     const int q = warp & 3, sub = warp >> 2;
     uint8_t *stg0 = sST + warp * NSLOT * SLOT;
     int it = 0, nst = 0;
