@@ -122,7 +122,7 @@ void rc_mlp_destroy(rc_mlp *n);
 
 /* ---------------------------------------------------------------------------
  * Cell state: caller-owned DEVICE arrays, component-major (field[k*ld + c]).
- * Every pointer 16-byte aligned; ld >= n and ld even.  Output pointers may be
+ * Every array pointer 16-byte aligned (red / diag: 8-byte); ld >= n and ld even.  Output pointers may be
  * NULL to skip that output (the stage still runs if any of its outputs is
  * requested).  Inputs are never written except T (h-mode: in = guess, out =
  * converged) and h (T-mode: out).
@@ -169,6 +169,16 @@ int rc_chem(const rc_mech *m, const rc_mlp *n, const rc_cells *c, void *ws, size
 
 /* a1 + a2 + a3-a5 in order on one stream; zeroes red and diag first. */
 int rc_step(const rc_mech *m, const rc_mlp *n, const rc_cells *c, void *ws, size_t ws_bytes, void *stream);
+
+/* Step a6 on one device for a step run as k sub-batches (e.g. to overlap the host
+ * copies of one batch with the compute of another, each rc_step writing its own
+ * red/diag): red = {max_i red_parts[i][0], sum_i red_parts[i][1]} (sum in index
+ * order, Neumaier-compensated), diag[j] = sum_i diag_parts[i][j].  Device
+ * pointers: red_parts [k][2] fp64, diag_parts [k][RC_DIAG_COUNT] int64 (NULL
+ * with diag NULL skips the counters); asynchronous on `stream`.
+ * Errors: RC_EINVAL (k < 1, NULL red/red_parts), RC_ECUDA. */
+int rc_combine_reductions(const double *red_parts, const int64_t *diag_parts, int k, double *red, int64_t *diag,
+                          void *stream);
 
 /* Multi-GPU block partition: rank r of world G gets
  * [begin, end) with boundaries floor(r N / G) rounded down to 128 cells (the

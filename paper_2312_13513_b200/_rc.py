@@ -58,6 +58,7 @@ EXPORTS = {
     "rc_chem": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(rc_cells), C.c_void_p, C.c_size_t, C.c_void_p]),
     "rc_step": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(rc_cells), C.c_void_p, C.c_size_t, C.c_void_p]),
     "rc_partition": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "rc_combine_reductions": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     "rc_last_launch_count": (C.c_int64, []),
     "rc_profile_enable": (C.c_int, [C.c_int]),
     "rc_profile_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
@@ -186,6 +187,12 @@ def rc_step(mech, mlp, cells, ws, stream=None):
     return check(lib().rc_step(mech.h, mlp.h if mlp is not None else None, C.byref(cells),
                                _ptr(ws) if ws is not None else None,
                                (ws.numel() * ws.element_size()) if ws is not None else 0, _stream(stream)))
+
+
+def rc_combine_reductions(red_parts, diag_parts, red, diag, stream=None):
+    """a6 over k sub-batches: red_parts [k][2] fp64, diag_parts [k][5] int64 (device tensors)."""
+    return check(lib().rc_combine_reductions(_ptr(red_parts), _ptr(diag_parts), int(red_parts.shape[0]), _ptr(red),
+                                             _ptr(diag), _stream(stream)))
 
 
 def rc_last_launch_count():

@@ -290,10 +290,11 @@ static int check_cells(const rc_mech *m, const rc_cells *c, CellsDev &o) {
   if (c->mode != RC_MODE_H && c->mode != RC_MODE_T) return rc_fail(RC_EINVAL, "mode must be RC_MODE_H or RC_MODE_T");
   if (!c->T || !c->p || !c->Y) return rc_fail(RC_EINVAL, "T, p and Y are required");
   if (c->mode == RC_MODE_H && !c->h) return rc_fail(RC_EINVAL, "h-mode needs h");
-  const void *ptrs[] = {c->h, c->T, c->p, c->Y, c->cp, c->rho, c->mu, c->lambda, c->D, c->wdot, c->qdot, c->o,
-                        c->red, c->diag};
+  const void *ptrs[] = {c->h, c->T, c->p, c->Y, c->cp, c->rho, c->mu, c->lambda, c->D, c->wdot, c->qdot, c->o};
   for (const void *p : ptrs)
     if (p && !aligned16(p)) return rc_fail(RC_EALIGN, "cell arrays must be 16-byte aligned");
+  if (((uintptr_t)c->red & 7u) || ((uintptr_t)c->diag & 7u))  // 64-bit atomics only
+    return rc_fail(RC_EALIGN, "red / diag must be 8-byte aligned");
   o = CellsDev{c->n, c->ld, c->mode, c->h, c->T, c->p, c->Y, c->cp, c->rho, c->mu, c->lambda, c->D, c->wdot,
                c->qdot, c->o, c->red, c->diag};
   return RC_OK;
@@ -369,6 +370,13 @@ extern "C" int rc_step(const rc_mech *m, const rc_mlp *n, const rc_cells *c, voi
   rc_reset_launches();
   rc_count_launch((int)total);
   return RC_OK;
+}
+
+extern "C" int rc_combine_reductions(const double *red_parts, const int64_t *diag_parts, int k, double *red,
+                                     int64_t *diag, void *stream) {
+  if (k < 1 || !red_parts || !red) return rc_fail(RC_EINVAL, "rc_combine_reductions: bad arguments");
+  rc_reset_launches();
+  return launch_combine_reductions(red_parts, diag_parts, k, red, diag, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int rc_partition(int64_t n_global, int rank, int world, int64_t *begin, int64_t *end) {

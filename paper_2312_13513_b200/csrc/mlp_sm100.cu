@@ -219,6 +219,25 @@ __global__ void __launch_bounds__(256) chem_epilogue_kernel(EpiArgs a, CellsDev 
   }
 }
 
+// step a6 over k sub-batch reductions (rc_combine_reductions): one thread, index order
+__global__ void combine_reductions_kernel(const double *rp, const int64_t *dp, int k, double *red, int64_t *diag) {
+  double mx = 0.0, S = 0.0, C = 0.0;
+  for (int i = 0; i < k; ++i) {
+    mx = fmax(mx, rp[2 * i]);
+    const double v = rp[2 * i + 1], t = S + v;
+    C += (fabs(S) >= fabs(v)) ? (S - t) + v : (v - t) + S;
+    S = t;
+  }
+  red[0] = mx;
+  red[1] = S + C;
+  if (diag && dp)
+    for (int j = 0; j < RC_DIAG_COUNT; ++j) {
+      int64_t a = 0;
+      for (int i = 0; i < k; ++i) a += dp[i * RC_DIAG_COUNT + j];
+      diag[j] = a;
+    }
+}
+
 __global__ void qdot_finalize_kernel(const double *qpart, int n, double *out) {
   // one warp, Neumaier-compensated, fixed order
   __shared__ double ss[32], sc[32];
@@ -334,6 +353,13 @@ uint16_t f2bf(float f) {  // round-to-nearest-even float -> bf16 bits
 }
 
 }  // namespace
+
+int launch_combine_reductions(const double *rp, const int64_t *dp, int k, double *red, int64_t *diag, cudaStream_t s) {
+  ProfScope prof(RC_STAGE_FINALIZE, s);
+  combine_reductions_kernel<<<1, 1, 0, s>>>(rp, dp, k, red, diag);
+  RC_LAUNCH_CHECK();
+  return RC_OK;
+}
 
 size_t chem_workspace_bytes(const rc_mech *, const rc_mlp *n, int64_t ncells) {
   int64_t cap = (ncells + 255) / 256 * 256;  // chunks of CTA-pair (256-row) tiles

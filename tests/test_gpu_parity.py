@@ -221,3 +221,38 @@ def test_sharded_equals_unsharded_bitwise():
                 assert np.array_equal(g[k], whole[k][b:e]), (k, world, r)
             for k in ("D", "wdot", "o"):
                 assert np.array_equal(g[k], whole[k][:, b:e]), (k, world, r)
+
+
+def test_sub_batches_in_place_and_combined_reductions():
+    """One step run as three sub-batches on views of the same component-major arrays
+    (pointer offsets, shared ld), each with its own red/diag, then rc_combine_reductions:
+    per-cell outputs bitwise equal to the single call, T_max exact, sum qdot to rounding."""
+    import torch
+    import paper_2312_13513_b200 as rc
+    c = inputs("C1")
+    G = Gpu("C1")
+    whole = G.run(c)
+    n = c["p"].shape[0]
+    st = rc.CellState(n, G.ns, G.n_nets).load(c["T_guess"], c["p"], c["Y"], h=c["h"])
+    ws = rc.aligned_workspace(G.mlp, n)
+    parts = [(0, 384), (384, 768), (768, n)]
+    red_parts = torch.zeros(len(parts), 2, dtype=torch.float64, device="cuda")
+    diag_parts = torch.zeros(len(parts), 5, dtype=torch.int64, device="cuda")
+    for i, (b, e) in enumerate(parts):
+        cells = rc.make_cells(e - b, st.ld, rc.RC_MODE_H, st.T[b:], st.p[b:], st.Y[:, b:], h=st.h[b:], cp=st.cp[b:],
+                              rho=st.rho[b:], mu=st.mu[b:], lam=st.lam[b:], D=st.D[:, b:], wdot=st.wdot[:, b:],
+                              qdot=st.qdot[b:], o=st.o[:, b:], dt=G.dt, red=red_parts[i], diag=diag_parts[i])
+        rc.rc_step(G.mech, G.mlp, cells, ws)
+    red = torch.zeros(2, dtype=torch.float64, device="cuda")
+    diag = torch.zeros(5, dtype=torch.int64, device="cuda")
+    rc.rc_combine_reductions(red_parts, diag_parts, red, diag)
+    torch.cuda.synchronize()
+    g = st.host()
+    for k, gk in (("T", "T"), ("cp", "cp"), ("rho", "rho"), ("mu", "mu"), ("lambda", "lam"), ("qdot", "qdot")):
+        assert np.array_equal(g[gk], whole[k]), k
+    for k in ("D", "wdot", "o"):
+        assert np.array_equal(g[k], whole[k]), k
+    r = red.cpu().numpy()
+    assert r[0] == whole["red"][0]
+    assert r[1] == pytest.approx(whole["red"][1], rel=1e-13)
+    assert np.array_equal(diag.cpu().numpy(), whole["diag"])
