@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "tf32"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "tf32", "tf32x3"])
     ap.add_argument("--strong", action="store_true", help="partition the config's cells (strong scaling)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -184,7 +184,7 @@ def run_ours(a):
     mech_d = load_mech(cfg.mech)
     bundle = make_bundle(cfg.mech, hidden=cfg.hidden)
     mech = rc.Mechanism(mech_d)
-    prec = rc.RC_BF16 if a.precision == "bf16" else rc.RC_TF32
+    prec = {"bf16": rc.RC_BF16, "tf32": rc.RC_TF32, "tf32x3": rc.RC_TF32X3}[a.precision]
     mlp = rc.MLPBundle(mech, bundle, prec)
     ns, nets = mech_d["ns"], bundle["n_nets"]
     idx, n_global = local_cells(cfg, rank, world, a.strong)

@@ -52,7 +52,7 @@ enum {
 };
 
 enum { RC_MODE_H = 0, RC_MODE_T = 1 };               /* rc_cells.mode */
-enum { RC_BF16 = 0, RC_TF32 = 1 };                    /* rc_mlp_desc.precision */
+enum { RC_BF16 = 0, RC_TF32 = 1, RC_TF32X3 = 2 };     /* rc_mlp_desc.precision */
 
 /* Diagnostic counters in rc_cells.diag[] (int64, accumulated with atomics). */
 enum {
@@ -114,7 +114,10 @@ typedef struct {
   int32_t precision;              /* RC_BF16: bf16 operands and activations, fp32 accumulate, tanh-form
                                      GELU (north_star gate 2e-2 on o);
                                      RC_TF32: tf32-rounded fp32 operands and activations, fp32
-                                     accumulate, exact-erf GELU (gate 1e-3 on o) */
+                                     accumulate, exact-erf GELU (gate 1e-3 on o);
+                                     RC_TF32X3: fp32-accurate GEMMs as three tf32 MMAs per product
+                                     (a_hi b_hi + a_lo b_hi + a_hi b_lo), activations kept as tf32
+                                     hi/lo pairs, exact-erf GELU (gate 1e-3 on o and wdot) */
 } rc_mlp_desc;
 
 int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *desc, rc_mlp **out);

@@ -11,11 +11,11 @@ PyTorch is used only for device memory, streams and torch.distributed.
 import numpy as np
 
 from . import _rc
-from ._rc import (RC_BF16, RC_TF32, RC_MODE_H, RC_MODE_T, DIAG_NAMES, Mechanism, MLPBundle, RcError, lib,
+from ._rc import (RC_BF16, RC_TF32, RC_TF32X3, RC_MODE_H, RC_MODE_T, DIAG_NAMES, Mechanism, MLPBundle, RcError, lib,
                   make_cells, rc_chem, rc_combine_reductions, rc_last_launch_count, rc_partition, rc_profile_enable, rc_profile_read, rc_step,
                   rc_thermo, rc_transport, STAGES)
 
-__all__ = ["Mechanism", "MLPBundle", "CellState", "RcError", "RC_BF16", "RC_TF32", "RC_MODE_H", "RC_MODE_T",
+__all__ = ["Mechanism", "MLPBundle", "CellState", "RcError", "RC_BF16", "RC_TF32", "RC_TF32X3", "RC_MODE_H", "RC_MODE_T",
            "rc_step", "rc_thermo", "rc_transport", "rc_chem", "rc_partition", "rc_combine_reductions",
            "rc_last_launch_count", "lib",
            "DIAG_NAMES", "make_cells", "rc_profile_enable", "rc_profile_read", "STAGES", "aligned_workspace"]

@@ -15,7 +15,7 @@ SO = os.path.join(HERE, "librc_b200.so")
 
 RC_OK, RC_EINVAL, RC_ENOMEM, RC_ECUDA, RC_EALIGN, RC_EUNSUPPORTED, RC_EDTMISMATCH = 0, -1, -2, -3, -4, -5, -6
 RC_MODE_H, RC_MODE_T = 0, 1
-RC_BF16, RC_TF32 = 0, 1
+RC_BF16, RC_TF32, RC_TF32X3 = 0, 1, 2
 DIAG_NAMES = ["newton_bisect", "newton_maxit", "nonfinite", "negY_in", "negY_out"]
 
 

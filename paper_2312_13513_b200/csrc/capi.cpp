@@ -236,7 +236,7 @@ extern "C" int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *d, rc_mlp **ou
   const int h1 = d->hidden[0], h2 = d->hidden[1], h3 = d->hidden[2];
   if (h1 < 64 || h2 < 16 || h3 < 16 || h1 % 64 || h2 % 16 || h3 % 16 || h1 > 4096 || h2 > 4096 || h3 > 4096)
     return rc_fail(RC_EUNSUPPORTED, "rc_mlp_create: hidden (%d,%d,%d) must be multiples of (64,16,16)", h1, h2, h3);
-  if (d->precision != RC_BF16 && d->precision != RC_TF32)
+  if (d->precision != RC_BF16 && d->precision != RC_TF32 && d->precision != RC_TF32X3)
     return rc_fail(RC_EINVAL, "rc_mlp_create: unknown precision %d", d->precision);
   if (!(d->lambda_bc > 0.0) || !(d->dt > 0.0)) return rc_fail(RC_EINVAL, "rc_mlp_create: lambda and dt must be > 0");
   double inv = 1.0 / d->lambda_bc;
@@ -272,7 +272,7 @@ extern "C" int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *d, rc_mlp **ou
 
 extern "C" void rc_mlp_destroy(rc_mlp *n) {
   if (!n) return;
-  void *ptrs[] = {n->d_W1, n->d_W2, n->d_W3, n->d_b1, n->d_b2, n->d_b3, n->d_w4, n->d_b4,
+  void *ptrs[] = {n->d_W1, n->d_W2, n->d_W3, n->d_W1lo, n->d_W2lo, n->d_W3lo, n->d_b1, n->d_b2, n->d_b3, n->d_w4, n->d_b4,
                   n->d_xmean, n->d_xinvstd, n->d_ymean, n->d_ystd, n->d_species};
   for (void *p : ptrs) cudaFree(p);
   delete n;

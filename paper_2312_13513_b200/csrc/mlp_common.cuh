@@ -65,6 +65,15 @@ struct Elem {
   static constexpr int KATOM = TF32 ? 8 : 16;
   static constexpr uint32_t FMT = TF32 ? 2u : 1u;  // instruction-descriptor a/b format
 };
+// precision modes of the MLP GEMMs (rc_mlp_desc.precision): 0 bf16, 1 tf32, 2 tf32x3
+// (fp32-accurate: a_hi b_hi + a_lo b_hi + a_hi b_lo with tf32 hi/lo operand pairs)
+template <int PREC>
+struct Prec {
+  static constexpr bool TF32 = PREC != 0;
+  static constexpr bool X3 = PREC == 2;
+  static constexpr int NOP = X3 ? 2 : 1;  // operand copies per tile (hi, lo)
+};
+
 template <bool TF32>
 __device__ __forceinline__ void mma_cta(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   if constexpr (TF32) rcx::mma_tf32(d, a, b, idesc, acc); else rcx::mma_bf16(d, a, b, idesc, acc);

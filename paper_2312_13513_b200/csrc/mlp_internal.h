@@ -15,8 +15,8 @@ struct L1Args {
 };
 int l1_tile_n();
 int l1_box_rows();
-int launch_l1(int KZ, bool tf32, const CUtensorMap &Z, const CUtensorMap &W, const CUtensorMap &Out, const L1Args &a,
-              cudaStream_t s);
+// maps: {z, W1, h1 store, z lo, W1 lo, h1 lo store} (the lo maps are used by precision 2 only)
+int launch_l1(int KZ, int prec, const CUtensorMap *maps, const L1Args &a, cudaStream_t s);
 int l2_pass_width(int h2);
 
 struct L2Args {
@@ -26,5 +26,5 @@ struct L2Args {
   float *opart;            // layer-3 mode: [nets][passes*4][cap] partial dots
   int cap;
 };
-int launch_l2_pair(int NP, bool tf32, const CUtensorMap &A, const CUtensorMap &Ba, const CUtensorMap &Bb, const CUtensorMap &Out,
-                   const L2Args &a, cudaStream_t s);
+// maps: {A, B piece 1, B piece 2, out store, A lo, B1 lo, B2 lo, out lo store} (lo: precision 2 only)
+int launch_l2_pair(int NP, int prec, const CUtensorMap *maps, const L2Args &a, cudaStream_t s);

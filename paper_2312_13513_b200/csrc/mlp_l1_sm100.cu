@@ -21,6 +21,8 @@
 // TF32 precision mode (RC_TF32): fp32 z/W1 (tf32-rounded) with kind::tf32 MMAs,
 // exact-erf GELU in fp32, fp32 h1 rounded to tf32; each warp's 32 x 64 block is
 // staged as two 32 x 32 fp32 swizzled blocks (one 8 KB slot per warp).
+// RC_TF32X3: z, W1 and h1 as tf32 hi/lo pairs, three MMAs per K atom
+// (z_hi W_hi + z_lo W_hi + z_hi W_lo); h1 hi and lo are stored one after the other.
 // Warps: 0..15 epilogue, 16 TMA producer, 17 MMA issuer.
 #include <cuda_bf16.h>
 
@@ -63,17 +65,20 @@ __device__ __forceinline__ void wait(uint64_t *bar, uint32_t phase) {
     rcx::mbar_wait(bar, phase);
 }
 
-template <int KZ, bool TF32>
+template <int KZ, int PREC>
 __global__ void __launch_bounds__(L1_THREADS, 1)
     l1_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapW,
-              const __grid_constant__ CUtensorMap mapOut, L1Args a) {
+              const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ CUtensorMap mapZlo,
+              const __grid_constant__ CUtensorMap mapWlo, const __grid_constant__ CUtensorMap mapOutlo, L1Args a) {
   static_assert(KZ == 16 || KZ == 32, "z row of 16 or 32 elements");
+  constexpr bool TF32 = rcm::Prec<PREC>::TF32, X3 = rcm::Prec<PREC>::X3;
+  constexpr int NOP = rcm::Prec<PREC>::NOP;
   using E = rcm::Elem<TF32>;
   constexpr int ROWB = KZ * E::BYTES;  // 32, 64 or 128-byte swizzled operand rows
   constexpr uint32_t SLOT = L1Stg<TF32>::SLOT;
   constexpr int NSLOT = L1Stg<TF32>::NSLOT;
   constexpr uint32_t A_BYTES = BM * ROWB, B_BYTES = BN * ROWB;
-  constexpr uint32_t STAGE = (A_BYTES + B_BYTES + 1023u) & ~1023u;
+  constexpr uint32_t STAGE = (NOP * (A_BYTES + B_BYTES) + 1023u) & ~1023u;  // [A hi | A lo | B hi | B lo]
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = rcx::smem_u32(smem_raw);
   uint8_t *smem = smem_raw + (((base_u32 + 1023u) & ~1023u) - base_u32);
@@ -89,6 +94,11 @@ __global__ void __launch_bounds__(L1_THREADS, 1)
     rcx::prefetch_tmap(&mapZ);
     rcx::prefetch_tmap(&mapW);
     rcx::prefetch_tmap(&mapOut);
+    if (X3) {
+      rcx::prefetch_tmap(&mapZlo);
+      rcx::prefetch_tmap(&mapWlo);
+      rcx::prefetch_tmap(&mapOutlo);
+    }
     for (int s = 0; s < S; ++s) {
       rcx::mbar_init(&full[s], 1);
       rcx::mbar_init(&empty[s], 1);
@@ -114,9 +124,12 @@ __global__ void __launch_bounds__(L1_THREADS, 1)
         const int nb = tile % a.n_tiles, rest = tile / a.n_tiles;
         const int mb = rest % a.m_tiles, net = rest / a.m_tiles;
         wait<1>(&empty[s], ph ^ 1);
-        rcx::mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
-        rcx::tma_load_3d(sW + s * STAGE, &mapZ, &full[s], 0, mb * BM, 0);
-        rcx::tma_load_3d(sW + s * STAGE + A_BYTES, &mapW, &full[s], 0, nb * BN, net);
+        rcx::mbar_arrive_expect_tx(&full[s], NOP * (A_BYTES + B_BYTES));
+        uint8_t *st = sW + s * STAGE;
+        rcx::tma_load_3d(st, &mapZ, &full[s], 0, mb * BM, 0);
+        if (X3) rcx::tma_load_3d(st + A_BYTES, &mapZlo, &full[s], 0, mb * BM, 0);
+        rcx::tma_load_3d(st + NOP * A_BYTES, &mapW, &full[s], 0, nb * BN, net);
+        if (X3) rcx::tma_load_3d(st + NOP * A_BYTES + B_BYTES, &mapWlo, &full[s], 0, nb * BN, net);
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
@@ -137,10 +150,16 @@ __global__ void __launch_bounds__(L1_THREADS, 1)
         TRACE(W_MMA, it, 2);
         rcx::tc_fence_after();
         const uint64_t ad = rcm::desc_sw<ROWB>(sW + s * STAGE);
-        const uint64_t bd = rcm::desc_sw<ROWB>(sW + s * STAGE + A_BYTES);
+        const uint64_t bd = rcm::desc_sw<ROWB>(sW + s * STAGE + NOP * A_BYTES);
+        constexpr uint64_t ALO = A_BYTES >> 4, BLO = B_BYTES >> 4;  // descriptor offsets of the lo copies
 #pragma unroll
-        for (int k = 0; k < KZ / E::KATOM; ++k)  // one 32-byte K atom per MMA: descriptor start += 2
+        for (int k = 0; k < KZ / E::KATOM; ++k) {  // one 32-byte K atom per MMA: descriptor start += 2
           rcm::mma_cta<TF32>(tmem + as * BN, ad + 2 * k, bd + 2 * k, idesc, k != 0);
+          if (X3) {
+            rcm::mma_cta<TF32>(tmem + as * BN, ad + ALO + 2 * k, bd + 2 * k, idesc, 1);
+            rcm::mma_cta<TF32>(tmem + as * BN, ad + 2 * k, bd + BLO + 2 * k, idesc, 1);
+          }
+        }
         rcx::mma_commit(&empty[s]);
         rcx::mma_commit(&tfull[as]);
         if (++s == S) { s = 0; ph ^= 1; }
@@ -234,7 +253,8 @@ __global__ void __launch_bounds__(L1_THREADS, 1)
       }
       __syncwarp();
       if constexpr (TF32) {
-        // exact GELU in fp32, tf32-rounded; [32 rows][32 fp32] blocks, 128-byte swizzle
+        // exact GELU in fp32, tf32-rounded (X3: hi now, lo after the hi stores have read the slot);
+        // [32 rows][32 fp32] blocks, 128-byte swizzle
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           float g[16];
@@ -245,6 +265,31 @@ __global__ void __launch_bounds__(L1_THREADS, 1)
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             *reinterpret_cast<float4 *>(r + (((u0 + u) ^ x) << 4)) = make_float4(g[4 * u], g[4 * u + 1], g[4 * u + 2], g[4 * u + 3]);
+        }
+        if constexpr (X3) {
+          rcm::fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            rcm::tma_store_3d(&mapOut, stg, nb * BN + sub * 64, mb * BM + q * 32, net);
+            rcm::tma_store_3d(&mapOut, stg + 4096, nb * BN + sub * 64 + 32, mb * BM + q * 32, net);
+            rcm::bulk_commit();
+            rcm::bulk_wait_read0();
+          }
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float g[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float y = rcm::gelu_erf_f32(__uint_as_float(v[c][j]));
+              g[j] = rcm::tf32_rn(y - rcm::tf32_rn(y));
+            }
+            uint8_t *r = stg + (c >> 1) * 4096 + lane * 128;
+            const int x = lane & 7, u0 = (c & 1) * 4;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              *reinterpret_cast<float4 *>(r + (((u0 + u) ^ x) << 4)) = make_float4(g[4 * u], g[4 * u + 1], g[4 * u + 2], g[4 * u + 3]);
+          }
         }
       } else {
 #pragma unroll
@@ -261,8 +306,9 @@ __global__ void __launch_bounds__(L1_THREADS, 1)
       TRACE(warp, it, 3);
       if (lane == 0) {
         if constexpr (TF32) {
-          rcm::tma_store_3d(&mapOut, stg, nb * BN + sub * 64, mb * BM + q * 32, net);
-          rcm::tma_store_3d(&mapOut, stg + 4096, nb * BN + sub * 64 + 32, mb * BM + q * 32, net);
+          const CUtensorMap *mo = X3 ? &mapOutlo : &mapOut;  // X3: the hi half was stored above
+          rcm::tma_store_3d(mo, stg, nb * BN + sub * 64, mb * BM + q * 32, net);
+          rcm::tma_store_3d(mo, stg + 4096, nb * BN + sub * 64 + 32, mb * BM + q * 32, net);
         } else {
           rcm::tma_store_3d(&mapOut, stg, nb * BN + sub * 64, mb * BM + q * 32, net);
         }
@@ -280,10 +326,11 @@ __global__ void __launch_bounds__(L1_THREADS, 1)
   }
 }
 
-template <int KZ, bool TF32>
-int launch_t(const CUtensorMap &Z, const CUtensorMap &W, const CUtensorMap &Out, L1Args a, cudaStream_t s) {
+template <int KZ, int PREC>
+int launch_t(const CUtensorMap *M, L1Args a, cudaStream_t s) {
+  constexpr bool TF32 = PREC != 0;
   constexpr int EB = rcm::Elem<TF32>::BYTES;
-  constexpr size_t STAGE = ((BM * KZ * EB + BN * KZ * EB) + 1023) & ~(size_t)1023;
+  constexpr size_t STAGE = (rcm::Prec<PREC>::NOP * (BM * KZ * EB + BN * KZ * EB) + 1023) & ~(size_t)1023;
   const size_t fixed = 1024 + NEPI * L1Stg<TF32>::NSLOT * L1Stg<TF32>::SLOT + 256;
   int stages = (int)((232448 - fixed) / STAGE);
   if (stages > 8) stages = 8;
@@ -291,12 +338,12 @@ int launch_t(const CUtensorMap &Z, const CUtensorMap &W, const CUtensorMap &Out,
   const size_t smem = fixed + stages * STAGE;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(l1_kernel<KZ, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaFuncSetAttribute(l1_kernel<KZ, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     attr = true;
   }
   const int total = a.m_tiles * a.n_tiles * a.nets;
   const int grid = total < mlp_num_sms() ? total : mlp_num_sms();
-  l1_kernel<KZ, TF32><<<grid, L1_THREADS, smem, s>>>(Z, W, Out, a);
+  l1_kernel<KZ, PREC><<<grid, L1_THREADS, smem, s>>>(M[0], M[1], M[2], M[3], M[4], M[5], a);
   RC_LAUNCH_CHECK();
   return RC_OK;
 }
@@ -312,11 +359,14 @@ extern "C" __attribute__((visibility("default"))) int rc_debug_l1trace(void *hos
 }
 #endif
 
-int launch_l1(int KZ, bool tf32, const CUtensorMap &Z, const CUtensorMap &W, const CUtensorMap &Out, const L1Args &a,
-              cudaStream_t s) {
+int launch_l1(int KZ, int prec, const CUtensorMap *maps, const L1Args &a, cudaStream_t s) {
   ProfScope prof(RC_STAGE_L1, s);
   if (a.N % 64) return rc_fail(RC_EUNSUPPORTED, "layer-1 GEMM: h1 = %d is not a multiple of 64", a.N);
-  if (KZ == 16) return tf32 ? launch_t<16, true>(Z, W, Out, a, s) : launch_t<16, false>(Z, W, Out, a, s);
-  if (KZ == 32) return tf32 ? launch_t<32, true>(Z, W, Out, a, s) : launch_t<32, false>(Z, W, Out, a, s);
+#define RC_L1(kz)                                                                                      \
+  if (KZ == kz)                                                                                        \
+    return prec == 0 ? launch_t<kz, 0>(maps, a, s) : prec == 1 ? launch_t<kz, 1>(maps, a, s) : launch_t<kz, 2>(maps, a, s);
+  RC_L1(16)
+  RC_L1(32)
+#undef RC_L1
   return rc_fail(RC_EUNSUPPORTED, "layer-1 GEMM: no instance for K = %d", KZ);
 }

@@ -41,9 +41,12 @@ namespace {
 
 constexpr int NEPI = 16;
 constexpr int L2_THREADS = 32 * NEPI + 64;
-// K chunk = one 128-byte swizzle row: 64 bf16 or 32 fp32 (tf32) elements
-template <bool TF32>
-constexpr int kc() { return 128 / rcm::Elem<TF32>::BYTES; }
+// K chunk = one swizzled operand row: 128 B = 64 bf16 or 32 fp32 (tf32) elements; 64 B = 16 fp32
+// for tf32x3, whose stages hold a hi and a lo copy of each operand
+template <int PREC>
+constexpr int row_bytes() { return PREC == 2 ? 64 : 128; }
+template <int PREC>
+constexpr int kc() { return row_bytes<PREC>() / rcm::Elem<(PREC != 0)>::BYTES; }
 // store staging per warp: [32 rows][16 cols] = 1 KB bf16 / 2 KB fp32, two slots
 template <bool TF32>
 constexpr uint32_t stg_bytes() { return 32 * 16 * rcm::Elem<TF32>::BYTES; }
@@ -56,7 +59,6 @@ using rcm::fence_async_smem;
 using rcm::gelu_bf16x2;
 using rcm::tma_store_3d;
 using rcm::tmem_ld32;
-__device__ __forceinline__ uint64_t desc_sw128(const void *smem) { return rcm::desc_sw<128>(smem); }
 __device__ __forceinline__ uint32_t cvt_f16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
@@ -82,19 +84,23 @@ __device__ long long g_l2trace[2][20][TR_TILES][4];  // [DOT][warp][tile][event]
   } while (0)
 #endif
 
-template <int NP, bool DOT, bool TF32>
+template <int NP, bool DOT, int PREC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     l2_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBa,
-                   const __grid_constant__ CUtensorMap mapBb, const __grid_constant__ CUtensorMap mapOut, L2Args a) {
+                   const __grid_constant__ CUtensorMap mapBb, const __grid_constant__ CUtensorMap mapOut,
+                   const __grid_constant__ CUtensorMap mapAlo, const __grid_constant__ CUtensorMap mapBalo,
+                   const __grid_constant__ CUtensorMap mapBblo, const __grid_constant__ CUtensorMap mapOutlo, L2Args a) {
   static_assert(NP % 16 == 0 && NP <= 512, "pass width");
   constexpr int P1 = NP > 256 ? 256 : NP, P2 = NP - P1;
   constexpr int H1 = P1 / 2, H2 = P2 / 2;  // B rows per CTA of each piece
   static_assert(H1 % 8 == 0 && H2 % 8 == 0, "8-row swizzle atoms");
+  constexpr bool TF32 = rcm::Prec<PREC>::TF32, X3 = rcm::Prec<PREC>::X3;
+  constexpr int NOP = rcm::Prec<PREC>::NOP;
   using E = rcm::Elem<TF32>;
-  constexpr int KC = kc<TF32>();
+  constexpr int RB = row_bytes<PREC>(), KC = kc<PREC>();
   constexpr uint32_t STG = stg_bytes<TF32>();
-  constexpr uint32_t A_BYTES = 128 * 128, B_BYTES = (NP / 2) * 128;  // 128-byte rows
-  constexpr uint32_t STAGE = (A_BYTES + B_BYTES + 1023u) & ~1023u;
+  constexpr uint32_t A_BYTES = 128 * RB, B_BYTES = (NP / 2) * RB;  // one copy; X3 stages hold hi and lo
+  constexpr uint32_t STAGE = (NOP * (A_BYTES + B_BYTES) + 1023u) & ~1023u;  // [A hi | A lo | B hi | B lo]
   constexpr int W_TMA = NEPI, W_MMA = NEPI + 1;
 
   extern __shared__ uint8_t smem_raw[];
@@ -118,6 +124,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     rcx::prefetch_tmap(&mapBa);
     if (P2 > 0) rcx::prefetch_tmap(&mapBb);
     if (!DOT) rcx::prefetch_tmap(&mapOut);
+    if (X3) {
+      rcx::prefetch_tmap(&mapAlo);
+      rcx::prefetch_tmap(&mapBalo);
+      if (P2 > 0) rcx::prefetch_tmap(&mapBblo);
+      if (!DOT) rcx::prefetch_tmap(&mapOutlo);
+    }
     for (int s = 0; s < S; ++s) { rcx::mbar_init(&full[s], 2); rcx::mbar_init(&empty[s], 1); }
     rcx::mbar_init(c2full, 1);
     rcx::mbar_init(c2empty, 2 * NEPI);
@@ -150,12 +162,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
         if (DOT) rcx::bulk_g2s(sB2 + zb * VEC + NP, a.w4 + (size_t)net * a.N + pass * NP, NP * 4, &bfull[zb]);
         for (int c = 0; c < C; ++c) {
           rcx::mbar_wait_sleep(&empty[s], ph ^ 1);
-          rcx::mbar_arrive_expect_tx_cluster(full0 + s * 8, A_BYTES + B_BYTES);
+          rcx::mbar_arrive_expect_tx_cluster(full0 + s * 8, NOP * (A_BYTES + B_BYTES));
           uint8_t *st = sW + s * STAGE;
+          uint8_t *sb = st + NOP * A_BYTES;
           rcx::tma_load_3d_pair(st, &mapA, &full[s], c * KC, mp * 256 + rank * 128, net);
-          rcx::tma_load_3d_pair(st + A_BYTES, &mapBa, &full[s], c * KC, pass * NP + rank * H1, net);
+          rcx::tma_load_3d_pair(sb, &mapBa, &full[s], c * KC, pass * NP + rank * H1, net);
           if (P2 > 0)
-            rcx::tma_load_3d_pair(st + A_BYTES + H1 * 128, &mapBb, &full[s], c * KC, pass * NP + P1 + rank * H2, net);
+            rcx::tma_load_3d_pair(sb + H1 * RB, &mapBb, &full[s], c * KC, pass * NP + P1 + rank * H2, net);
+          if (X3) {
+            rcx::tma_load_3d_pair(st + A_BYTES, &mapAlo, &full[s], c * KC, mp * 256 + rank * 128, net);
+            rcx::tma_load_3d_pair(sb + B_BYTES, &mapBalo, &full[s], c * KC, pass * NP + rank * H1, net);
+            if (P2 > 0)
+              rcx::tma_load_3d_pair(sb + B_BYTES + H1 * RB, &mapBblo, &full[s], c * KC, pass * NP + P1 + rank * H2, net);
+          }
           if (++s == S) { s = 0; ph ^= 1; }
         }
       }
@@ -175,13 +194,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
         for (int c = 0; c < C; ++c) {
           rcx::mbar_wait(&full[s], ph);
           rcx::tc_fence_after();
-          const uint64_t da = desc_sw128(sW + s * STAGE);
-          const uint64_t db = desc_sw128(sW + s * STAGE + A_BYTES);
+          const uint64_t da = rcm::desc_sw<RB>(sW + s * STAGE);
+          const uint64_t db = rcm::desc_sw<RB>(sW + s * STAGE + NOP * A_BYTES);
+          constexpr uint64_t ALO = A_BYTES >> 4, BLO = B_BYTES >> 4, BP2 = (H1 * RB) >> 4;
 #pragma unroll
           for (int k = 0; k < KC / E::KATOM; ++k) {  // 32-byte K atoms: descriptor start += 2
-            rcm::mma_pair<TF32>(tmem, da + 2 * k, db + 2 * k, idp1, (c | k) != 0);
-            if (P2 > 0)
-              rcm::mma_pair<TF32>(tmem + P1, da + 2 * k, db + (uint64_t)((H1 * 128) >> 4) + 2 * k, idp2, (c | k) != 0);
+            const uint32_t acc = (c | k) != 0;
+            rcm::mma_pair<TF32>(tmem, da + 2 * k, db + 2 * k, idp1, acc);
+            if (P2 > 0) rcm::mma_pair<TF32>(tmem + P1, da + 2 * k, db + BP2 + 2 * k, idp2, acc);
+            if (X3) {  // + a_lo b_hi + a_hi b_lo
+              rcm::mma_pair<TF32>(tmem, da + ALO + 2 * k, db + 2 * k, idp1, 1);
+              if (P2 > 0) rcm::mma_pair<TF32>(tmem + P1, da + ALO + 2 * k, db + BP2 + 2 * k, idp2, 1);
+              rcm::mma_pair<TF32>(tmem, da + 2 * k, db + BLO + 2 * k, idp1, 1);
+              if (P2 > 0) rcm::mma_pair<TF32>(tmem + P1, da + 2 * k, db + BLO + BP2 + 2 * k, idp2, 1);
+            }
           }
           rcx::mma_commit_pair(&empty[s]);
           if (++s == S) { s = 0; ph ^= 1; }
@@ -252,30 +278,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
                 dot = fmaf(rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j + 3]) + b.w), w.w, dot);
               }
             } else {  // layer 2: tf32-rounded exact GELU -> [32 rows][64 B] staging (64-byte swizzle) -> TMA store
-              float g[16];
+              float y[16];
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
                 const float4 b = bb[j];
-                g[4 * j] = rcm::tf32_rn(rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j]) + b.x));
-                g[4 * j + 1] = rcm::tf32_rn(rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j + 1]) + b.y));
-                g[4 * j + 2] = rcm::tf32_rn(rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j + 2]) + b.z));
-                g[4 * j + 3] = rcm::tf32_rn(rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j + 3]) + b.w));
+                y[4 * j] = rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j]) + b.x);
+                y[4 * j + 1] = rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j + 1]) + b.y);
+                y[4 * j + 2] = rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j + 2]) + b.z);
+                y[4 * j + 3] = rcm::gelu_erf_f32(__uint_as_float(v[16 * h + 4 * j + 3]) + b.w);
               }
-              uint8_t *stg = stg_base + (nst & 1) * STG;
-              if (lane == 0) bulk_wait_read1();
-              __syncwarp();
-              const int x = (lane >> 1) & 3;
 #pragma unroll
-              for (int u = 0; u < 4; ++u)
-                *reinterpret_cast<float4 *>(stg + lane * 64 + ((u ^ x) << 4)) =
-                    make_float4(g[4 * u], g[4 * u + 1], g[4 * u + 2], g[4 * u + 3]);
-              fence_async_smem();
-              __syncwarp();
-              if (lane == 0) {
-                tma_store_3d(&mapOut, stg, pass * NP + col, grow, net);
-                bulk_commit();
+              for (int part = 0; part < NOP; ++part) {  // hi (= tf32(y)); X3: then lo (= tf32(y - hi))
+                float g[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) g[j] = part == 0 ? rcm::tf32_rn(y[j]) : rcm::tf32_rn(y[j] - rcm::tf32_rn(y[j]));
+                uint8_t *stg = stg_base + (nst & 1) * STG;
+                if (lane == 0) bulk_wait_read1();
+                __syncwarp();
+                const int x = (lane >> 1) & 3;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                  *reinterpret_cast<float4 *>(stg + lane * 64 + ((u ^ x) << 4)) =
+                      make_float4(g[4 * u], g[4 * u + 1], g[4 * u + 2], g[4 * u + 3]);
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                  tma_store_3d(part == 0 ? &mapOut : &mapOutlo, stg, pass * NP + col, grow, net);
+                  bulk_commit();
+                }
+                ++nst;
               }
-              ++nst;
             }
           }
         }
@@ -366,11 +398,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
   }
 }
 
-template <int NP, bool DOT, bool TF32>
-int launch_l2_pair_t(const CUtensorMap &A, const CUtensorMap &Ba, const CUtensorMap &Bb, const CUtensorMap &Out,
-                     L2Args a, cudaStream_t s) {
-  constexpr size_t STAGE = ((128 * 128 + (NP / 2) * 128) + 1023) & ~(size_t)1023;
-  const size_t fixed = 1024 + NEPI * 2 * stg_bytes<TF32>() + 2 * (DOT ? 2 : 1) * NP * 4 + 512;
+template <int NP, bool DOT, int PREC>
+int launch_l2_pair_t(const CUtensorMap *M, L2Args a, cudaStream_t s) {
+  constexpr int RB = row_bytes<PREC>();
+  constexpr size_t STAGE = (rcm::Prec<PREC>::NOP * (128 * RB + (NP / 2) * RB) + 1023) & ~(size_t)1023;
+  const size_t fixed = 1024 + NEPI * 2 * stg_bytes<(PREC != 0)>() + 2 * (DOT ? 2 : 1) * NP * 4 + 512;
   int stages = (int)((232448 - fixed) / STAGE);
   if (stages > 8) stages = 8;
   if (stages < 2) return rc_fail(RC_EUNSUPPORTED, "layer-2 GEMM: pass width %d does not fit", NP);
@@ -378,13 +410,13 @@ int launch_l2_pair_t(const CUtensorMap &A, const CUtensorMap &Ba, const CUtensor
   const size_t smem = fixed + stages * STAGE;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(l2_pair_kernel<NP, DOT, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaFuncSetAttribute(l2_pair_kernel<NP, DOT, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     attr = true;
   }
   const int total = a.nets * (a.m_tiles / 2) * a.passes;
   int clusters = mlp_num_sms() / 2;
   if (clusters > total) clusters = total;
-  l2_pair_kernel<NP, DOT, TF32><<<2 * clusters, L2_THREADS, smem, s>>>(A, Ba, Bb, Out, a);
+  l2_pair_kernel<NP, DOT, PREC><<<2 * clusters, L2_THREADS, smem, s>>>(M[0], M[1], M[2], M[3], M[4], M[5], M[6], M[7], a);
   RC_LAUNCH_CHECK();
   return RC_OK;
 }
@@ -404,15 +436,16 @@ int l2_pass_width(int h2) {
   return 0;
 }
 
-int launch_l2_pair(int NP, bool tf32, const CUtensorMap &A, const CUtensorMap &Ba, const CUtensorMap &Bb, const CUtensorMap &Out,
-                   const L2Args &a, cudaStream_t s) {
+int launch_l2_pair(int NP, int prec, const CUtensorMap *maps, const L2Args &a, cudaStream_t s) {
   ProfScope prof(a.w4 ? RC_STAGE_L3 : RC_STAGE_L2, s);
-#define RC_L2P(np)                                                                     \
-  if (NP == np)                                                                        \
-    return a.w4 ? (tf32 ? launch_l2_pair_t<np, true, true>(A, Ba, Bb, Out, a, s)        \
-                        : launch_l2_pair_t<np, true, false>(A, Ba, Bb, Out, a, s))      \
-                : (tf32 ? launch_l2_pair_t<np, false, true>(A, Ba, Bb, Out, a, s)       \
-                        : launch_l2_pair_t<np, false, false>(A, Ba, Bb, Out, a, s));
+#define RC_L2P_PREC(np, dot)                                                                                \
+  return prec == 0 ? launch_l2_pair_t<np, dot, 0>(maps, a, s)                                               \
+                   : prec == 1 ? launch_l2_pair_t<np, dot, 1>(maps, a, s) : launch_l2_pair_t<np, dot, 2>(maps, a, s);
+#define RC_L2P(np)                     \
+  if (NP == np) {                      \
+    if (a.w4) RC_L2P_PREC(np, true)    \
+    else RC_L2P_PREC(np, false)        \
+  }
   RC_L2P(400)
   RC_L2P(256)
   RC_L2P(208)
@@ -421,5 +454,6 @@ int launch_l2_pair(int NP, bool tf32, const CUtensorMap &A, const CUtensorMap &B
   RC_L2P(32)
   RC_L2P(16)
 #undef RC_L2P
+#undef RC_L2P_PREC
   return rc_fail(RC_EUNSUPPORTED, "layer-2 GEMM: no instance for pass width %d", NP);
 }

@@ -53,7 +53,8 @@ struct ProArgs {
   float lambda, inv_lambda;
   const float *xmean, *xinvstd;
   void *z;  // [cap][kz] bf16 (or tf32-rounded fp32): z-scored inputs, two 1.0 columns (b1 hi/lo), zeros
-  int tf32;
+  int tf32;         // 0 bf16, 1 tf32, 2 tf32 hi at z and tf32 lo at z + lo_off
+  int64_t lo_off;   // elements
 };
 
 __global__ void __launch_bounds__(256) prologue_kernel(ProArgs a, CellsDev c) {
@@ -80,11 +81,16 @@ __global__ void __launch_bounds__(256) prologue_kernel(ProArgs a, CellsDev c) {
   }
   if (a.tf32) {
     float4 *dst = reinterpret_cast<float4 *>(static_cast<float *>(a.z) + (size_t)r * a.kz);
+    float4 *lo = reinterpret_cast<float4 *>(static_cast<float *>(a.z) + a.lo_off + (size_t)r * a.kz);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       if (q * 4 >= a.kz) break;
-      dst[q] = make_float4(rcm::tf32_rn(x[4 * q]), rcm::tf32_rn(x[4 * q + 1]), rcm::tf32_rn(x[4 * q + 2]),
-                           rcm::tf32_rn(x[4 * q + 3]));
+      const float4 h = make_float4(rcm::tf32_rn(x[4 * q]), rcm::tf32_rn(x[4 * q + 1]), rcm::tf32_rn(x[4 * q + 2]),
+                                   rcm::tf32_rn(x[4 * q + 3]));
+      dst[q] = h;
+      if (a.tf32 == 2)
+        lo[q] = make_float4(rcm::tf32_rn(x[4 * q] - h.x), rcm::tf32_rn(x[4 * q + 1] - h.y),
+                            rcm::tf32_rn(x[4 * q + 2] - h.z), rcm::tf32_rn(x[4 * q + 3] - h.w));
     }
     return;
   }
@@ -325,10 +331,11 @@ WsLayout ws_layout(const rc_mlp *n, int cap) {
   L.cap = cap;
   size_t o = 0;
   L.qpart = o; o = al(o + QPART_BLOCKS * 8);
-  const size_t eb = n->precision == RC_TF32 ? 4 : 2;  // activation element bytes
-  L.z = o; o = al(o + (size_t)cap * n->kpad1 * eb);
-  L.h1 = o; o = al(o + (size_t)n->n_nets * cap * n->h1 * eb);
-  L.h2 = o; o = al(o + (size_t)n->n_nets * cap * n->h2 * eb);
+  // activation element bytes (RC_TF32X3 keeps a tf32 hi and a tf32 lo array of each)
+  const size_t eb = n->precision == RC_BF16 ? 2 : 4, nc = n->precision == RC_TF32X3 ? 2 : 1;
+  L.z = o; o = al(o + nc * (size_t)cap * n->kpad1 * eb);
+  L.h1 = o; o = al(o + nc * (size_t)n->n_nets * cap * n->h1 * eb);
+  L.h2 = o; o = al(o + nc * (size_t)n->n_nets * cap * n->h2 * eb);
   const int np3 = 4 * (n->h3 / l2_pass_width(n->h3));  // partial dots per row: 4 column quarters per pass
   L.opart = o; o = al(o + (size_t)n->n_nets * np3 * cap * 4);
   L.total = o;
@@ -361,9 +368,11 @@ int launch_combine_reductions(const double *rp, const int64_t *dp, int k, double
   return RC_OK;
 }
 
+int cap_limit(const rc_mlp *n) { return n->precision == RC_TF32X3 ? std::min(MAX_CAP, 32768) : MAX_CAP; }
+
 size_t chem_workspace_bytes(const rc_mech *, const rc_mlp *n, int64_t ncells) {
   int64_t cap = (ncells + 255) / 256 * 256;  // chunks of CTA-pair (256-row) tiles
-  if (cap > MAX_CAP) cap = MAX_CAP;
+  if (cap > cap_limit(n)) cap = cap_limit(n);
   if (cap < 256) cap = 256;
   return ws_layout(n, (int)cap).total;
 }
@@ -371,17 +380,27 @@ size_t chem_workspace_bytes(const rc_mech *, const rc_mlp *n, int64_t ncells) {
 int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
   if (n->h1 % 64 || !l2_pass_width(n->h2) || !l2_pass_width(n->h3))
     return rc_fail(RC_EUNSUPPORTED, "hidden widths (%d,%d,%d) not supported by the MLP kernels", n->h1, n->h2, n->h3);
-  const bool tf32 = n->precision == RC_TF32;
+  const bool tf32 = n->precision != RC_BF16, x3 = n->precision == RC_TF32X3;
   const int nets = n->n_nets, din = n->d_in, h1 = n->h1, h2 = n->h2, h3 = n->h3, kp = n->kpad1;
   const size_t P = (size_t)h1 * din + h1 + (size_t)h2 * h1 + h2 + (size_t)h3 * h2 + h3 + h3 + 1;
   // weights, K-major [net][out][in]: bf16 (RNE) or tf32-rounded fp32
   std::vector<uint16_t> W1((size_t)nets * h1 * kp, 0), W2((size_t)nets * h2 * h1), W3((size_t)nets * h3 * h2);
   std::vector<float> F1, F2, F3;
+  std::vector<float> L1v, L2v, L3v;  // RC_TF32X3: tf32 residuals W - W_hi
   if (tf32) {
     F1.assign((size_t)nets * h1 * kp, 0.f);
     F2.resize((size_t)nets * h2 * h1);
     F3.resize((size_t)nets * h3 * h2);
   }
+  if (x3) {
+    L1v.assign((size_t)nets * h1 * kp, 0.f);
+    L2v.resize((size_t)nets * h2 * h1);
+    L3v.resize((size_t)nets * h3 * h2);
+  }
+  auto split = [&](double w, float &hi, float *lo) {  // hi = tf32(w); lo = tf32(w - hi) (X3 only)
+    hi = f2tf32((float)w);
+    if (lo) *lo = f2tf32((float)(w - (double)hi));
+  };
   std::vector<float> b1((size_t)nets * h1), b2((size_t)nets * h2), b3((size_t)nets * h3), w4((size_t)nets * h3), b4(nets);
   for (int i = 0; i < nets; ++i) {
     const double *p = d->params + i * P;
@@ -389,11 +408,12 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
     for (int r = 0; r < h1; ++r) {
       const size_t row = ((size_t)i * h1 + r) * kp;
       if (tf32) {
-        for (int k = 0; k < din; ++k) F1[row + k] = f2tf32((float)p[(size_t)r * din + k]);
-        // b1 folded into the layer-1 MMA as tf32 hi + lo parts (z carries 1.0 in columns din, din+1)
+        for (int k = 0; k < din; ++k) split(p[(size_t)r * din + k], F1[row + k], x3 ? &L1v[row + k] : nullptr);
+        // b1 folded into the layer-1 MMA as tf32 hi + lo parts (z carries 1.0 in columns din, din+1);
+        // X3 also keeps the residual of the lo part
         const float hi = f2tf32((float)pb1[r]);
         F1[row + din] = hi;
-        F1[row + din + 1] = f2tf32((float)(pb1[r] - (double)hi));
+        split(pb1[r] - (double)hi, F1[row + din + 1], x3 ? &L1v[row + din + 1] : nullptr);
       } else {
         // W1 is stored halved (exact in bf16): the layer-1 epilogue evaluates GELU(2y) from y = x/2
         for (int k = 0; k < din; ++k) W1[row + k] = f2bf(0.5f * (float)p[(size_t)r * din + k]);
@@ -409,14 +429,14 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
     }
     p += (size_t)h1 * din + h1;
     for (size_t e = 0; e < (size_t)h2 * h1; ++e) {
-      if (tf32) F2[(size_t)i * h2 * h1 + e] = f2tf32((float)p[e]);
+      if (tf32) split(p[e], F2[(size_t)i * h2 * h1 + e], x3 ? &L2v[(size_t)i * h2 * h1 + e] : nullptr);
       else W2[(size_t)i * h2 * h1 + e] = f2bf((float)p[e]);
     }
     p += (size_t)h2 * h1;
     for (int r = 0; r < h2; ++r) b2[(size_t)i * h2 + r] = (float)p[r];
     p += h2;
     for (size_t e = 0; e < (size_t)h3 * h2; ++e) {
-      if (tf32) F3[(size_t)i * h3 * h2 + e] = f2tf32((float)p[e]);
+      if (tf32) split(p[e], F3[(size_t)i * h3 * h2 + e], x3 ? &L3v[(size_t)i * h3 * h2 + e] : nullptr);
       else W3[(size_t)i * h3 * h2 + e] = f2bf((float)p[e]);
     }
     p += (size_t)h3 * h2;
@@ -444,6 +464,9 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
             up((void **)&n->d_xmean, xm.data(), xm.size() * 4) && up((void **)&n->d_xinvstd, xi.data(), xi.size() * 4) &&
             up((void **)&n->d_ymean, d->y_mean, nets * 8) && up((void **)&n->d_ystd, d->y_std, nets * 8) &&
             up((void **)&n->d_species, d->species_of_net, nets * 4);
+  if (ok && x3)
+    ok = up(&n->d_W1lo, L1v.data(), L1v.size() * 4) && up(&n->d_W2lo, L2v.data(), L2v.size() * 4) &&
+         up(&n->d_W3lo, L3v.data(), L3v.size() * 4);
   if (!ok) return rc_fail(RC_ENOMEM, "rc_mlp_create: device upload failed");
   return RC_OK;
 }
@@ -451,41 +474,58 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
 int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, size_t ws_bytes, cudaStream_t s) {
   if (c.n == 0) return RC_OK;
   // chunk capacity: largest multiple of 128 (<= MAX_CAP, <= n rounded up) whose layout fits the workspace
-  int cap = (int)std::min<int64_t>((c.n + 255) / 256 * 256, MAX_CAP);
+  int cap = (int)std::min<int64_t>((c.n + 255) / 256 * 256, cap_limit(n));
   while (cap > 256 && ws_layout(n, cap).total > ws_bytes) cap -= 256;
   WsLayout L = ws_layout(n, cap);
   if (L.total > ws_bytes) return rc_fail(RC_EINVAL, "workspace too small (%zu < %zu)", ws_bytes, L.total);
   uint8_t *w = static_cast<uint8_t *>(ws);
-  void *z = w + L.z, *h1 = w + L.h1, *h2 = w + L.h2;
-  const bool tf32 = n->precision == RC_TF32;
-  const int EB = tf32 ? 4 : 2, KC = 128 / EB;  // element bytes; K elements per 128-byte operand row
+  const int prec = n->precision == RC_BF16 ? 0 : n->precision == RC_TF32 ? 1 : 2;
+  const bool tf32 = prec != 0, x3 = prec == 2;
+  const int EB = tf32 ? 4 : 2;
+  const int RB = x3 ? 64 : 128, KC = RB / EB;  // element bytes; K elements per swizzled operand row
+  const int nets = n->n_nets;
+  // activations: hi copy at the start of each region, X3's lo copy right after it
+  uint8_t *z = w + L.z, *h1 = w + L.h1, *h2 = w + L.h2;
+  const size_t zlo = (size_t)cap * n->kpad1 * EB, h1lo = (size_t)nets * cap * n->h1 * EB,
+               h2lo = (size_t)nets * cap * n->h2 * EB;
   auto *opart = reinterpret_cast<float *>(w + L.opart);
   auto *qpart = reinterpret_cast<double *>(w + L.qpart);
-  const int nets = n->n_nets;
   const int bn1 = l1_tile_n(), NP = l2_pass_width(n->h2), NP3 = l2_pass_width(n->h3), KZ = n->kpad1;
   const int P1 = NP > 256 ? 256 : NP, P2 = NP - P1;
   const int Q1 = NP3 > 256 ? 256 : NP3, Q2 = NP3 - Q1;
-  CUtensorMap mz, mh1, mh1st, mh2, mh2st, mw1, mw2a, mw2b, mw3a, mw3b;
+  // layer 1: {z, W1, h1 store (32-row boxes of one 128-byte row), z lo, W1 lo, h1 lo store}
+  // layers 2/3: {A, B piece 1, B piece 2, h2 store (32 x 16 boxes), lo copies of the same}
+  CUtensorMap m1[6], m2[8], m3[8];
+  const int sbox = 128 / EB;  // h1 store box width: one 128-byte row
   int rc;
-  // operand maps: 128-byte rows (KC elements) except z/W1 (KZ elements); store maps: 32-row boxes
-  if ((rc = make_map(&mz, z, KZ, cap, 1, BM, KZ, EB)) ||
-      (rc = make_map(&mw1, n->d_W1, KZ, n->h1, nets, l1_box_rows(), KZ, EB)) ||
-      (rc = make_map(&mh1, h1, n->h1, cap, nets, BM, KC, EB)) ||
-      (rc = make_map(&mh1st, h1, n->h1, cap, nets, 32, KC, EB)) ||
-      (rc = make_map(&mw2a, n->d_W2, n->h1, n->h2, nets, P1 / 2, KC, EB)) ||
-      (rc = make_map(&mw2b, n->d_W2, n->h1, n->h2, nets, P2 > 0 ? P2 / 2 : P1 / 2, KC, EB)) ||
-      (rc = make_map(&mh2, h2, n->h2, cap, nets, BM, KC, EB)) ||
-      (rc = make_map(&mh2st, h2, n->h2, cap, nets, 32, 16, EB)) ||
-      (rc = make_map(&mw3a, n->d_W3, n->h2, n->h3, nets, Q1 / 2, KC, EB)) ||
-      (rc = make_map(&mw3b, n->d_W3, n->h2, n->h3, nets, Q2 > 0 ? Q2 / 2 : Q1 / 2, KC, EB)))
-    return rc;
+  for (int part = 0; part < (x3 ? 2 : 1); ++part) {
+    const size_t oz = part ? zlo : 0, o1 = part ? h1lo : 0, o2 = part ? h2lo : 0;
+    const void *W1 = part ? n->d_W1lo : n->d_W1, *W2 = part ? n->d_W2lo : n->d_W2, *W3 = part ? n->d_W3lo : n->d_W3;
+    CUtensorMap *a1 = m1 + 3 * part, *a2 = m2 + 4 * part, *a3 = m3 + 4 * part;
+    if ((rc = make_map(&a1[0], z + oz, KZ, cap, 1, BM, KZ, EB)) ||
+        (rc = make_map(&a1[1], W1, KZ, n->h1, nets, l1_box_rows(), KZ, EB)) ||
+        (rc = make_map(&a1[2], h1 + o1, n->h1, cap, nets, 32, sbox, EB)) ||
+        (rc = make_map(&a2[0], h1 + o1, n->h1, cap, nets, BM, KC, EB)) ||
+        (rc = make_map(&a2[1], W2, n->h1, n->h2, nets, P1 / 2, KC, EB)) ||
+        (rc = make_map(&a2[2], W2, n->h1, n->h2, nets, P2 > 0 ? P2 / 2 : P1 / 2, KC, EB)) ||
+        (rc = make_map(&a2[3], h2 + o2, n->h2, cap, nets, 32, 16, EB)) ||
+        (rc = make_map(&a3[0], h2 + o2, n->h2, cap, nets, BM, KC, EB)) ||
+        (rc = make_map(&a3[1], W3, n->h2, n->h3, nets, Q1 / 2, KC, EB)) ||
+        (rc = make_map(&a3[2], W3, n->h2, n->h3, nets, Q2 > 0 ? Q2 / 2 : Q1 / 2, KC, EB)))
+      return rc;
+    a3[3] = a2[3];  // unused by the dot epilogue
+  }
+  if (!x3) {  // the lo slots are never read: any valid map
+    for (int k = 0; k < 3; ++k) m1[3 + k] = m1[k];
+    for (int k = 0; k < 4; ++k) m2[4 + k] = m2[k], m3[4 + k] = m3[k];
+  }
   RC_CUDA_TRY(cudaMemsetAsync(qpart, 0, QPART_BLOCKS * 8, s));
   int64_t launches = 1;
   for (int64_t c0 = 0; c0 < c.n; c0 += cap) {
     const int rows = (int)std::min<int64_t>(cap, c.n - c0);
     const int mt = (rows + 2 * BM - 1) / (2 * BM) * 2;  // even: CTA pairs of 128-row tiles
     ProArgs pa{c0, rows, mt * BM, n->d_in, n->ns, KZ, (float)n->lambda_bc, (float)(1.0 / n->lambda_bc), n->d_xmean,
-               n->d_xinvstd, z, tf32 ? 1 : 0};
+               n->d_xinvstd, z, prec, (int64_t)(zlo / EB)};
     {
       ProfScope prof(RC_STAGE_PROLOGUE, s);
       prologue_kernel<<<(mt * BM + 255) / 256, 256, 0, s>>>(pa, c);
@@ -493,13 +533,13 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
     }
     // layer 1: h1 = GELU(z W1^T) (b1 folded into z's constant-1 columns)
     L1Args g1{mt, (n->h1 + bn1 - 1) / bn1, nets, n->h1, 0, cap};
-    if ((rc = launch_l1(KZ, tf32, mz, mw1, mh1st, g1, s))) return rc;
+    if ((rc = launch_l1(KZ, prec, m1, g1, s))) return rc;
     // layer 2: h2 = GELU(h1 W2^T + b2), CTA-pair GEMM
     L2Args la{mt, n->h2 / NP, nets, (n->h1 + KC - 1) / KC, n->h2, 0, n->d_b2, nullptr, nullptr, cap};
-    if ((rc = launch_l2_pair(NP, tf32, mh1, mw2a, mw2b, mh2st, la, s))) return rc;
+    if ((rc = launch_l2_pair(NP, prec, m2, la, s))) return rc;
     // layer 3 + folded layer 4: the same CTA-pair GEMM with the dot epilogue (K = h2, zero-filled to KC)
     L2Args l3{mt, n->h3 / NP3, nets, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, n->d_w4, opart, cap};
-    if ((rc = launch_l2_pair(NP3, tf32, mh2, mw3a, mw3b, mh2st, l3, s))) return rc;
+    if ((rc = launch_l2_pair(NP3, prec, m3, l3, s))) return rc;
     EpiArgs ea{c0, rows, cap, nets, 4 * (n->h3 / NP3), n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt, opart,
                n->d_b4, n->d_ymean, n->d_ystd, m->d_P, m->d_thermo, n->d_species, qpart};
     const size_t esm = (size_t)ThermoSeg::size(m->ns) * 8 + (size_t)((m->ns * m->ns + 1) & ~1) * 8;

@@ -64,6 +64,7 @@ struct rc_mlp {
   std::vector<int> species_of_net;
   // device buffers
   void *d_W1 = nullptr, *d_W2 = nullptr, *d_W3 = nullptr;   // [nets][N][K] bf16 or fp32(tf32-rounded)
+  void *d_W1lo = nullptr, *d_W2lo = nullptr, *d_W3lo = nullptr;  // RC_TF32X3: tf32(W - W_hi)
   float *d_b1 = nullptr, *d_b2 = nullptr, *d_b3 = nullptr;  // [nets][N]
   float *d_w4 = nullptr;                                    // [nets][h3]
   float *d_b4 = nullptr;                                    // [nets]

@@ -145,6 +145,21 @@ def test_tf32_paper_shape_sample():
     print(f"C2 tf32 sampled errors: o {eo:.2e} wdot {ew:.2e} qdot {eq:.2e}")
 
 
+@pytest.mark.parametrize("cfg,n", [("C1", 1000), ("C2", 65536)])
+def test_tf32x3_meets_1e3_on_outputs_and_wdot(cfg, n):
+    """RC_TF32X3 (three tf32 MMAs per product on hi/lo operand pairs: fp32-accurate
+    GEMMs): the 1e-3 gate holds for o and for the derived wdot/qdot too (R18)."""
+    c = inputs(cfg, begin=0, end=n)
+    g = Gpu(cfg, precision=2).run(c)
+    cols = np.unique((uniform(4343, np.arange(128)) * n).astype(np.int64)) if n > 1000 else None
+    sub = c if cols is None else {k: (v[..., cols] if isinstance(v, np.ndarray) else v) for k, v in c.items()}
+    o = run_oracle(cfg, sub)
+    if cols is None:
+        check_fp64(g, o)
+    eo, ew, eq = check_chem(g, o, mech("h2_9sp"), cols, tol=TF32_TOL, dtol=TF32_TOL)
+    print(f"{cfg} tf32x3 errors: o {eo:.2e} wdot {ew:.2e} qdot {eq:.2e}")
+
+
 def test_ch4_paper_shape_sample():
     """C4 (CH4/air, 20 species, 19 nets, d_in 22): parity on a hashed sample."""
     cols = _sample("C4", 256)
