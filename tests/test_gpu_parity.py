@@ -170,6 +170,18 @@ def test_ch4_paper_shape_sample():
     check_chem(g, o, mech("ch4_20sp"))
 
 
+@pytest.mark.parametrize("prec,tol,dtol", [(1, 1e-3, 2e-3), (2, 1e-3, 1e-3)])
+def test_ch4_tf32_modes_sample(prec, tol, dtol):
+    """C4 (d_in 22 -> 32-wide z rows, 19 nets) in the TF32 and TF32X3 modes."""
+    cols = _sample("C4", 128)
+    c = inputs("C4", idx=cols)
+    o = run_oracle("C4", c)
+    g = Gpu("C4", precision=prec).run(c)
+    check_fp64(g, o)
+    eo, ew, eq = check_chem(g, o, mech("ch4_20sp"), tol=tol, dtol=dtol)
+    print(f"C4 precision {prec} errors: o {eo:.2e} wdot {ew:.2e} qdot {eq:.2e}")
+
+
 def test_padding_untouched_and_single_cell():
     c = inputs("C1", begin=0, end=1)
     o = run_oracle("C1", c)

@@ -6,6 +6,8 @@
 #include <cuda_bf16.h>
 
 __device__ __forceinline__ uint32_t tanh2(uint32_t x) { uint32_t r; asm volatile("tanh.approx.bf16x2 %0, %1;" : "=r"(r) : "r"(x)); return r; }
+__device__ __forceinline__ uint32_t tanh2h(uint32_t x) { uint32_t r; asm volatile("tanh.approx.f16x2 %0, %1;" : "=r"(r) : "r"(x)); return r; }
+__device__ __forceinline__ uint32_t ex2h(uint32_t x) { uint32_t r; asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(x)); return r; }
 __device__ __forceinline__ float tanh1(float x) { float r; asm volatile("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
 __device__ __forceinline__ uint32_t fma2(uint32_t a, uint32_t b, uint32_t c) { uint32_t r; asm volatile("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c)); return r; }
 __device__ __forceinline__ uint32_t gelu2(uint32_t x) {
@@ -34,6 +36,8 @@ __global__ void k(int iters, uint32_t *out) {
         uint32_t p; asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(f[i]), "f"(f[(i + 1) & 7]));
         p = gelu2(p); f[i] = __uint_as_float(p) * 1e-3f + f[i];
       }
+      if (MODE == 7) v[i] = tanh2h(v[i]);
+      if (MODE == 8) v[i] = ex2h(v[i]);
       if (MODE == 6) { uint32_t p; asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(f[i]), "f"(f[(i + 1) & 7])); f[i] = __uint_as_float(p) + f[i]; }
     }
   }
@@ -45,16 +49,16 @@ __global__ void k(int iters, uint32_t *out) {
 int main() {
   uint32_t *d; cudaMalloc(&d, 4);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const char *names[] = {"tanh.approx.bf16x2 (elements)", "tanh.approx.f32", "fma.rn.bf16x2 (elements)", "gelu bf16x2 (elements)", "gelu f32", "cvt+gelu bf16x2 (elements)", "cvt.rn.bf16x2.f32 (elements)"};
+  const char *names[] = {"tanh.approx.bf16x2 (elements)", "tanh.approx.f32", "fma.rn.bf16x2 (elements)", "gelu bf16x2 (elements)", "gelu f32", "cvt+gelu bf16x2 (elements)", "cvt.rn.bf16x2.f32 (elements)", "tanh.approx.f16x2 (elements)", "ex2.approx.f16x2 (elements)"};
   for (int warps : {16}) {
-    for (int m = 0; m < 7; ++m) {
+    for (int m = 0; m < 9; ++m) {
       int iters = 4096; dim3 g(148), b(32 * warps);
       auto launch = [&]() { switch (m) { case 0: k<0><<<g, b>>>(iters, d); break; case 1: k<1><<<g, b>>>(iters, d); break;
-        case 2: k<2><<<g, b>>>(iters, d); break; case 3: k<3><<<g, b>>>(iters, d); break; case 4: k<4><<<g, b>>>(iters, d); break; case 5: k<5><<<g, b>>>(iters, d); break; case 6: k<6><<<g, b>>>(iters, d); break; } };
+        case 2: k<2><<<g, b>>>(iters, d); break; case 3: k<3><<<g, b>>>(iters, d); break; case 4: k<4><<<g, b>>>(iters, d); break; case 5: k<5><<<g, b>>>(iters, d); break; case 6: k<6><<<g, b>>>(iters, d); break; case 7: k<7><<<g, b>>>(iters, d); break; case 8: k<8><<<g, b>>>(iters, d); break; } };
       launch(); cudaDeviceSynchronize();
       cudaEventRecord(e0); launch(); cudaEventRecord(e1); cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
-      double elems = 8.0 * iters * g.x * b.x * ((m == 0 || m == 2 || m == 3 || m == 5 || m == 6) ? 2 : 1);
+      double elems = 8.0 * iters * g.x * b.x * ((m == 0 || m == 2 || m == 3 || m == 5 || m == 6 || m == 7 || m == 8) ? 2 : 1);
       printf("warps/SM=%2d %-32s %8.1f Gelem/s = %6.1f elem/clk/SM @1.9GHz\n", warps, names[m], elems / ms / 1e6, elems / ms / 1e6 / 148 / 1.9);
     }
   }
