@@ -26,5 +26,15 @@ struct L2Args {
   float *opart;            // layer-3 mode: [nets][passes*4][cap] partial dots
   int cap;
 };
+// fused layers 1+2 (mlp_l12_sm100.cu, bf16, h2 = 800): clusters of two CTA pairs share h1 chunks
+// maps: {z (KZ x 128 rows), W1 (KZ x 16 rows), W2 piece 1 (32 x 128 rows), W2 piece 2 (32 x 72 rows),
+//        h2 store (16 x 32)}
+struct L12Args {
+  int m_tiles, nets, chunks, N, stages, lead_in;
+  const float *bias;  // b2 [nets][N]
+};
+bool l12_supported(int h1, int h2, int kz);
+int launch_l12(int KZ, const CUtensorMap *maps, const L12Args &a, cudaStream_t s);
+
 // maps: {A, B piece 1, B piece 2, out store, A lo, B1 lo, B2 lo, out lo store} (lo: precision 2 only)
 int launch_l2_pair(int NP, int prec, const CUtensorMap *maps, const L2Args &a, cudaStream_t s);

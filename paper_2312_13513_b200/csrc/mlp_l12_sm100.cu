@@ -1,0 +1,453 @@
+// mlp_l12_sm100.cu -- layers 1 and 2 of the per-species MLP fused (PAPER.md:114:
+// inputs -> 1600 -> 800, GELU), bf16, so the 1600-wide h1 never goes to HBM:
+//
+//   h2 = GELU( GELU(z W1^T) W2^T + b2 )      (W1 stored halved, b1 folded, as in layer 1)
+//
+// A cluster of four CTAs = two CTA pairs owns a 256-cell row block.  Pair p
+// computes the layer-2 outputs of pass p (400 of the 800 columns) with the
+// cta_group::2 GEMM of the layer-2 kernel (M = 256, N = 256 + 144, K chunks of
+// 64).  Both pairs need every 64-column chunk of h1 for all 256 rows, so each
+// pair produces half of it: pair p computes columns [32p, 32p + 32) of the chunk
+// (a cta_group::2 MMA, M = 256, N = 32, K = 16/32, into a double-buffered TMEM
+// accumulator), eight epilogue warps per CTA apply GELU and write the 128 x 32
+// bf16 half-chunk into the CTA's A slot, and a forwarder thread copies it with
+// one 8 KB DSMEM bulk copy into the same slot of the CTA with the same rows in
+// the other pair.  Each A slot is therefore [half-chunk 0 | half-chunk 1], both
+// 64-byte-swizzled [128 rows][32 cols] tiles, which is how the layer-2 MMAs read
+// it (K steps 0-1 from the first half, 2-3 from the second).
+//
+// Per CTA and 64-column chunk this costs 4096 GELUs (256 clk of MUFU) against
+// 800 clk of layer-2 MMA, instead of a separate layer-1 pass writing and then
+// re-reading 3.2 KB of h1 per cell and net.
+//
+// Barriers (per CTA; "leader" = even CTA of a pair, which issues the MMAs):
+//   full/empty[S]   W2 + W1 stages (pair TMA, leader counts both CTAs' bytes)
+//   zfull/zempty[2] z tile of the row block (pair TMA)
+//   a1full/a1empty[2] layer-1 accumulators (commit -> pair; 16 producer warps of the pair)
+//   own[R]          this CTA's half-chunk written (8 local producer warps)
+//   peer[R]         the other pair's half-chunk arrived (DSMEM bulk copy, 8 KB)
+//   afull[R]        slot complete in both CTAs of the pair (2 forwarders -> leader)
+//   aempty[R]       slot consumed by both pairs (commit multicast to all four CTAs)
+//   c2full/c2empty  layer-2 accumulator, bfull/bempty the b2 slice (as the layer-2 kernel)
+// Warps: 0..15 epilogue (0..7 also produce h1), 16 TMA producer, 17 layer-2 MMA
+// issuer, 18 half-chunk copier, 19 layer-1 MMA issuer (even CTA) / forwarder (odd CTA).
+#include <cuda_bf16.h>
+
+#include <cstdio>
+#include <cstdlib>
+
+#include "mlp_common.cuh"
+#include "mlp_internal.h"
+
+namespace {
+
+constexpr int NEPI = 16, NPROD = 8;
+// W_AUX: the layer-1 MMA issuer in the even CTA of a pair, the slot forwarder in the odd one
+constexpr int W_TMA = NEPI, W_MMA = NEPI + 1, W_CPY = NEPI + 2, W_AUX = NEPI + 3;
+constexpr int L12_THREADS = 32 * (NEPI + 4);
+constexpr int NA1 = 3;                        // layer-1 accumulators (32 TMEM columns each)
+constexpr int NP = 400, P1 = 256, P2 = 144, H1 = P1 / 2, H2 = P2 / 2;  // pass width and its two MMA pieces
+constexpr uint32_t HALF = 128 * 64;           // [128 rows][32 bf16] half-chunk, 64-byte swizzle (8 KB)
+constexpr uint32_t SLOT = 2 * HALF;
+constexpr uint32_t W2H = (NP / 2) * 64;       // W2 K-half tile of one CTA: 200 rows x 64 B (12.8 KB)
+constexpr uint32_t W2H_AL = 13312;            // 1 KB aligned
+constexpr uint32_t TMEM_ACC1 = 416;          // acc2 uses [0, 400); acc1 b at 416 + 32 b
+
+using rcm::cvt_bf16x2;
+using rcm::gelu_bf16x2;
+
+#ifdef L12TRACE  // timing experiment: clock64 stamps of cluster 0, first 64 chunks (tools/l12trace.py)
+__device__ long long g_l12trace[4][4][64][4];  // [cta rank][role: 0 MMA, 1 producer warp 0, 2 forwarder][chunk][event]
+#define TR(role, ch, ev)                                                                              \
+  do {                                                                                                \
+    if (blockIdx.x < 4 && (ch) < 64 && lane == 0) g_l12trace[blockIdx.x & 3][role][ch][ev] = clock64(); \
+  } while (0)
+#else
+#define TR(role, ch, ev) \
+  do {                   \
+  } while (0)
+#endif
+
+// R = ring depth: chunk g uses W2 stage and A slot g % R, so one barrier per chunk tells the
+// layer-2 issuer that both operands are in place (every wait between MMAs costs a tensor-pipe bubble)
+template <int KZ, int R>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
+    l12_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapW1,
+               const __grid_constant__ CUtensorMap mapW2a, const __grid_constant__ CUtensorMap mapW2b,
+               const __grid_constant__ CUtensorMap mapOut, L12Args a) {
+  constexpr uint32_t Z_BYTES = 128 * KZ * 2, W1_CH = 16 * KZ * 2;  // W1: 16 rows per CTA and chunk
+  constexpr uint32_t STAGE_BYTES = 2 * W2H;                         // TMA bytes per CTA
+  constexpr uint32_t STAGE = 2 * W2H_AL;                            // layout size
+  constexpr int MAXCH = (NP / 16 + 3) / 4;
+
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = rcx::smem_u32(smem_raw);
+  uint8_t *smem = smem_raw + (((base_u32 + 1023u) & ~1023u) - base_u32);
+  constexpr int S = R;
+  uint8_t *sW = smem;                        // R x [W2 k-half 0 | W2 k-half 1]
+  uint8_t *sA = sW + S * STAGE;              // R x SLOT
+  uint8_t *sZ = sA + R * SLOT;               // 2 x Z_BYTES
+  uint8_t *sW1 = sZ + 2 * ((Z_BYTES + 1023u) & ~1023u);  // this CTA's W1 rows of every chunk of the net
+  uint8_t *sST = sW1 + ((a.chunks * W1_CH + 1023u) & ~1023u);  // NEPI x 2 x 1 KB h2 store staging
+  float *sB2 = reinterpret_cast<float *>(sST + NEPI * 2 * 1024);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sB2 + 2 * NP);
+  // ready[i]: leader = both operands of chunk i in both CTAs (leader copy warp, odd forwarder, incoming
+  //   copy, W2 TMA of both CTAs); odd CTA = the incoming half-chunk.  freed[i]: both pairs consumed it.
+  uint64_t *ready = bar, *freed = ready + R, *zfull = freed + R, *zempty = zfull + 2, *a1full = zempty + 2,
+           *a1empty = a1full + NA1, *own = a1empty + NA1, *c2full = own + R, *c2empty = c2full + 1,
+           *bfull = c2empty + 1, *bempty = bfull + 2, *w1full = bempty + 2, *w1empty = w1full + 1;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(w1empty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = rcx::cluster_rank();
+  const int pr = (int)(rank >> 1), prank = (int)(rank & 1);  // pair (= layer-2 pass), rank in the pair
+  const uint32_t lead = rank & ~1u, partner = rank ^ 2u;
+  const uint16_t pair_mask = (uint16_t)(3u << (2 * pr));
+  if (warp == W_TMA && lane == 0) {
+    rcx::prefetch_tmap(&mapZ);
+    rcx::prefetch_tmap(&mapW1);
+    rcx::prefetch_tmap(&mapW2a);
+    rcx::prefetch_tmap(&mapW2b);
+    rcx::prefetch_tmap(&mapOut);
+    for (int r = 0; r < R; ++r) {
+      rcx::mbar_init(&ready[r], prank == 0 ? 5 : 1);
+      rcx::mbar_init(&freed[r], 2);
+      rcx::mbar_init(&own[r], NPROD);
+    }
+    rcx::mbar_init(w1full, 2);
+    rcx::mbar_init(w1empty, 1);
+    for (int z = 0; z < 2; ++z) {
+      rcx::mbar_init(&zfull[z], 2);
+      rcx::mbar_init(&zempty[z], 1);
+      rcx::mbar_init(&bfull[z], 1);
+      rcx::mbar_init(&bempty[z], NEPI);
+    }
+    for (int z = 0; z < NA1; ++z) {
+      rcx::mbar_init(&a1full[z], 1);
+      rcx::mbar_init(&a1empty[z], 2 * NPROD);
+    }
+    rcx::mbar_init(c2full, 1);
+    rcx::mbar_init(c2empty, 2 * NEPI);
+    rcx::fence_mbar_init();
+  }
+  if (warp == W_MMA) rcx::tmem_alloc_pair(tmem_slot, 512);
+  rcx::tc_fence_before();
+  rcx::cluster_sync();
+  rcx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int C = a.chunks;  // 64-column h1 chunks (K chunks of layer 2)
+  const int pairs = a.m_tiles / 2;
+  const int total = a.nets * pairs;
+  const int cl = blockIdx.x >> 2, ncl = gridDim.x >> 2;
+
+  if (warp == W_TMA) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer (all CTAs)
+      const uint32_t ready0 = rcx::map_cta(ready, lead), zfull0 = rcx::map_cta(zfull, lead);
+      const uint32_t w1full0 = rcx::map_cta(w1full, lead);
+      uint32_t g = 0, nw = 0;
+      int it = 0, cur_net = -1;
+      for (int tile = cl; tile < total; tile += ncl, ++it) {
+        const int mp = tile % pairs, net = tile / pairs;
+        const int zb = it & 1;
+        if (net != cur_net) {  // this CTA's W1 rows of all chunks of the new net (one 5D box)
+          rcx::mbar_wait_sleep(w1empty, (nw & 1) ^ 1);
+          rcx::mbar_arrive_expect_tx_cluster(w1full0, C * W1_CH);
+          rcx::tma_load_5d_pair(sW1, &mapW1, w1full, 0, 0, pr * 2 + prank, 0, net);
+          cur_net = net;
+          ++nw;
+        }
+        rcx::mbar_wait_sleep(&zempty[zb], ((it >> 1) & 1) ^ 1);
+        rcx::mbar_arrive_expect_tx_cluster(zfull0 + zb * 8, Z_BYTES);
+        rcx::tma_load_3d_pair(sZ + zb * ((Z_BYTES + 1023u) & ~1023u), &mapZ, &zfull[zb], 0, mp * 256 + prank * 128, 0);
+        rcx::mbar_wait_sleep(&bempty[zb], ((it >> 1) & 1) ^ 1);
+        rcx::mbar_arrive_expect_tx(&bfull[zb], NP * 4);
+        rcx::bulk_g2s(sB2 + zb * NP, a.bias + (size_t)net * a.N + pr * NP, NP * 4, &bfull[zb]);
+        for (int c = 0; c < C; ++c, ++g) {
+          const int s = (int)(g % S);
+          rcx::mbar_wait_sleep(&freed[s], ((g / S) & 1) ^ 1);
+          rcx::mbar_arrive_expect_tx_cluster(ready0 + s * 8, STAGE_BYTES);
+          uint8_t *st = sW + s * STAGE;
+#pragma unroll
+          for (int kh = 0; kh < 2; ++kh) {
+            rcx::tma_load_3d_pair(st + kh * W2H_AL, &mapW2a, &ready[s], c * 64 + kh * 32, pr * NP + prank * H1, net);
+            rcx::tma_load_3d_pair(st + kh * W2H_AL + H1 * 64, &mapW2b, &ready[s], c * 64 + kh * 32,
+                                  pr * NP + P1 + prank * H2, net);
+          }
+        }
+      }
+    }
+  } else if (warp == W_AUX && prank == 0) {
+    if (lane == 0) {  // ---------------------------------- layer-1 MMA issuer (pair leaders)
+      // Runs ahead of the layer-2 issuer by up to NA1 chunks (the layer-1 accumulators), so the
+      // GELU + DSMEM exchange of a half-chunk overlaps several layer-2 chunk periods.
+      constexpr uint32_t id1 = rcx::make_idesc(1u, 256, 32);
+      uint32_t g = 0, nw = 0;
+      int it = 0, cur_net = -1;
+      for (int tile = cl; tile < total; tile += ncl, ++it) {
+        const int zb = it & 1, net = tile / pairs;
+        if (net != cur_net) {
+          if (cur_net >= 0) rcx::mma_commit_pair_mask(w1empty, pair_mask);  // done with the previous net's W1
+          rcx::mbar_wait(w1full, nw & 1);
+          cur_net = net;
+          ++nw;
+        }
+        rcx::mbar_wait_sleep(&zfull[zb], (it >> 1) & 1);
+        const uint64_t dz = rcm::desc_sw<KZ * 2>(sZ + zb * ((Z_BYTES + 1023u) & ~1023u));
+        for (int c = 0; c < C; ++c, ++g) {
+          const uint32_t b = g % NA1;
+          rcx::mbar_wait(&a1empty[b], ((g / NA1) & 1) ^ 1);
+          rcx::tc_fence_after();
+          const uint64_t dw = rcm::desc_sw<KZ * 2>(sW1 + c * W1_CH);
+#pragma unroll
+          for (int k = 0; k < KZ / 16; ++k) rcx::mma_bf16_pair(tmem + TMEM_ACC1 + b * 32, dz + 2 * k, dw + 2 * k, id1, k != 0);
+          rcx::mma_commit_pair_mask(&a1full[b], pair_mask);
+        }
+        rcx::mma_commit_pair_mask(&zempty[zb], pair_mask);
+      }
+    }
+  } else if (warp == W_MMA) {
+    if (lane == 0 && prank == 0) {  // --------------------------------- layer-2 MMA issuer (pair leaders)
+      constexpr uint32_t idp1 = rcx::make_idesc(1u, 256, P1), idp2 = rcx::make_idesc(1u, 256, P2);
+      uint32_t G = 0;
+      int it = 0;
+      for (int tile = cl; tile < total; tile += ncl, ++it, G += C) {
+        rcx::mbar_wait_sleep(c2empty, (it & 1) ^ 1);  // previous tile's acc2 copied out
+        rcx::tc_fence_after();
+        for (int c = 0; c < C; ++c) {
+          const uint32_t g = G + c;
+          const int s = (int)(g % R), slot = s;
+          TR(0, g, 0);
+          rcx::mbar_wait(&ready[s], (g / R) & 1);  // W2 stage and h1 chunk, both CTAs of the pair
+          TR(0, g, 1);
+          rcx::tc_fence_after();
+          uint8_t *A = sA + slot * SLOT;
+          uint8_t *B = sW + s * STAGE;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {  // K16 steps: 0-1 in the first half-chunk, 2-3 in the second
+            const uint64_t da = rcm::desc_sw<64>(A + (k >> 1) * HALF) + 2 * (k & 1);
+            const uint64_t db = rcm::desc_sw<64>(B + (k >> 1) * W2H_AL) + 2 * (k & 1);
+            const uint32_t acc = (c | k) != 0;
+            rcx::mma_bf16_pair(tmem, da, db, idp1, acc);
+            rcx::mma_bf16_pair(tmem + P1, da, db + ((H1 * 64) >> 4), idp2, acc);
+          }
+          rcx::mma_commit_pair_mask(&freed[s], (uint16_t)0xF);  // all four CTAs wait for both pairs
+          TR(0, g, 2);
+        }
+        rcx::mma_commit_pair_mask(c2full, pair_mask);
+      }
+    }
+  } else if (warp == W_CPY) {
+    if (lane == 0) {  // -------------------------------------- this CTA's half-chunk -> the other pair
+      const uint32_t ready_lead = rcx::map_cta(ready, lead);
+      uint32_t g = 0;
+      for (int tile = cl; tile < total; tile += ncl)
+        for (int c = 0; c < C; ++c, ++g) {
+          const int slot = (int)(g % R);
+          rcx::mbar_wait(&own[slot], (g / R) & 1);  // this CTA's half-chunk is in the slot
+          uint8_t *mine = sA + slot * SLOT + pr * HALF;
+          const uint32_t dst_bar = rcx::map_cta(&ready[slot], partner);
+          rcx::mbar_arrive_expect_tx_cluster(dst_bar, HALF);
+          rcx::bulk_s2s_cluster(rcx::map_cta(mine, partner), mine, HALF, dst_bar);
+          if (prank == 0) rcx::mbar_arrive_cluster(ready_lead + slot * 8);  // leader: own half in place
+        }
+    }
+  } else if (warp == W_AUX) {
+    if (lane == 0) {  // ---------------------------------- odd CTA: both halves in place -> leader
+      const uint32_t ready_lead = rcx::map_cta(ready, lead);
+      uint32_t g = 0;
+      for (int tile = cl; tile < total; tile += ncl)
+        for (int c = 0; c < C; ++c, ++g) {
+          const int slot = (int)(g % R);
+          const uint32_t par = (g / R) & 1;
+          TR(2, g, 0);
+          rcx::mbar_wait(&own[slot], par);
+          TR(2, g, 1);
+          rcx::mbar_wait(&ready[slot], par);  // the other pair's half-chunk arrived
+          TR(2, g, 2);
+          rcx::mbar_arrive_cluster(ready_lead + slot * 8);
+        }
+    }
+  } else {  // ------------------------------------------------------ epilogue warps 0..15
+    const int q = warp & 3, sub = warp >> 2;
+    const bool producer = warp < NPROD;
+    const int ph = (warp >> 2) & 1;  // producers: 16-column half of this pair's 32-column half-chunk
+    const uint32_t tq = (uint32_t)(q * 32) << 16;
+    constexpr int NCH = NP / 16;
+    const int ch_lo = (NCH * sub) / 4, ch_hi = (NCH * (sub + 1)) / 4, nch = ch_hi - ch_lo;
+    const uint32_t c2empty0 = rcx::map_cta(c2empty, lead), a1empty0 = rcx::map_cta(a1empty, lead);
+    uint8_t *stg_base = sST + warp * 2 * 1024;
+    const int row = q * 32 + lane;
+    uint32_t nst = 0;
+    // h1 production of global chunk g (this CTA's tiles in order, C chunks each)
+    auto produce = [&](uint32_t g) {
+      const uint32_t b = g % NA1;
+      if (warp == 0) TR(1, g, 0);
+      rcx::mbar_wait(&a1full[b], (g / NA1) & 1);
+      if (warp == 0) TR(1, g, 1);
+      rcx::tc_fence_after();
+      uint32_t v[16];
+      rcx::tmem_ld16(tmem + tq + TMEM_ACC1 + b * 32 + ph * 16, v);
+      rcx::tmem_ld_wait();
+      rcx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) rcx::mbar_arrive_cluster(a1empty0 + b * 8);
+      uint32_t pk[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        pk[j] = rcm::gelu_half_bf16x2(cvt_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1])));
+      const int slot = (int)(g % R);
+      rcx::mbar_wait(&freed[slot], ((g / R) & 1) ^ 1);  // both pairs are done with the slot
+      if (warp == 0) TR(1, g, 2);
+      uint8_t *r = sA + slot * SLOT + pr * HALF + row * 64;
+      const int x = (row >> 1) & 3;  // 64-byte swizzle: 16-byte unit u of row r at u ^ ((r >> 1) & 3)
+      *reinterpret_cast<uint4 *>(r + (((2 * ph) ^ x) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      *reinterpret_cast<uint4 *>(r + (((2 * ph + 1) ^ x) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      rcm::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) rcx::mbar_arrive(&own[slot]);
+      if (warp == 0) TR(1, g, 3);
+    };
+    // drain acc2 of this CTA's it-th tile (128 rows x 400 columns): two-phase as in the layer-2 kernel
+    auto drain = [&](int it, int tile) {
+      const int mp = tile % pairs, net = tile / pairs;
+      rcx::mbar_wait_sleep(c2full, it & 1);
+      rcx::mbar_wait(&bfull[it & 1], (it >> 1) & 1);
+      rcx::tc_fence_after();
+      const float *b2 = sB2 + (it & 1) * NP;
+      const int grow = mp * 256 + prank * 128 + q * 32;
+      uint32_t pk[MAXCH][8];
+#pragma unroll
+      for (int c = 0; c < MAXCH; ++c) {
+        if (c < nch) {
+          uint32_t v[16];
+          rcx::tmem_ld16(tmem + tq + (ch_lo + c) * 16, v);
+          rcx::tmem_ld_wait();
+          const float4 *bb = reinterpret_cast<const float4 *>(b2 + (ch_lo + c) * 16);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 bv = bb[j];
+            pk[c][2 * j] = cvt_bf16x2(__uint_as_float(v[4 * j]) + bv.x, __uint_as_float(v[4 * j + 1]) + bv.y);
+            pk[c][2 * j + 1] = cvt_bf16x2(__uint_as_float(v[4 * j + 2]) + bv.z, __uint_as_float(v[4 * j + 3]) + bv.w);
+          }
+        }
+      }
+      rcx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
+#pragma unroll
+      for (int c = 0; c < MAXCH; ++c) {
+        if (c < nch) {
+          uint32_t gg[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) gg[j] = gelu_bf16x2(pk[c][j]);
+          uint8_t *stg = stg_base + (nst & 1) * 1024;
+          if (lane == 0) rcm::bulk_wait_read1();
+          __syncwarp();
+          const int sw = (lane >> 2) & 1;
+          *reinterpret_cast<uint4 *>(stg + lane * 32 + (sw << 4)) = make_uint4(gg[0], gg[1], gg[2], gg[3]);
+          *reinterpret_cast<uint4 *>(stg + lane * 32 + ((sw ^ 1) << 4)) = make_uint4(gg[4], gg[5], gg[6], gg[7]);
+          rcm::fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            rcm::tma_store_3d(&mapOut, stg, pr * NP + (ch_lo + c) * 16, grow, net);
+            rcm::bulk_commit();
+          }
+          ++nst;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) rcx::mbar_arrive(&bempty[it & 1]);
+    };
+    const int ntiles = cl < total ? (total - 1 - cl) / ncl + 1 : 0;
+    if (producer) {
+      // Produce the first min(R, C) chunks of tile t+1 before draining tile t: they only need slots
+      // the end of tile t's mainloop frees, so the next tile's MMAs start right after the drain's
+      // copy-out instead of waiting for production to restart.
+      const int lead_in = a.lead_in < C ? a.lead_in : C;
+      const uint32_t nchunks = (uint32_t)ntiles * C;
+      int dt = 0;  // next tile to drain
+      for (uint32_t g = 0; g < nchunks; ++g) {
+        produce(g);
+        if (g + 1 == (uint32_t)(dt + 1) * C + lead_in) {
+          drain(dt, cl + dt * ncl);
+          ++dt;
+        }
+      }
+      for (; dt < ntiles; ++dt) drain(dt, cl + dt * ncl);
+    } else {
+      for (int it = 0; it < ntiles; ++it) drain(it, cl + it * ncl);
+    }
+    if (lane == 0) rcm::bulk_wait_all();
+    __syncwarp();
+  }
+  rcx::tc_fence_before();
+  rcx::cluster_sync();
+  if (warp == W_MMA) {
+    rcx::tc_fence_after();
+    rcx::tmem_dealloc_pair(tmem, 512);
+  }
+}
+
+template <int KZ>
+int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
+  constexpr int R = KZ == 16 ? 4 : 3;
+  constexpr size_t Z_AL = ((size_t)128 * KZ * 2 + 1023) & ~(size_t)1023;
+  constexpr size_t STAGE = 2 * W2H_AL;
+  const size_t w1 = ((size_t)a.chunks * 16 * KZ * 2 + 1023) & ~(size_t)1023;
+  const size_t smem = 1024 + R * (SLOT + STAGE) + 2 * Z_AL + w1 + NEPI * 2 * 1024 + 2 * NP * 4 + 1024;
+  if (smem > 232448) return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel: shared memory");
+  a.stages = R;
+  static int li = -1;
+  if (li < 0) {
+    const char *e = getenv("RC_L12_LEADIN");  // experiments (tools/l12var.sh)
+    li = e ? atoi(e) : R;
+  }
+  a.lead_in = li < 0 ? 0 : (li > R ? R : li);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(l12_kernel<KZ, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    attr = true;
+  }
+  // persistent grid: only as many clusters of four as can be resident at once (a 4-CTA cluster
+  // must fit in one GPC, so fewer than 148 / 4 are; a second wave would serialise their tiles)
+  static int resident = 0;
+  if (!resident) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(4 * (mlp_num_sms() / 4));
+    cfg.blockDim = dim3(L12_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 4;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&resident, l12_kernel<KZ, R>, &cfg) != cudaSuccess || resident <= 0)
+      resident = mlp_num_sms() / 4;
+    if (getenv("RC_VERBOSE")) fprintf(stderr, "fused layer-1/2 kernel: %d resident clusters of 4\n", resident);
+  }
+  const int total = a.nets * (a.m_tiles / 2);
+  int clusters = resident;
+  if (clusters > total) clusters = total;
+  l12_kernel<KZ, R><<<4 * clusters, L12_THREADS, smem, s>>>(M[0], M[1], M[2], M[3], M[4], a);
+  RC_LAUNCH_CHECK();
+  return RC_OK;
+}
+
+}  // namespace
+
+bool l12_supported(int h1, int h2, int kz) { return h1 % 64 == 0 && h2 == 2 * NP && (kz == 16 || kz == 32); }
+
+#ifdef L12TRACE
+extern "C" __attribute__((visibility("default"))) int rc_debug_l12trace(void *host) {
+  return (int)cudaMemcpyFromSymbol(host, g_l12trace, sizeof(g_l12trace));
+}
+#endif
+
+int launch_l12(int KZ, const CUtensorMap *maps, const L12Args &a, cudaStream_t s) {
+  ProfScope prof(RC_STAGE_L2, s);
+  if (KZ == 16) return launch_t<16>(maps, a, s);
+  if (KZ == 32) return launch_t<32>(maps, a, s);
+  return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel: K = %d", KZ);
+}

@@ -413,8 +413,25 @@ int launch_l2_pair_t(const CUtensorMap *M, L2Args a, cudaStream_t s) {
     cudaFuncSetAttribute(l2_pair_kernel<NP, DOT, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     attr = true;
   }
+  static int resident = 0;  // CTA pairs that fit at once (a persistent grid must not need a second wave)
+  if (!resident) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * (mlp_num_sms() / 2));
+    cfg.blockDim = dim3(L2_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&resident, l2_pair_kernel<NP, DOT, PREC>, &cfg) != cudaSuccess || resident <= 0)
+      resident = mlp_num_sms() / 2;
+    if (getenv("RC_VERBOSE")) fprintf(stderr, "pair GEMM<%d,%d,%d>: %d resident CTA pairs\n", NP, (int)DOT, PREC, resident);
+  }
   const int total = a.nets * (a.m_tiles / 2) * a.passes;
-  int clusters = mlp_num_sms() / 2;
+  int clusters = resident;
   if (clusters > total) clusters = total;
   l2_pair_kernel<NP, DOT, PREC><<<2 * clusters, L2_THREADS, smem, s>>>(M[0], M[1], M[2], M[3], M[4], M[5], M[6], M[7], a);
   RC_LAUNCH_CHECK();

@@ -307,6 +307,23 @@ int make_map(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint64_
   return RC_OK;
 }
 
+// W1 [nets][h1][KZ] bf16 as 5D {KZ, 16 rows, 4 row groups, h1/64 chunks, nets}: one box = the 16 rows
+// of group g (= 2 pair + rank, the CTA of the fused layer-1/2 cluster) in every 64-row chunk
+int make_map_w1_groups(CUtensorMap *m, const void *W1, int KZ, int h1, int nets) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return rc_fail(RC_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t row = (cuuint64_t)KZ * 2;
+  cuuint64_t dims[5] = {(cuuint64_t)KZ, 16, 4, (cuuint64_t)(h1 / 64), (cuuint64_t)nets};
+  cuuint64_t strides[4] = {row, 16 * row, 64 * row, (cuuint64_t)h1 * row};
+  cuuint32_t box[5] = {(cuuint32_t)KZ, 16, 1, (cuuint32_t)(h1 / 64), 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const CUtensorMapSwizzle sw = KZ * 2 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(W1), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return rc_fail(RC_ECUDA, "cuTensorMapEncodeTiled (W1 groups) failed (%d)", (int)r);
+  return RC_OK;
+}
+
 }  // namespace
 int mlp_num_sms() {
   static int n = 0;
@@ -515,6 +532,16 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
       return rc;
     a3[3] = a2[3];  // unused by the dot epilogue
   }
+  // fused layers 1+2 (bf16, paper widths); RC_NO_FUSE=1 forces the layer-wise path (tests, comparisons)
+  const char *nf = getenv("RC_NO_FUSE");
+  const bool fused = prec == 0 && l12_supported(n->h1, n->h2, KZ) && !(nf && nf[0] == '1');
+  CUtensorMap m12[5];
+  if (fused && ((rc = make_map(&m12[0], z, KZ, cap, 1, BM, KZ, EB)) ||
+                (rc = make_map_w1_groups(&m12[1], n->d_W1, KZ, n->h1, nets)) ||
+                (rc = make_map(&m12[2], n->d_W2, n->h1, n->h2, nets, 128, 32, EB)) ||
+                (rc = make_map(&m12[3], n->d_W2, n->h1, n->h2, nets, 72, 32, EB)) ||
+                (rc = make_map(&m12[4], h2, n->h2, cap, nets, 32, 16, EB))))
+    return rc;
   if (!x3) {  // the lo slots are never read: any valid map
     for (int k = 0; k < 3; ++k) m1[3 + k] = m1[k];
     for (int k = 0; k < 4; ++k) m2[4 + k] = m2[k], m3[4 + k] = m3[k];
@@ -531,12 +558,18 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
       prologue_kernel<<<(mt * BM + 255) / 256, 256, 0, s>>>(pa, c);
       RC_LAUNCH_CHECK();
     }
-    // layer 1: h1 = GELU(z W1^T) (b1 folded into z's constant-1 columns)
-    L1Args g1{mt, (n->h1 + bn1 - 1) / bn1, nets, n->h1, 0, cap};
-    if ((rc = launch_l1(KZ, prec, m1, g1, s))) return rc;
-    // layer 2: h2 = GELU(h1 W2^T + b2), CTA-pair GEMM
-    L2Args la{mt, n->h2 / NP, nets, (n->h1 + KC - 1) / KC, n->h2, 0, n->d_b2, nullptr, nullptr, cap};
-    if ((rc = launch_l2_pair(NP, prec, m2, la, s))) return rc;
+    if (fused) {
+      // layers 1+2 in one kernel: h1 stays on chip (clusters of two CTA pairs share its chunks)
+      L12Args g12{mt, nets, n->h1 / 64, n->h2, 0, 0, n->d_b2};
+      if ((rc = launch_l12(KZ, m12, g12, s))) return rc;
+    } else {
+      // layer 1: h1 = GELU(z W1^T) (b1 folded into z's constant-1 columns)
+      L1Args g1{mt, (n->h1 + bn1 - 1) / bn1, nets, n->h1, 0, cap};
+      if ((rc = launch_l1(KZ, prec, m1, g1, s))) return rc;
+      // layer 2: h2 = GELU(h1 W2^T + b2), CTA-pair GEMM
+      L2Args la{mt, n->h2 / NP, nets, (n->h1 + KC - 1) / KC, n->h2, 0, n->d_b2, nullptr, nullptr, cap};
+      if ((rc = launch_l2_pair(NP, prec, m2, la, s))) return rc;
+    }
     // layer 3 + folded layer 4: the same CTA-pair GEMM with the dot epilogue (K = h2, zero-filled to KC)
     L2Args l3{mt, n->h3 / NP3, nets, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, n->d_w4, opart, cap};
     if ((rc = launch_l2_pair(NP3, prec, m3, l3, s))) return rc;
