@@ -197,7 +197,9 @@ int rc_partition(int64_t n_global, int rank, int world, int64_t *begin, int64_t 
  * ------------------------------------------------------------------------- */
 enum {
   RC_STAGE_THERMO = 0, RC_STAGE_TRANSPORT = 1, RC_STAGE_PROLOGUE = 2, RC_STAGE_L1 = 3, RC_STAGE_L2 = 4,
-  RC_STAGE_L3 = 5, RC_STAGE_EPILOGUE = 6, RC_STAGE_FINALIZE = 7, RC_STAGE_COUNT = 8
+  RC_STAGE_L3 = 5, RC_STAGE_EPILOGUE = 6, RC_STAGE_FINALIZE = 7,
+  RC_STAGE_L12 = 8,  /* fused layers 1+2 (bf16 at the paper widths; replaces L1 and L2) */
+  RC_STAGE_COUNT = 9
 };
 int rc_profile_enable(int on);
 int rc_profile_read(double *ms /* [RC_STAGE_COUNT] */, int64_t *launches /* [RC_STAGE_COUNT] */, int reset);

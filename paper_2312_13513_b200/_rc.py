@@ -199,7 +199,7 @@ def rc_last_launch_count():
     return int(lib().rc_last_launch_count())
 
 
-STAGES = ["thermo", "transport", "prologue", "L1", "L2", "L3", "epilogue", "finalize"]
+STAGES = ["thermo", "transport", "prologue", "L1", "L2", "L3", "epilogue", "finalize", "L12"]
 
 
 def rc_profile_enable(on=True):

@@ -446,7 +446,7 @@ extern "C" __attribute__((visibility("default"))) int rc_debug_l12trace(void *ho
 #endif
 
 int launch_l12(int KZ, const CUtensorMap *maps, const L12Args &a, cudaStream_t s) {
-  ProfScope prof(RC_STAGE_L2, s);
+  ProfScope prof(RC_STAGE_L12, s);
   if (KZ == 16) return launch_t<16>(maps, a, s);
   if (KZ == 32) return launch_t<32>(maps, a, s);
   return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel: K = %d", KZ);

@@ -108,8 +108,10 @@ def main():
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     json.dump(out, open(os.path.join(ROOT, "profiles", f"ncu_{tag}.json"), "w"), indent=1)
     traffic = {k: v.get("dram_bytes") for k, v in caps.items()}
+    l12 = next((v for k, v in traffic.items() if "l12_kernel" in k), None)  # fused layers 1+2 (default bf16 path)
     l2 = next((v for k, v in traffic.items() if "l2_pair_kernel" in k and ", 0, " in k), None)  # layer 2 (not DOT)
-    json.dump({"per_launch_dram_bytes": traffic, "L2_gemm_dram_bytes_per_launch": l2,
+    json.dump({"per_launch_dram_bytes": traffic, "dominant_kernel_dram_bytes_per_launch": l12 if l12 else l2,
+               "L2_gemm_dram_bytes_per_launch": l2,
                "source": f"ncu --set full, profiles/ncu_{tag}.json"},
               open(os.path.join(ROOT, "profiles", f"traffic_{tag}.json"), "w"), indent=1)
     print(json.dumps(out["launch_list"], indent=1)[:3000])
