@@ -199,7 +199,8 @@ extern "C" int rc_mech_create(const rc_mech_desc *d, rc_mech **out) {
     }
   if (cudaMalloc(&m->d_thermo, th.size() * 8) != cudaSuccess ||
       cudaMalloc(&m->d_transport, tr.size() * 8) != cudaSuccess ||
-      cudaMalloc(&m->d_P, ns * ns * 8) != cudaSuccess) {
+      cudaMalloc(&m->d_P, (size_t)((ns * ns + 1) & ~1) * 8) != cudaSuccess ||  // padded: 16-byte bulk copies
+      cudaMemset(m->d_P, 0, (size_t)((ns * ns + 1) & ~1) * 8) != cudaSuccess) {
     rc_mech_destroy(m);
     return rc_fail(RC_ENOMEM, "rc_mech_create: cudaMalloc failed");
   }

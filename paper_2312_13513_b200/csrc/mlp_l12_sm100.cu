@@ -16,9 +16,9 @@
 // 64-byte-swizzled [128 rows][32 cols] tiles, which is how the layer-2 MMAs read
 // it (K steps 0-1 from the first half, 2-3 from the second).
 //
-// Per CTA and 64-column chunk this costs 4096 GELUs (256 clk of MUFU) against
-// 800 clk of layer-2 MMA, instead of a separate layer-1 pass writing and then
-// re-reading 3.2 KB of h1 per cell and net.
+// Per CTA and chunk period this costs on average 4096 GELUs (256 clk of MUFU)
+// against 800 clk of layer-2 MMA, instead of a separate layer-1 pass writing and
+// then re-reading 3.2 KB of h1 per cell and net.
 //
 // Barriers (per CTA; "leader" = even CTA of a pair, which issues the MMAs):
 //   full/empty[S]   W2 + W1 stages (pair TMA, leader counts both CTAs' bytes)
@@ -45,13 +45,11 @@ constexpr int NEPI = 16, NPROD = 8;
 // W_AUX: the layer-1 MMA issuer in the even CTA of a pair, the slot forwarder in the odd one
 constexpr int W_TMA = NEPI, W_MMA = NEPI + 1, W_CPY = NEPI + 2, W_AUX = NEPI + 3;
 constexpr int L12_THREADS = 32 * (NEPI + 4);
-constexpr int NA1 = 3;                        // layer-1 accumulators (32 TMEM columns each)
+constexpr int NA1 = 1;                        // layer-1 accumulator (64 TMEM columns)
 constexpr int NP = 400, P1 = 256, P2 = 144, H1 = P1 / 2, H2 = P2 / 2;  // pass width and its two MMA pieces
-constexpr uint32_t HALF = 128 * 64;           // [128 rows][32 bf16] half-chunk, 64-byte swizzle (8 KB)
-constexpr uint32_t SLOT = 2 * HALF;
-constexpr uint32_t W2H = (NP / 2) * 64;       // W2 K-half tile of one CTA: 200 rows x 64 B (12.8 KB)
-constexpr uint32_t W2H_AL = 13312;            // 1 KB aligned
-constexpr uint32_t TMEM_ACC1 = 416;          // acc2 uses [0, 400); acc1 b at 416 + 32 b
+constexpr uint32_t SLOT = 128 * 128;         // [128 rows][64 bf16] h1 chunk, 128-byte swizzle (16 KB)
+constexpr uint32_t W2T = (NP / 2) * 128;      // W2 chunk tile of one CTA: 200 rows x 128 B (25.6 KB)
+constexpr uint32_t TMEM_ACC1 = 448;          // acc2 uses [0, 400)
 
 using rcm::cvt_bf16x2;
 using rcm::gelu_bf16x2;
@@ -75,24 +73,25 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
     l12_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapW1,
                const __grid_constant__ CUtensorMap mapW2a, const __grid_constant__ CUtensorMap mapW2b,
                const __grid_constant__ CUtensorMap mapOut, L12Args a) {
-  constexpr uint32_t Z_BYTES = 128 * KZ * 2, W1_CH = 16 * KZ * 2;  // W1: 16 rows per CTA and chunk
-  constexpr uint32_t STAGE_BYTES = 2 * W2H;                         // TMA bytes per CTA
-  constexpr uint32_t STAGE = 2 * W2H_AL;                            // layout size
+  constexpr uint32_t Z_BYTES = 128 * KZ * 2, W1_CH = 32 * KZ * 2;  // W1: 32 rows per CTA and chunk
+  constexpr uint32_t STAGE_BYTES = W2T;                             // TMA bytes per CTA
+  constexpr uint32_t STAGE = (W2T + 1023u) & ~1023u;                // layout size
   constexpr int MAXCH = (NP / 16 + 3) / 4;
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = rcx::smem_u32(smem_raw);
   uint8_t *smem = smem_raw + (((base_u32 + 1023u) & ~1023u) - base_u32);
   constexpr int S = R;
-  uint8_t *sW = smem;                        // R x [W2 k-half 0 | W2 k-half 1]
+  uint8_t *sW = smem;                        // R x W2 chunk tile
   uint8_t *sA = sW + S * STAGE;              // R x SLOT
   uint8_t *sZ = sA + R * SLOT;               // 2 x Z_BYTES
-  uint8_t *sW1 = sZ + 2 * ((Z_BYTES + 1023u) & ~1023u);  // this CTA's W1 rows of every chunk of the net
-  uint8_t *sST = sW1 + ((a.chunks * W1_CH + 1023u) & ~1023u);  // NEPI x 2 x 1 KB h2 store staging
+  uint8_t *sW1 = sZ + 2 * ((Z_BYTES + 1023u) & ~1023u);  // this CTA's W1 rows of its pair's chunks of the net
+  uint8_t *sST = sW1 + ((((a.chunks + 1) / 2) * W1_CH + 1023u) & ~1023u);  // NEPI x 2 x 1 KB h2 store staging
   float *sB2 = reinterpret_cast<float *>(sST + NEPI * 2 * 1024);
   uint64_t *bar = reinterpret_cast<uint64_t *>(sB2 + 2 * NP);
-  // ready[i]: leader = both operands of chunk i in both CTAs (leader copy warp, odd forwarder, incoming
-  //   copy, W2 TMA of both CTAs); odd CTA = the incoming half-chunk.  freed[i]: both pairs consumed it.
+  // ready[i]: leader = both operands of chunk i in both CTAs (its slot: own copier or incoming copy;
+  //   the odd forwarder; W2 TMA of both CTAs); odd CTA = its slot.  own[i]: the local producers wrote
+  //   slot i (chunks of this pair).  freed[i]: both pairs consumed chunk i's slot and stage.
   uint64_t *ready = bar, *freed = ready + R, *zfull = freed + R, *zempty = zfull + 2, *a1full = zempty + 2,
            *a1empty = a1full + NA1, *own = a1empty + NA1, *c2full = own + R, *c2empty = c2full + 1,
            *bfull = c2empty + 1, *bempty = bfull + 2, *w1full = bempty + 2, *w1empty = w1full + 1;
@@ -110,7 +109,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
     rcx::prefetch_tmap(&mapW2b);
     rcx::prefetch_tmap(&mapOut);
     for (int r = 0; r < R; ++r) {
-      rcx::mbar_init(&ready[r], prank == 0 ? 5 : 1);
+      rcx::mbar_init(&ready[r], prank == 0 ? 4 : 1);
       rcx::mbar_init(&freed[r], 2);
       rcx::mbar_init(&own[r], NPROD);
     }
@@ -151,8 +150,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
         const int zb = it & 1;
         if (net != cur_net) {  // this CTA's W1 rows of all chunks of the new net (one 5D box)
           rcx::mbar_wait_sleep(w1empty, (nw & 1) ^ 1);
-          rcx::mbar_arrive_expect_tx_cluster(w1full0, C * W1_CH);
-          rcx::tma_load_5d_pair(sW1, &mapW1, w1full, 0, 0, pr * 2 + prank, 0, net);
+          rcx::mbar_arrive_expect_tx_cluster(w1full0, ((C + 1) / 2) * W1_CH);
+          rcx::tma_load_5d_pair(sW1, &mapW1, w1full, 0, 0, pr * 2 + prank, 0, net);  // rows c*64 + 32 prank, c%2 == pr
           cur_net = net;
           ++nw;
         }
@@ -167,12 +166,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           rcx::mbar_wait_sleep(&freed[s], ((g / S) & 1) ^ 1);
           rcx::mbar_arrive_expect_tx_cluster(ready0 + s * 8, STAGE_BYTES);
           uint8_t *st = sW + s * STAGE;
-#pragma unroll
-          for (int kh = 0; kh < 2; ++kh) {
-            rcx::tma_load_3d_pair(st + kh * W2H_AL, &mapW2a, &ready[s], c * 64 + kh * 32, pr * NP + prank * H1, net);
-            rcx::tma_load_3d_pair(st + kh * W2H_AL + H1 * 64, &mapW2b, &ready[s], c * 64 + kh * 32,
-                                  pr * NP + P1 + prank * H2, net);
-          }
+          rcx::tma_load_3d_pair(st, &mapW2a, &ready[s], c * 64, pr * NP + prank * H1, net);
+          rcx::tma_load_3d_pair(st + H1 * 128, &mapW2b, &ready[s], c * 64, pr * NP + P1 + prank * H2, net);
         }
       }
     }
@@ -180,7 +175,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
     if (lane == 0) {  // ---------------------------------- layer-1 MMA issuer (pair leaders)
       // Runs ahead of the layer-2 issuer by up to NA1 chunks (the layer-1 accumulators), so the
       // GELU + DSMEM exchange of a half-chunk overlaps several layer-2 chunk periods.
-      constexpr uint32_t id1 = rcx::make_idesc(1u, 256, 32);
+      constexpr uint32_t id1 = rcx::make_idesc(1u, 256, 64);
       uint32_t g = 0, nw = 0;
       int it = 0, cur_net = -1;
       for (int tile = cl; tile < total; tile += ncl, ++it) {
@@ -193,13 +188,13 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
         }
         rcx::mbar_wait_sleep(&zfull[zb], (it >> 1) & 1);
         const uint64_t dz = rcm::desc_sw<KZ * 2>(sZ + zb * ((Z_BYTES + 1023u) & ~1023u));
-        for (int c = 0; c < C; ++c, ++g) {
+        for (int c = pr; c < C; c += 2, ++g) {  // g counts this pair's chunks
           const uint32_t b = g % NA1;
           rcx::mbar_wait(&a1empty[b], ((g / NA1) & 1) ^ 1);
           rcx::tc_fence_after();
-          const uint64_t dw = rcm::desc_sw<KZ * 2>(sW1 + c * W1_CH);
+          const uint64_t dw = rcm::desc_sw<KZ * 2>(sW1 + (c >> 1) * W1_CH);
 #pragma unroll
-          for (int k = 0; k < KZ / 16; ++k) rcx::mma_bf16_pair(tmem + TMEM_ACC1 + b * 32, dz + 2 * k, dw + 2 * k, id1, k != 0);
+          for (int k = 0; k < KZ / 16; ++k) rcx::mma_bf16_pair(tmem + TMEM_ACC1 + b * 64, dz + 2 * k, dw + 2 * k, id1, k != 0);
           rcx::mma_commit_pair_mask(&a1full[b], pair_mask);
         }
         rcx::mma_commit_pair_mask(&zempty[zb], pair_mask);
@@ -223,12 +218,11 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           uint8_t *A = sA + slot * SLOT;
           uint8_t *B = sW + s * STAGE;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {  // K16 steps: 0-1 in the first half-chunk, 2-3 in the second
-            const uint64_t da = rcm::desc_sw<64>(A + (k >> 1) * HALF) + 2 * (k & 1);
-            const uint64_t db = rcm::desc_sw<64>(B + (k >> 1) * W2H_AL) + 2 * (k & 1);
+          for (int k = 0; k < 4; ++k) {  // K16 steps: 32-byte atoms along the 128-byte rows
+            const uint64_t da = rcm::desc_sw<128>(A) + 2 * k, db = rcm::desc_sw<128>(B) + 2 * k;
             const uint32_t acc = (c | k) != 0;
             rcx::mma_bf16_pair(tmem, da, db, idp1, acc);
-            rcx::mma_bf16_pair(tmem + P1, da, db + ((H1 * 64) >> 4), idp2, acc);
+            rcx::mma_bf16_pair(tmem + P1, da, db + ((H1 * 128) >> 4), idp2, acc);
           }
           rcx::mma_commit_pair_mask(&freed[s], (uint16_t)0xF);  // all four CTAs wait for both pairs
           TR(0, g, 2);
@@ -237,18 +231,20 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
       }
     }
   } else if (warp == W_CPY) {
-    if (lane == 0) {  // -------------------------------------- this CTA's half-chunk -> the other pair
-      const uint32_t ready_lead = rcx::map_cta(ready, lead);
-      uint32_t g = 0;
+    if (lane == 0) {  // ------------------------------- this pair's chunks: slot ready here, copy to the other pair
+      uint32_t g = 0, my = 0;
       for (int tile = cl; tile < total; tile += ncl)
         for (int c = 0; c < C; ++c, ++g) {
+          if ((c & 1) != pr) continue;
           const int slot = (int)(g % R);
-          rcx::mbar_wait(&own[slot], (g / R) & 1);  // this CTA's half-chunk is in the slot
-          uint8_t *mine = sA + slot * SLOT + pr * HALF;
+          // own[] is indexed by this pair's chunk count (the pair skips every other chunk)
+          rcx::mbar_wait(&own[my % R], (my / R) & 1);  // the local producers wrote the chunk
+          ++my;
+          rcx::mbar_arrive(&ready[slot]);
+          uint8_t *src = sA + slot * SLOT;
           const uint32_t dst_bar = rcx::map_cta(&ready[slot], partner);
-          rcx::mbar_arrive_expect_tx_cluster(dst_bar, HALF);
-          rcx::bulk_s2s_cluster(rcx::map_cta(mine, partner), mine, HALF, dst_bar);
-          if (prank == 0) rcx::mbar_arrive_cluster(ready_lead + slot * 8);  // leader: own half in place
+          rcx::mbar_arrive_expect_tx_cluster(dst_bar, SLOT);
+          rcx::bulk_s2s_cluster(rcx::map_cta(src, partner), src, SLOT, dst_bar);
         }
     }
   } else if (warp == W_AUX) {
@@ -260,9 +256,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           const int slot = (int)(g % R);
           const uint32_t par = (g / R) & 1;
           TR(2, g, 0);
-          rcx::mbar_wait(&own[slot], par);
-          TR(2, g, 1);
-          rcx::mbar_wait(&ready[slot], par);  // the other pair's half-chunk arrived
+          rcx::mbar_wait(&ready[slot], par);  // the chunk is in this CTA's slot
           TR(2, g, 2);
           rcx::mbar_arrive_cluster(ready_lead + slot * 8);
         }
@@ -279,32 +273,42 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
     const int row = q * 32 + lane;
     uint32_t nst = 0;
     // h1 production of global chunk g (this CTA's tiles in order, C chunks each)
-    auto produce = [&](uint32_t g) {
-      const uint32_t b = g % NA1;
+    uint32_t lg = 0;  // this pair's chunks produced so far (layer-1 accumulator phase)
+    auto produce = [&](uint32_t g) {  // global chunk g: only this pair's chunks (g % C parity == pr)
+      if ((int)((g % C) & 1) != pr) return;
+      const uint32_t b = lg % NA1, my = lg;  // my: index among this pair's chunks (own[] ring)
       if (warp == 0) TR(1, g, 0);
-      rcx::mbar_wait(&a1full[b], (g / NA1) & 1);
+      rcx::mbar_wait(&a1full[b], (lg / NA1) & 1);
       if (warp == 0) TR(1, g, 1);
       rcx::tc_fence_after();
-      uint32_t v[16];
-      rcx::tmem_ld16(tmem + tq + TMEM_ACC1 + b * 32 + ph * 16, v);
+      uint32_t v[2][16];
+      rcx::tmem_ld16(tmem + tq + TMEM_ACC1 + b * 64 + ph * 32, v[0]);
+      rcx::tmem_ld16(tmem + tq + TMEM_ACC1 + b * 64 + ph * 32 + 16, v[1]);
       rcx::tmem_ld_wait();
       rcx::tc_fence_before();
       __syncwarp();
       if (lane == 0) rcx::mbar_arrive_cluster(a1empty0 + b * 8);
-      uint32_t pk[8];
+      ++lg;
+      uint32_t pk[2][8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        pk[j] = rcm::gelu_half_bf16x2(cvt_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1])));
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          pk[h][j] = rcm::gelu_half_bf16x2(cvt_bf16x2(__uint_as_float(v[h][2 * j]), __uint_as_float(v[h][2 * j + 1])));
       const int slot = (int)(g % R);
       rcx::mbar_wait(&freed[slot], ((g / R) & 1) ^ 1);  // both pairs are done with the slot
       if (warp == 0) TR(1, g, 2);
-      uint8_t *r = sA + slot * SLOT + pr * HALF + row * 64;
-      const int x = (row >> 1) & 3;  // 64-byte swizzle: 16-byte unit u of row r at u ^ ((r >> 1) & 3)
-      *reinterpret_cast<uint4 *>(r + (((2 * ph) ^ x) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-      *reinterpret_cast<uint4 *>(r + (((2 * ph + 1) ^ x) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      // columns [32 ph, 32 ph + 32) of the chunk = 16-byte units 4 ph .. 4 ph + 3 of the 128-byte row
+      uint8_t *r = sA + slot * SLOT + row * 128;
+      const int x = row & 7;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        *reinterpret_cast<uint4 *>(r + (((4 * ph + u) ^ x) << 4)) =
+            make_uint4(pk[u >> 1][4 * (u & 1)], pk[u >> 1][4 * (u & 1) + 1], pk[u >> 1][4 * (u & 1) + 2],
+                       pk[u >> 1][4 * (u & 1) + 3]);
       rcm::fence_async_smem();
       __syncwarp();
-      if (lane == 0) rcx::mbar_arrive(&own[slot]);
+      if (lane == 0) rcx::mbar_arrive(&own[my % R]);
       if (warp == 0) TR(1, g, 3);
     };
     // drain acc2 of this CTA's it-th tile (128 rows x 400 columns): two-phase as in the layer-2 kernel
@@ -392,8 +396,8 @@ template <int KZ>
 int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
   constexpr int R = KZ == 16 ? 4 : 3;
   constexpr size_t Z_AL = ((size_t)128 * KZ * 2 + 1023) & ~(size_t)1023;
-  constexpr size_t STAGE = 2 * W2H_AL;
-  const size_t w1 = ((size_t)a.chunks * 16 * KZ * 2 + 1023) & ~(size_t)1023;
+  constexpr size_t STAGE = ((size_t)W2T + 1023) & ~(size_t)1023;
+  const size_t w1 = ((size_t)((a.chunks + 1) / 2) * 32 * KZ * 2 + 1023) & ~(size_t)1023;
   const size_t smem = 1024 + R * (SLOT + STAGE) + 2 * Z_AL + w1 + NEPI * 2 * 1024 + 2 * NP * 4 + 1024;
   if (smem > 232448) return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel: shared memory");
   a.stages = R;

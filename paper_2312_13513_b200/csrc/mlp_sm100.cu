@@ -307,15 +307,18 @@ int make_map(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint64_
   return RC_OK;
 }
 
-// W1 [nets][h1][KZ] bf16 as 5D {KZ, 16 rows, 4 row groups, h1/64 chunks, nets}: one box = the 16 rows
-// of group g (= 2 pair + rank, the CTA of the fused layer-1/2 cluster) in every 64-row chunk
+// W1 [nets][h1][KZ] bf16 as 5D {KZ, 32 rows, 4 groups, h1/128 chunk pairs, nets}: row
+// 128 cp + 32 q4 + i.  One box at q4 = 2 pair + rank = the 32 rows a CTA of the fused
+// layer-1/2 cluster needs of each of its pair's chunks (c = 2 cp + pair).  The last chunk
+// pair may reach 64 rows past the net (zero-padded after the last net, see mlp_upload).
 int make_map_w1_groups(CUtensorMap *m, const void *W1, int KZ, int h1, int nets) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return rc_fail(RC_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t row = (cuuint64_t)KZ * 2;
-  cuuint64_t dims[5] = {(cuuint64_t)KZ, 16, 4, (cuuint64_t)(h1 / 64), (cuuint64_t)nets};
-  cuuint64_t strides[4] = {row, 16 * row, 64 * row, (cuuint64_t)h1 * row};
-  cuuint32_t box[5] = {(cuuint32_t)KZ, 16, 1, (cuuint32_t)(h1 / 64), 1};
+  const cuuint64_t cps = (cuuint64_t)(h1 / 64 + 1) / 2;
+  cuuint64_t dims[5] = {(cuuint64_t)KZ, 32, 4, cps, (cuuint64_t)nets};
+  cuuint64_t strides[4] = {row, 32 * row, 128 * row, (cuuint64_t)h1 * row};
+  cuuint32_t box[5] = {(cuuint32_t)KZ, 32, 1, (cuuint32_t)cps, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   const CUtensorMapSwizzle sw = KZ * 2 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(W1), dims, strides, box, estr,
@@ -401,7 +404,10 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
   const int nets = n->n_nets, din = n->d_in, h1 = n->h1, h2 = n->h2, h3 = n->h3, kp = n->kpad1;
   const size_t P = (size_t)h1 * din + h1 + (size_t)h2 * h1 + h2 + (size_t)h3 * h2 + h3 + h3 + 1;
   // weights, K-major [net][out][in]: bf16 (RNE) or tf32-rounded fp32
-  std::vector<uint16_t> W1((size_t)nets * h1 * kp, 0), W2((size_t)nets * h2 * h1), W3((size_t)nets * h3 * h2);
+  // W1 gets 64 zero rows after the last net: the fused layer-1/2 kernel's W1 box of the last
+  // chunk pair can reach past the last net when h1 / 64 is odd
+  std::vector<uint16_t> W1((size_t)nets * h1 * kp + 64 * (size_t)kp, 0), W2((size_t)nets * h2 * h1),
+      W3((size_t)nets * h3 * h2);
   std::vector<float> F1, F2, F3;
   std::vector<float> L1v, L2v, L3v;  // RC_TF32X3: tf32 residuals W - W_hi
   if (tf32) {
@@ -538,8 +544,8 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   CUtensorMap m12[5];
   if (fused && ((rc = make_map(&m12[0], z, KZ, cap, 1, BM, KZ, EB)) ||
                 (rc = make_map_w1_groups(&m12[1], n->d_W1, KZ, n->h1, nets)) ||
-                (rc = make_map(&m12[2], n->d_W2, n->h1, n->h2, nets, 128, 32, EB)) ||
-                (rc = make_map(&m12[3], n->d_W2, n->h1, n->h2, nets, 72, 32, EB)) ||
+                (rc = make_map(&m12[2], n->d_W2, n->h1, n->h2, nets, 128, 64, EB)) ||
+                (rc = make_map(&m12[3], n->d_W2, n->h1, n->h2, nets, 72, 64, EB)) ||
                 (rc = make_map(&m12[4], h2, n->h2, cap, nets, 32, 16, EB))))
     return rc;
   if (!x3) {  // the lo slots are never read: any valid map

@@ -207,6 +207,19 @@ __device__ __forceinline__ void mma_commit_pair_mask(uint64_t *bar, uint16_t mas
       "h"(mask)
       : "memory");
 }
+// cluster-scope release arrive on a (possibly remote) mbarrier: orders this thread's prior
+// shared::cluster stores before the arrival for the CTA that waits on it
+__device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t cluster_addr, uint4 v) {
+  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(cluster_addr), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_cluster() {
+  asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+}
 // bulk copy of this CTA's shared memory into another CTA of the cluster; completion
 // (bytes) counted on an mbarrier in the destination CTA (cluster addresses from map_cta)
 __device__ __forceinline__ void bulk_s2s_cluster(uint32_t dst_cluster, const void *src, uint32_t bytes,

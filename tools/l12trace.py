@@ -31,5 +31,5 @@ for g in list(range(0, 6)) + list(range(20, 32)) + list(range(44, 56)):
     p = [b[r, 1, g] for r in range(4)]
     fw = [b[r, 2, g] for r in range(4)]
     print(f"chunk {g:2d} MMA A: wait {m0[0]:8d} +{m0[1]-m0[0]:6d} iss {m0[2]-m0[1]:5d} | B: wait {m2[0]:8d} +{m2[1]-m2[0]:6d} | "
-          + " ".join(f"P{r}: a1 {p[r][1]-p[r][0]:6d} ae {p[r][2]-p[r][1]:6d} st {p[r][3]-p[r][2]:5d} @{p[r][3]:8d}" for r in (1, 3))
+          + " ".join(f"P{r}: a1 {p[r][1]-p[r][0]:6d} ae {p[r][2]-p[r][1]:6d} st {p[r][3]-p[r][2]:5d} @{p[r][3]:8d}" for r in (0, 2))
           + " | " + " ".join(f"F{r}: own {fw[r][1]-fw[r][0]:6d} peer {fw[r][2]-fw[r][1]:6d}" for r in (0, 2)))

@@ -7,8 +7,9 @@
 
 template <int ROWB>
 __device__ __forceinline__ uint64_t dsw(const void *p) {
+  constexpr uint64_t layout = ROWB == 128 ? 2 : ROWB == 64 ? 4 : 6;
   uint64_t d = (uint64_t)((rcx::smem_u32(p) & 0x3FFFF) >> 4);
-  d |= (uint64_t)((8 * ROWB) >> 4) << 32; d |= (uint64_t)1 << 46; d |= (uint64_t)2 << 61; return d;
+  d |= (uint64_t)((8 * ROWB) >> 4) << 32; d |= (uint64_t)1 << 46; d |= layout << 61; return d;
 }
 
 // mode 0: cta_group::1, M=128, N=n1 (+ n2 second MMA); mode 1: cta_group::2 M=256
@@ -30,6 +31,7 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int iters, int n1, int n2, un
     const uint32_t M = PAIR ? 256 : 128;
     uint32_t id1 = rcx::make_idesc(1, M, n1), id2 = rcx::make_idesc(1, M, n2 > 0 ? n2 : 16);
     uint64_t da = dsw<128>(base), db = dsw<128>(base + 32768);
+    if (l1 == 64) { da = dsw<64>(base); db = dsw<64>(base + 32768); }  // 64-byte swizzle operands
     unsigned long long t0 = clock64();
     const uint32_t idl1 = rcx::make_idesc(1, M, 64);
     uint64_t dz = dsw<128>(base + 65536), dw1 = dsw<128>(base + 98304);
@@ -76,7 +78,7 @@ int main() {
   cudaFuncSetAttribute(mma_loop<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(mma_loop<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  struct C { int pair, n1, n2, l1; } cs[] = {{1, 256, 144, 0}, {1, 256, 0, 0}, {1, 144, 0, 0}, {1, 128, 128, 0}, {1, 128, 0, 0}, {1, 256, 144, 11}, {1, 256, 144, 21}, {1, 256, 0, 11}};
+  struct C { int pair, n1, n2, l1; } cs[] = {{1, 256, 144, 0}, {1, 256, 144, 64}, {1, 256, 144, 11}, {1, 256, 144, 21}};
   for (auto c : cs) {
     int iters = 2000;
     cudaLaunchConfig_t cfg = {};
