@@ -28,7 +28,7 @@ struct L2Args {
 };
 // fused layers 1+2 (mlp_l12_sm100.cu, bf16, h2 = 800): clusters of two CTA pairs share h1 chunks
 // maps: {z (KZ x 128 rows), W1 (KZ x 16 rows), W2 piece 1 (32 x 128 rows), W2 piece 2 (32 x 72 rows),
-//        h2 store (16 x 32)}
+//        h2 store (16 x 32), b2 as K = 16 operand piece 1 (16 x 128 rows), piece 2 (16 x 72 rows)}
 struct L12Args {
   int m_tiles, nets, chunks, N, stages, lead_in;
   const float *bias;  // b2 [nets][N]

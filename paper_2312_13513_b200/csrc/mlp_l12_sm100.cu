@@ -55,7 +55,8 @@ using rcm::cvt_bf16x2;
 using rcm::gelu_bf16x2;
 
 #ifdef L12TRACE  // timing experiment: clock64 stamps of cluster 0, first 64 chunks (tools/l12trace.py)
-__device__ long long g_l12trace[4][4][64][4];  // [cta rank][role: 0 MMA, 1 producer warp 0, 2 forwarder][chunk][event]
+// [cta rank][role: 0 MMA, 1 producer warp 0, 2 forwarder, 3 drain (by tile), 4 layer-1 issuer, 5 TMA (by tile)][chunk][event]
+__device__ long long g_l12trace[4][6][64][4];
 #define TR(role, ch, ev)                                                                              \
   do {                                                                                                \
     if (blockIdx.x < 4 && (ch) < 64 && lane == 0) g_l12trace[blockIdx.x & 3][role][ch][ev] = clock64(); \
@@ -72,11 +73,13 @@ template <int KZ, int R>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
     l12_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapW1,
                const __grid_constant__ CUtensorMap mapW2a, const __grid_constant__ CUtensorMap mapW2b,
-               const __grid_constant__ CUtensorMap mapOut, L12Args a) {
+               const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ CUtensorMap mapBa,
+               const __grid_constant__ CUtensorMap mapBb, L12Args a) {
   constexpr uint32_t Z_BYTES = 128 * KZ * 2, W1_CH = 32 * KZ * 2;  // W1: 32 rows per CTA and chunk
   constexpr uint32_t STAGE_BYTES = W2T;                             // TMA bytes per CTA
+  constexpr uint32_t BK_BYTES = (NP / 2) * 32, BK_AL = 7168;        // b2 as a K = 16 operand: 200 rows x 32 B
   constexpr uint32_t STAGE = (W2T + 1023u) & ~1023u;                // layout size
-  constexpr int MAXCH = (NP / 16 + 3) / 4;
+  static_assert(NP == 400 && P1 == 256, "drain split below assumes 25 column groups, 16 in piece 1");
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = rcx::smem_u32(smem_raw);
@@ -86,15 +89,16 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
   uint8_t *sA = sW + S * STAGE;              // R x SLOT
   uint8_t *sZ = sA + R * SLOT;               // 2 x Z_BYTES
   uint8_t *sW1 = sZ + 2 * ((Z_BYTES + 1023u) & ~1023u);  // this CTA's W1 rows of its pair's chunks of the net
-  uint8_t *sST = sW1 + ((((a.chunks + 1) / 2) * W1_CH + 1023u) & ~1023u);  // NEPI x 2 x 1 KB h2 store staging
-  float *sB2 = reinterpret_cast<float *>(sST + NEPI * 2 * 1024);
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sB2 + 2 * NP);
+  uint8_t *sST = sW1 + ((((a.chunks + 1) / 2) * W1_CH + 1023u) & ~1023u);  // 8 drain warps x 2 x 1 KB h2 staging
+  uint8_t *sBK = sST + (NEPI - NPROD) * 2 * 1024;  // 2 x b2 operand tile (with the z tile of the same buffer)
+  uint8_t *sOnes = sBK + 2 * BK_AL;                // 128 rows x 16 bf16 ones: the A side of the b2 MMA
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sOnes + 4096);
   // ready[i]: leader = both operands of chunk i in both CTAs (its slot: own copier or incoming copy;
   //   the odd forwarder; W2 TMA of both CTAs); odd CTA = its slot.  own[i]: the local producers wrote
   //   slot i (chunks of this pair).  freed[i]: both pairs consumed chunk i's slot and stage.
   uint64_t *ready = bar, *freed = ready + R, *zfull = freed + R, *zempty = zfull + 2, *a1full = zempty + 2,
            *a1empty = a1full + NA1, *own = a1empty + NA1, *c2full = own + R, *c2empty = c2full + 1,
-           *bfull = c2empty + 1, *bempty = bfull + 2, *w1full = bempty + 2, *w1empty = w1full + 1;
+           *c2emptyB = c2empty + 1, *w1full = c2emptyB + 1, *w1empty = w1full + 1;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(w1empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -108,6 +112,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
     rcx::prefetch_tmap(&mapW2a);
     rcx::prefetch_tmap(&mapW2b);
     rcx::prefetch_tmap(&mapOut);
+    rcx::prefetch_tmap(&mapBa);
+    rcx::prefetch_tmap(&mapBb);
     for (int r = 0; r < R; ++r) {
       rcx::mbar_init(&ready[r], prank == 0 ? 4 : 1);
       rcx::mbar_init(&freed[r], 2);
@@ -118,17 +124,18 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
     for (int z = 0; z < 2; ++z) {
       rcx::mbar_init(&zfull[z], 2);
       rcx::mbar_init(&zempty[z], 1);
-      rcx::mbar_init(&bfull[z], 1);
-      rcx::mbar_init(&bempty[z], NEPI);
     }
     for (int z = 0; z < NA1; ++z) {
       rcx::mbar_init(&a1full[z], 1);
       rcx::mbar_init(&a1empty[z], 2 * NPROD);
     }
     rcx::mbar_init(c2full, 1);
-    rcx::mbar_init(c2empty, 2 * NEPI);
+    rcx::mbar_init(c2empty, 2 * (NEPI - NPROD));  // piece 1: the drain warps of both CTAs
+    rcx::mbar_init(c2emptyB, 2 * (NEPI - NPROD));  // piece 2
     rcx::fence_mbar_init();
   }
+  for (int i = threadIdx.x; i < 1024; i += L12_THREADS) reinterpret_cast<uint32_t *>(sOnes)[i] = 0x3F803F80u;
+  rcm::fence_async_smem();  // the ones tile is read by the tensor core (async proxy)
   if (warp == W_MMA) rcx::tmem_alloc_pair(tmem_slot, 512);
   rcx::tc_fence_before();
   rcx::cluster_sync();
@@ -139,15 +146,32 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
   const int total = a.nets * pairs;
   const int cl = blockIdx.x >> 2, ncl = gridDim.x >> 2;
 
+  // Registers are rebalanced by warpgroup: the single-thread roles (warps 16..19) give registers
+  // to the 16 epilogue warps (96 per thread at launch -> 48 / 104).
+  if (warp >= NEPI) {
+  rcx::setmaxnreg_dec<48>();
   if (warp == W_TMA) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer (all CTAs)
       const uint32_t ready0 = rcx::map_cta(ready, lead), zfull0 = rcx::map_cta(zfull, lead);
       const uint32_t w1full0 = rcx::map_cta(w1full, lead);
       uint32_t g = 0, nw = 0;
       int it = 0, cur_net = -1;
+      // z tile and b2 operand tile of the it-th tile: issued half-way through the previous tile, so
+      // the layer-1 MMAs of a tile's first chunks never wait for them at the tile transition
+      auto load_zb = [&](int tile, int it) {
+        const int zb = it & 1, net = tile / pairs;
+        TR(5, it, 0);
+        rcx::mbar_wait_sleep(&zempty[zb], ((it >> 1) & 1) ^ 1);
+        rcx::mbar_arrive_expect_tx_cluster(zfull0 + zb * 8, Z_BYTES + BK_BYTES);
+        rcx::tma_load_3d_pair(sZ + zb * ((Z_BYTES + 1023u) & ~1023u), &mapZ, &zfull[zb], 0,
+                              (tile % pairs) * 256 + prank * 128, 0);
+        rcx::tma_load_3d_pair(sBK + zb * BK_AL, &mapBa, &zfull[zb], 0, pr * NP + prank * H1, net);
+        rcx::tma_load_3d_pair(sBK + zb * BK_AL + H1 * 32, &mapBb, &zfull[zb], 0, pr * NP + P1 + prank * H2, net);
+        TR(5, it, 1);
+      };
+      if (cl < total) load_zb(cl, 0);
       for (int tile = cl; tile < total; tile += ncl, ++it) {
-        const int mp = tile % pairs, net = tile / pairs;
-        const int zb = it & 1;
+        const int net = tile / pairs;
         if (net != cur_net) {  // this CTA's W1 rows of all chunks of the new net (one 5D box)
           rcx::mbar_wait_sleep(w1empty, (nw & 1) ^ 1);
           rcx::mbar_arrive_expect_tx_cluster(w1full0, ((C + 1) / 2) * W1_CH);
@@ -155,12 +179,6 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           cur_net = net;
           ++nw;
         }
-        rcx::mbar_wait_sleep(&zempty[zb], ((it >> 1) & 1) ^ 1);
-        rcx::mbar_arrive_expect_tx_cluster(zfull0 + zb * 8, Z_BYTES);
-        rcx::tma_load_3d_pair(sZ + zb * ((Z_BYTES + 1023u) & ~1023u), &mapZ, &zfull[zb], 0, mp * 256 + prank * 128, 0);
-        rcx::mbar_wait_sleep(&bempty[zb], ((it >> 1) & 1) ^ 1);
-        rcx::mbar_arrive_expect_tx(&bfull[zb], NP * 4);
-        rcx::bulk_g2s(sB2 + zb * NP, a.bias + (size_t)net * a.N + pr * NP, NP * 4, &bfull[zb]);
         for (int c = 0; c < C; ++c, ++g) {
           const int s = (int)(g % S);
           rcx::mbar_wait_sleep(&freed[s], ((g / S) & 1) ^ 1);
@@ -168,6 +186,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           uint8_t *st = sW + s * STAGE;
           rcx::tma_load_3d_pair(st, &mapW2a, &ready[s], c * 64, pr * NP + prank * H1, net);
           rcx::tma_load_3d_pair(st + H1 * 128, &mapW2b, &ready[s], c * 64, pr * NP + P1 + prank * H2, net);
+          if (c == C / 2 && tile + ncl < total) load_zb(tile + ncl, it + 1);
         }
       }
     }
@@ -186,11 +205,15 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           cur_net = net;
           ++nw;
         }
+        TR(4, it * C, 0);
         rcx::mbar_wait_sleep(&zfull[zb], (it >> 1) & 1);
+        TR(4, it * C, 1);
         const uint64_t dz = rcm::desc_sw<KZ * 2>(sZ + zb * ((Z_BYTES + 1023u) & ~1023u));
         for (int c = pr; c < C; c += 2, ++g) {  // g counts this pair's chunks
           const uint32_t b = g % NA1;
+          TR(4, it * C + c, 2);
           rcx::mbar_wait(&a1empty[b], ((g / NA1) & 1) ^ 1);
+          TR(4, it * C + c, 3);
           rcx::tc_fence_after();
           const uint64_t dw = rcm::desc_sw<KZ * 2>(sW1 + (c >> 1) * W1_CH);
 #pragma unroll
@@ -206,8 +229,6 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
       uint32_t G = 0;
       int it = 0;
       for (int tile = cl; tile < total; tile += ncl, ++it, G += C) {
-        rcx::mbar_wait_sleep(c2empty, (it & 1) ^ 1);  // previous tile's acc2 copied out
-        rcx::tc_fence_after();
         for (int c = 0; c < C; ++c) {
           const uint32_t g = G + c;
           const int s = (int)(g % R), slot = s;
@@ -217,10 +238,34 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           rcx::tc_fence_after();
           uint8_t *A = sA + slot * SLOT;
           uint8_t *B = sW + s * STAGE;
+          if (c == 0) {
+            // first chunk of a tile: the accumulator starts at b2 (one K = 16 MMA of a ones tile
+            // against the b2 operand tile), and the drain releases it in two pieces, so the
+            // piece-1 MMAs (columns [0, 256)) run while piece 2 is still being copied out
+            const int zb = it & 1;
+            rcx::mbar_wait(&zfull[zb], (it >> 1) & 1);
+            const uint64_t d1 = rcm::desc_sw<32>(sOnes), dbk = rcm::desc_sw<32>(sBK + zb * BK_AL);
+            rcx::mbar_wait_sleep(c2empty, (it & 1) ^ 1);
+            rcx::tc_fence_after();
+            rcx::mma_bf16_pair(tmem, d1, dbk, idp1, 0);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              rcx::mma_bf16_pair(tmem, rcm::desc_sw<128>(A) + 2 * k, rcm::desc_sw<128>(B) + 2 * k, idp1, 1);
+            rcx::mbar_wait(c2emptyB, (it & 1) ^ 1);
+            rcx::tc_fence_after();
+            rcx::mma_bf16_pair(tmem + P1, d1, dbk + ((H1 * 32) >> 4), idp2, 0);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              rcx::mma_bf16_pair(tmem + P1, rcm::desc_sw<128>(A) + 2 * k, rcm::desc_sw<128>(B) + ((H1 * 128) >> 4) + 2 * k,
+                                 idp2, 1);
+            rcx::mma_commit_pair_mask(&freed[s], (uint16_t)0xF);
+            TR(0, g, 2);
+            continue;
+          }
 #pragma unroll
           for (int k = 0; k < 4; ++k) {  // K16 steps: 32-byte atoms along the 128-byte rows
             const uint64_t da = rcm::desc_sw<128>(A) + 2 * k, db = rcm::desc_sw<128>(B) + 2 * k;
-            const uint32_t acc = (c | k) != 0;
+            const uint32_t acc = 1;
             rcx::mma_bf16_pair(tmem, da, db, idp1, acc);
             rcx::mma_bf16_pair(tmem + P1, da, db + ((H1 * 128) >> 4), idp2, acc);
           }
@@ -261,22 +306,19 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           rcx::mbar_arrive_cluster(ready_lead + slot * 8);
         }
     }
-  } else {  // ------------------------------------------------------ epilogue warps 0..15
-    const int q = warp & 3, sub = warp >> 2;
-    const bool producer = warp < NPROD;
-    const int ph = (warp >> 2) & 1;  // producers: 16-column half of this pair's 32-column half-chunk
+  }
+  } else if (warp < NPROD) {  // ---------------------------------------- h1 producers, warps 0..7
+    rcx::setmaxnreg_dec<72>();
+    const int q = warp & 3, ph = (warp >> 2) & 1;  // ph: 32-column half of the 64-column chunk
     const uint32_t tq = (uint32_t)(q * 32) << 16;
-    constexpr int NCH = NP / 16;
-    const int ch_lo = (NCH * sub) / 4, ch_hi = (NCH * (sub + 1)) / 4, nch = ch_hi - ch_lo;
-    const uint32_t c2empty0 = rcx::map_cta(c2empty, lead), a1empty0 = rcx::map_cta(a1empty, lead);
-    uint8_t *stg_base = sST + warp * 2 * 1024;
+    const uint32_t a1empty0 = rcx::map_cta(a1empty, lead);
     const int row = q * 32 + lane;
-    uint32_t nst = 0;
-    // h1 production of global chunk g (this CTA's tiles in order, C chunks each)
-    uint32_t lg = 0;  // this pair's chunks produced so far (layer-1 accumulator phase)
-    auto produce = [&](uint32_t g) {  // global chunk g: only this pair's chunks (g % C parity == pr)
-      if ((int)((g % C) & 1) != pr) return;
-      const uint32_t b = lg % NA1, my = lg;  // my: index among this pair's chunks (own[] ring)
+    const int ntiles = cl < total ? (total - 1 - cl) / ncl + 1 : 0;
+    const uint32_t nchunks = (uint32_t)ntiles * C;
+    uint32_t lg = 0;  // this pair's chunks produced so far (layer-1 accumulator phase, own[] ring)
+    for (uint32_t g = 0; g < nchunks; ++g) {  // this CTA's tiles in order, C chunks each
+      if ((int)((g % C) & 1) != pr) continue;  // the other pair's chunk
+      const uint32_t b = lg % NA1, my = lg;
       if (warp == 0) TR(1, g, 0);
       rcx::mbar_wait(&a1full[b], (lg / NA1) & 1);
       if (warp == 0) TR(1, g, 1);
@@ -310,36 +352,71 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
       __syncwarp();
       if (lane == 0) rcx::mbar_arrive(&own[my % R]);
       if (warp == 0) TR(1, g, 3);
-    };
-    // drain acc2 of this CTA's it-th tile (128 rows x 400 columns): two-phase as in the layer-2 kernel
-    auto drain = [&](int it, int tile) {
+    }
+  } else {  // ------------------------------------------------------ acc2 drain, warps 8..15
+    rcx::setmaxnreg_inc<144>();
+    // Two warps per TMEM lane quadrant; warp half hh drains column groups (16 columns) 8hh..8hh+7
+    // of piece 1 (the N = 256 MMA, columns [0, 256)) and then 16..20 (hh = 0) or 21..24 (hh = 1)
+    // of piece 2.  Each piece is released as soon as it is copied out (c2empty / c2emptyB), so the
+    // MMA issuer restarts piece 1 of the next tile while piece 2 is still being copied.  The
+    // producers never drain: h1 production runs straight through the tile transition.
+    const int w = warp - NPROD, q = w & 3, hh = w >> 2;
+    const uint32_t tq = (uint32_t)(q * 32) << 16;
+    const int nch = 13 - hh;
+    auto grp = [&](int c) { return c < 8 ? 8 * hh + c : 16 + 5 * hh + (c - 8); };
+    const uint32_t c2empty0 = rcx::map_cta(c2empty, lead), c2emptyB0 = rcx::map_cta(c2emptyB, lead);
+    uint8_t *stg_base = sST + w * 2 * 1024;  // two 1 KB TMA-store staging buffers per warp
+    uint32_t nst = 0;
+    const int ntiles = cl < total ? (total - 1 - cl) / ncl + 1 : 0;
+    for (int it = 0; it < ntiles; ++it) {
+      const int tile = cl + it * ncl;
       const int mp = tile % pairs, net = tile / pairs;
       rcx::mbar_wait_sleep(c2full, it & 1);
-      rcx::mbar_wait(&bfull[it & 1], (it >> 1) & 1);
+      if (warp == 8) TR(3, it, 0);
       rcx::tc_fence_after();
-      const float *b2 = sB2 + (it & 1) * NP;
       const int grow = mp * 256 + prank * 128 + q * 32;
-      uint32_t pk[MAXCH][8];
+      uint32_t pk[13][8];
+      // accumulator columns (n groups from v, b2 already included) -> bf16 pairs
+      auto cvt = [&](const uint32_t *v, int c, int n) {
 #pragma unroll
-      for (int c = 0; c < MAXCH; ++c) {
-        if (c < nch) {
-          uint32_t v[16];
-          rcx::tmem_ld16(tmem + tq + (ch_lo + c) * 16, v);
-          rcx::tmem_ld_wait();
-          const float4 *bb = reinterpret_cast<const float4 *>(b2 + (ch_lo + c) * 16);
+        for (int h = 0; h < n; ++h)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 bv = bb[j];
-            pk[c][2 * j] = cvt_bf16x2(__uint_as_float(v[4 * j]) + bv.x, __uint_as_float(v[4 * j + 1]) + bv.y);
-            pk[c][2 * j + 1] = cvt_bf16x2(__uint_as_float(v[4 * j + 2]) + bv.z, __uint_as_float(v[4 * j + 3]) + bv.w);
-          }
-        }
+          for (int j = 0; j < 8; ++j)
+            pk[c + h][j] = cvt_bf16x2(__uint_as_float(v[16 * h + 2 * j]), __uint_as_float(v[16 * h + 2 * j + 1]));
+      };
+      // piece 1: two rounds of two 32-column loads in flight
+#pragma unroll
+      for (int c = 0; c < 8; c += 4) {
+        uint32_t v[64];
+        rcm::tmem_ld32(tmem + tq + grp(c) * 16, *reinterpret_cast<uint32_t(*)[32]>(v));
+        rcm::tmem_ld32(tmem + tq + grp(c + 2) * 16, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        rcx::tmem_ld_wait();
+        cvt(v, c, 4);
       }
       rcx::tc_fence_before();
       __syncwarp();
       if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
+      // piece 2: groups 8..11 (32-column loads), then group 12 (hh = 0 only)
 #pragma unroll
-      for (int c = 0; c < MAXCH; ++c) {
+      for (int c = 8; c < 12; c += 2) {
+        uint32_t v[32];
+        rcm::tmem_ld32(tmem + tq + grp(c) * 16, v);
+        rcx::tmem_ld_wait();
+        cvt(v, c, 2);
+      }
+      if (hh == 0) {
+        uint32_t v[16];
+        rcx::tmem_ld16(tmem + tq + grp(12) * 16, v);
+        rcx::tmem_ld_wait();
+        cvt(v, 12, 1);
+      }
+      rcx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) rcx::mbar_arrive_cluster(c2emptyB0);
+      if (warp == 8) TR(3, it, 1);
+      // phase 2: GELU and TMA stores (32 rows x 16 columns per store) under the next tile's MMAs
+#pragma unroll
+      for (int c = 0; c < 13; ++c) {
         if (c < nch) {
           uint32_t gg[8];
 #pragma unroll
@@ -353,33 +430,13 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           rcm::fence_async_smem();
           __syncwarp();
           if (lane == 0) {
-            rcm::tma_store_3d(&mapOut, stg, pr * NP + (ch_lo + c) * 16, grow, net);
+            rcm::tma_store_3d(&mapOut, stg, pr * NP + grp(c) * 16, grow, net);
             rcm::bulk_commit();
           }
           ++nst;
         }
       }
-      __syncwarp();
-      if (lane == 0) rcx::mbar_arrive(&bempty[it & 1]);
-    };
-    const int ntiles = cl < total ? (total - 1 - cl) / ncl + 1 : 0;
-    if (producer) {
-      // Produce the first min(R, C) chunks of tile t+1 before draining tile t: they only need slots
-      // the end of tile t's mainloop frees, so the next tile's MMAs start right after the drain's
-      // copy-out instead of waiting for production to restart.
-      const int lead_in = a.lead_in < C ? a.lead_in : C;
-      const uint32_t nchunks = (uint32_t)ntiles * C;
-      int dt = 0;  // next tile to drain
-      for (uint32_t g = 0; g < nchunks; ++g) {
-        produce(g);
-        if (g + 1 == (uint32_t)(dt + 1) * C + lead_in) {
-          drain(dt, cl + dt * ncl);
-          ++dt;
-        }
-      }
-      for (; dt < ntiles; ++dt) drain(dt, cl + dt * ncl);
-    } else {
-      for (int it = 0; it < ntiles; ++it) drain(it, cl + it * ncl);
+      if (warp == 8) TR(3, it, 2);
     }
     if (lane == 0) rcm::bulk_wait_all();
     __syncwarp();
@@ -398,7 +455,7 @@ int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
   constexpr size_t Z_AL = ((size_t)128 * KZ * 2 + 1023) & ~(size_t)1023;
   constexpr size_t STAGE = ((size_t)W2T + 1023) & ~(size_t)1023;
   const size_t w1 = ((size_t)((a.chunks + 1) / 2) * 32 * KZ * 2 + 1023) & ~(size_t)1023;
-  const size_t smem = 1024 + R * (SLOT + STAGE) + 2 * Z_AL + w1 + NEPI * 2 * 1024 + 2 * NP * 4 + 1024;
+  const size_t smem = 1024 + R * (SLOT + STAGE) + 2 * Z_AL + w1 + (NEPI - NPROD) * 2 * 1024 + 2 * 7168 + 4096 + 1024;
   if (smem > 232448) return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel: shared memory");
   a.stages = R;
   static int li = -1;
@@ -434,7 +491,7 @@ int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
   const int total = a.nets * (a.m_tiles / 2);
   int clusters = resident;
   if (clusters > total) clusters = total;
-  l12_kernel<KZ, R><<<4 * clusters, L12_THREADS, smem, s>>>(M[0], M[1], M[2], M[3], M[4], a);
+  l12_kernel<KZ, R><<<4 * clusters, L12_THREADS, smem, s>>>(M[0], M[1], M[2], M[3], M[4], M[5], M[6], a);
   RC_LAUNCH_CHECK();
   return RC_OK;
 }

@@ -424,6 +424,9 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
     hi = f2tf32((float)w);
     if (lo) *lo = f2tf32((float)(w - (double)hi));
   };
+  // b2 as an extra K = 16 operand of the layer-2 MMAs (the A side is a tile of ones):
+  // column 0 = bf16(b), column 1 = bf16(b - bf16(b)), so the accumulator starts at b to ~2^-17
+  std::vector<uint16_t> B2k(tf32 ? 0 : (size_t)nets * h2 * 16, 0);
   std::vector<float> b1((size_t)nets * h1), b2((size_t)nets * h2), b3((size_t)nets * h3), w4((size_t)nets * h3), b4(nets);
   for (int i = 0; i < nets; ++i) {
     const double *p = d->params + i * P;
@@ -456,7 +459,17 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
       else W2[(size_t)i * h2 * h1 + e] = f2bf((float)p[e]);
     }
     p += (size_t)h2 * h1;
-    for (int r = 0; r < h2; ++r) b2[(size_t)i * h2 + r] = (float)p[r];
+    for (int r = 0; r < h2; ++r) {
+      b2[(size_t)i * h2 + r] = (float)p[r];
+      if (!tf32) {
+        const uint16_t hi = f2bf((float)p[r]);
+        uint32_t hb = (uint32_t)hi << 16;
+        float hf;
+        std::memcpy(&hf, &hb, 4);
+        B2k[((size_t)i * h2 + r) * 16] = hi;
+        B2k[((size_t)i * h2 + r) * 16 + 1] = f2bf((float)(p[r] - (double)hf));
+      }
+    }
     p += h2;
     for (size_t e = 0; e < (size_t)h3 * h2; ++e) {
       if (tf32) split(p[e], F3[(size_t)i * h3 * h2 + e], x3 ? &L3v[(size_t)i * h3 * h2 + e] : nullptr);
@@ -487,6 +500,7 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
             up((void **)&n->d_xmean, xm.data(), xm.size() * 4) && up((void **)&n->d_xinvstd, xi.data(), xi.size() * 4) &&
             up((void **)&n->d_ymean, d->y_mean, nets * 8) && up((void **)&n->d_ystd, d->y_std, nets * 8) &&
             up((void **)&n->d_species, d->species_of_net, nets * 4);
+  if (ok && !tf32) ok = up(&n->d_b2k, B2k.data(), B2k.size() * 2);
   if (ok && x3)
     ok = up(&n->d_W1lo, L1v.data(), L1v.size() * 4) && up(&n->d_W2lo, L2v.data(), L2v.size() * 4) &&
          up(&n->d_W3lo, L3v.data(), L3v.size() * 4);
@@ -541,12 +555,14 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   // fused layers 1+2 (bf16, paper widths); RC_NO_FUSE=1 forces the layer-wise path (tests, comparisons)
   const char *nf = getenv("RC_NO_FUSE");
   const bool fused = prec == 0 && l12_supported(n->h1, n->h2, KZ) && !(nf && nf[0] == '1');
-  CUtensorMap m12[5];
+  CUtensorMap m12[7];
   if (fused && ((rc = make_map(&m12[0], z, KZ, cap, 1, BM, KZ, EB)) ||
                 (rc = make_map_w1_groups(&m12[1], n->d_W1, KZ, n->h1, nets)) ||
                 (rc = make_map(&m12[2], n->d_W2, n->h1, n->h2, nets, 128, 64, EB)) ||
                 (rc = make_map(&m12[3], n->d_W2, n->h1, n->h2, nets, 72, 64, EB)) ||
-                (rc = make_map(&m12[4], h2, n->h2, cap, nets, 32, 16, EB))))
+                (rc = make_map(&m12[4], h2, n->h2, cap, nets, 32, 16, EB)) ||
+                (rc = make_map(&m12[5], n->d_b2k, 16, n->h2, nets, 128, 16, EB)) ||
+                (rc = make_map(&m12[6], n->d_b2k, 16, n->h2, nets, 72, 16, EB))))
     return rc;
   if (!x3) {  // the lo slots are never read: any valid map
     for (int k = 0; k < 3; ++k) m1[3 + k] = m1[k];

@@ -38,6 +38,17 @@ __global__ void k(int iters, uint32_t *out) {
       }
       if (MODE == 7) v[i] = tanh2h(v[i]);
       if (MODE == 8) v[i] = ex2h(v[i]);
+      if (MODE == 9) {  // RNE to bf16 on the FMA pipe (Veltkamp split, s = 2^16 + 1) + PRMT pack
+        const float a = f[i], b = f[(i + 1) & 7];
+        const float ta = a * 65537.0f, tb = b * 65537.0f;
+        const float ha = ta - (ta - a), hb = tb - (tb - b);
+        uint32_t p; asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(p) : "r"(__float_as_uint(ha)), "r"(__float_as_uint(hb)));
+        f[i] = __uint_as_float(p) + f[i];
+      }
+      if (MODE == 10) {  // one cvt.rn.bf16x2 + one tanh.approx.f32 per pair: do they share a pipe?
+        uint32_t p; asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(f[i]), "f"(f[(i + 1) & 7]));
+        f[i] = __uint_as_float(p) + tanh1(f[i]);
+      }
       if (MODE == 6) { uint32_t p; asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(f[i]), "f"(f[(i + 1) & 7])); f[i] = __uint_as_float(p) + f[i]; }
     }
   }
@@ -49,16 +60,16 @@ __global__ void k(int iters, uint32_t *out) {
 int main() {
   uint32_t *d; cudaMalloc(&d, 4);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const char *names[] = {"tanh.approx.bf16x2 (elements)", "tanh.approx.f32", "fma.rn.bf16x2 (elements)", "gelu bf16x2 (elements)", "gelu f32", "cvt+gelu bf16x2 (elements)", "cvt.rn.bf16x2.f32 (elements)", "tanh.approx.f16x2 (elements)", "ex2.approx.f16x2 (elements)"};
+  const char *names[] = {"tanh.approx.bf16x2 (elements)", "tanh.approx.f32", "fma.rn.bf16x2 (elements)", "gelu bf16x2 (elements)", "gelu f32", "cvt+gelu bf16x2 (elements)", "cvt.rn.bf16x2.f32 (elements)", "tanh.approx.f16x2 (elements)", "ex2.approx.f16x2 (elements)", "veltkamp rne + prmt (elements)", "cvt pair + tanh.f32 (pairs)"};
   for (int warps : {16}) {
-    for (int m = 0; m < 9; ++m) {
+    for (int m = 0; m < 11; ++m) {
       int iters = 4096; dim3 g(148), b(32 * warps);
       auto launch = [&]() { switch (m) { case 0: k<0><<<g, b>>>(iters, d); break; case 1: k<1><<<g, b>>>(iters, d); break;
-        case 2: k<2><<<g, b>>>(iters, d); break; case 3: k<3><<<g, b>>>(iters, d); break; case 4: k<4><<<g, b>>>(iters, d); break; case 5: k<5><<<g, b>>>(iters, d); break; case 6: k<6><<<g, b>>>(iters, d); break; case 7: k<7><<<g, b>>>(iters, d); break; case 8: k<8><<<g, b>>>(iters, d); break; } };
+        case 2: k<2><<<g, b>>>(iters, d); break; case 3: k<3><<<g, b>>>(iters, d); break; case 4: k<4><<<g, b>>>(iters, d); break; case 5: k<5><<<g, b>>>(iters, d); break; case 6: k<6><<<g, b>>>(iters, d); break; case 7: k<7><<<g, b>>>(iters, d); break; case 8: k<8><<<g, b>>>(iters, d); break; case 9: k<9><<<g, b>>>(iters, d); break; case 10: k<10><<<g, b>>>(iters, d); break; } };
       launch(); cudaDeviceSynchronize();
       cudaEventRecord(e0); launch(); cudaEventRecord(e1); cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
-      double elems = 8.0 * iters * g.x * b.x * ((m == 0 || m == 2 || m == 3 || m == 5 || m == 6 || m == 7 || m == 8) ? 2 : 1);
+      double elems = 8.0 * iters * g.x * b.x * ((m == 0 || m == 2 || m == 3 || m == 5 || m == 6 || m == 7 || m == 8 || m == 9) ? 2 : 1);
       printf("warps/SM=%2d %-32s %8.1f Gelem/s = %6.1f elem/clk/SM @1.9GHz\n", warps, names[m], elems / ms / 1e6, elems / ms / 1e6 / 148 / 1.9);
     }
   }
