@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO = os.path.join(HERE, "librc_b200.so")
+SO = os.environ.get("RC_LIB") or os.path.join(HERE, "librc_b200.so")  # RC_LIB: A/B experiments (tools/ab.sh)
 
 RC_OK, RC_EINVAL, RC_ENOMEM, RC_ECUDA, RC_EALIGN, RC_EUNSUPPORTED, RC_EDTMISMATCH = 0, -1, -2, -3, -4, -5, -6
 RC_MODE_H, RC_MODE_T = 0, 1

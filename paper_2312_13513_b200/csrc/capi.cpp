@@ -274,7 +274,7 @@ extern "C" int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *d, rc_mlp **ou
 extern "C" void rc_mlp_destroy(rc_mlp *n) {
   if (!n) return;
   void *ptrs[] = {n->d_W1, n->d_W2, n->d_W3, n->d_W1lo, n->d_W2lo, n->d_W3lo, n->d_b1, n->d_b2, n->d_b3, n->d_w4, n->d_b4,
-                  n->d_b2k, n->d_xmean, n->d_xinvstd, n->d_ymean, n->d_ystd, n->d_species};
+                  n->d_b2k, n->d_b3k, n->d_xmean, n->d_xinvstd, n->d_ymean, n->d_ystd, n->d_species};
   for (void *p : ptrs) cudaFree(p);
   delete n;
 }

@@ -36,5 +36,6 @@ struct L12Args {
 bool l12_supported(int h1, int h2, int kz);
 int launch_l12(int KZ, const CUtensorMap *maps, const L12Args &a, cudaStream_t s);
 
-// maps: {A, B piece 1, B piece 2, out store, A lo, B1 lo, B2 lo, out lo store} (lo: precision 2 only)
+// maps: {A, B piece 1, B piece 2, out store, A lo, B1 lo, B2 lo, out lo store, bias operand piece 1,
+//        bias operand piece 2} (lo: precision 2 only; bias operand tiles: bf16 only)
 int launch_l2_pair(int NP, int prec, const CUtensorMap *maps, const L2Args &a, cudaStream_t s);

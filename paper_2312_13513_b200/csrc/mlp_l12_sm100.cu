@@ -245,19 +245,22 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
             const int zb = it & 1;
             rcx::mbar_wait(&zfull[zb], (it >> 1) & 1);
             const uint64_t d1 = rcm::desc_sw<32>(sOnes), dbk = rcm::desc_sw<32>(sBK + zb * BK_AL);
+            // (one accumulator chain advances ~220 clk per MMA: after the first two piece-1 MMAs the
+            // pieces are interleaved again, as in the main loop)
+            const uint64_t da = rcm::desc_sw<128>(A), db = rcm::desc_sw<128>(B);
             rcx::mbar_wait_sleep(c2empty, (it & 1) ^ 1);
             rcx::tc_fence_after();
             rcx::mma_bf16_pair(tmem, d1, dbk, idp1, 0);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              rcx::mma_bf16_pair(tmem, rcm::desc_sw<128>(A) + 2 * k, rcm::desc_sw<128>(B) + 2 * k, idp1, 1);
+            rcx::mma_bf16_pair(tmem, da, db, idp1, 1);
             rcx::mbar_wait(c2emptyB, (it & 1) ^ 1);
             rcx::tc_fence_after();
             rcx::mma_bf16_pair(tmem + P1, d1, dbk + ((H1 * 32) >> 4), idp2, 0);
+            rcx::mma_bf16_pair(tmem + P1, da, db + ((H1 * 128) >> 4), idp2, 1);
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              rcx::mma_bf16_pair(tmem + P1, rcm::desc_sw<128>(A) + 2 * k, rcm::desc_sw<128>(B) + ((H1 * 128) >> 4) + 2 * k,
-                                 idp2, 1);
+            for (int k = 1; k < 4; ++k) {
+              rcx::mma_bf16_pair(tmem, da + 2 * k, db + 2 * k, idp1, 1);
+              rcx::mma_bf16_pair(tmem + P1, da + 2 * k, db + ((H1 * 128) >> 4) + 2 * k, idp2, 1);
+            }
             rcx::mma_commit_pair_mask(&freed[s], (uint16_t)0xF);
             TR(0, g, 2);
             continue;

@@ -89,7 +89,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     l2_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBa,
                    const __grid_constant__ CUtensorMap mapBb, const __grid_constant__ CUtensorMap mapOut,
                    const __grid_constant__ CUtensorMap mapAlo, const __grid_constant__ CUtensorMap mapBalo,
-                   const __grid_constant__ CUtensorMap mapBblo, const __grid_constant__ CUtensorMap mapOutlo, L2Args a) {
+                   const __grid_constant__ CUtensorMap mapBblo, const __grid_constant__ CUtensorMap mapOutlo,
+                   const __grid_constant__ CUtensorMap mapKa, const __grid_constant__ CUtensorMap mapKb, L2Args a) {
   static_assert(NP % 16 == 0 && NP <= 512, "pass width");
   constexpr int P1 = NP > 256 ? 256 : NP, P2 = NP - P1;
   constexpr int H1 = P1 / 2, H2 = P2 / 2;  // B rows per CTA of each piece
@@ -102,6 +103,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
   constexpr uint32_t A_BYTES = 128 * RB, B_BYTES = (NP / 2) * RB;  // one copy; X3 stages hold hi and lo
   constexpr uint32_t STAGE = (NOP * (A_BYTES + B_BYTES) + 1023u) & ~1023u;  // [A hi | A lo | B hi | B lo]
   constexpr int W_TMA = NEPI, W_MMA = NEPI + 1;
+  // bf16: the bias is folded into the MMAs (one K = 16 MMA per piece of a ones tile against the
+  // (b_hi, b_lo, 0...) operand tile at the start of a tile), so the drain only converts; tf32/X3
+  // add the fp32 bias in the epilogue
+  constexpr bool BFOLD = !TF32;
+  constexpr uint32_t BK_BYTES = (NP / 2) * 32, BK_AL = ((NP / 2) * 32 + 1023u) & ~1023u;
+  constexpr int P1G = P1 / 16, P2G = P2 / 16;  // 16-column groups of the two accumulator pieces
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = rcx::smem_u32(smem_raw);
@@ -111,10 +118,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
   uint8_t *sST = sW + S * STAGE;                        // NEPI x 2 x 1 KB store staging
   float *sB2 = reinterpret_cast<float *>(sST + NEPI * 2 * STG);  // 2 x [b | w4 (DOT)] slices
   constexpr int VEC = DOT ? 2 * NP : NP;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sB2 + 2 * VEC);
-  uint64_t *full = bar, *empty = full + S, *c2full = empty + S, *c2empty = c2full + 1, *bfull = c2empty + 1,
-           *bempty = bfull + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bempty + 2);
+  uint8_t *sBK = reinterpret_cast<uint8_t *>(sB2) + ((2 * VEC * 4 + 1023u) & ~1023u);  // BFOLD: 2 x b operand tile
+  uint8_t *sOnes = sBK + (BFOLD ? 2 * BK_AL : 0);                                   // BFOLD: 128 x 16 bf16 ones
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sOnes + (BFOLD ? 4096 : 0));
+  uint64_t *full = bar, *empty = full + S, *c2full = empty + S, *c2empty = c2full + 1, *c2emptyB = c2empty + 1,
+           *bfull = c2emptyB + 1, *bempty = bfull + 2, *bkfull = bempty + 2, *bkempty = bkfull + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bkempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = rcx::cluster_rank();
@@ -130,11 +139,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
       if (P2 > 0) rcx::prefetch_tmap(&mapBblo);
       if (!DOT) rcx::prefetch_tmap(&mapOutlo);
     }
+    if (BFOLD) {
+      rcx::prefetch_tmap(&mapKa);
+      if (P2 > 0) rcx::prefetch_tmap(&mapKb);
+    }
     for (int s = 0; s < S; ++s) { rcx::mbar_init(&full[s], 2); rcx::mbar_init(&empty[s], 1); }
     rcx::mbar_init(c2full, 1);
-    rcx::mbar_init(c2empty, 2 * NEPI);
-    for (int z = 0; z < 2; ++z) { rcx::mbar_init(&bfull[z], 1); rcx::mbar_init(&bempty[z], NEPI); }
+    rcx::mbar_init(c2empty, 2 * NEPI);   // piece 1 (columns [0, P1)) copied out, both CTAs
+    rcx::mbar_init(c2emptyB, 2 * NEPI);  // piece 2
+    for (int z = 0; z < 2; ++z) {
+      rcx::mbar_init(&bfull[z], 1);
+      rcx::mbar_init(&bempty[z], NEPI);
+      rcx::mbar_init(&bkfull[z], 2);
+      rcx::mbar_init(&bkempty[z], 1);
+    }
     rcx::fence_mbar_init();
+  }
+  if (BFOLD) {
+    for (int i = threadIdx.x; i < 1024; i += L2_THREADS) reinterpret_cast<uint32_t *>(sOnes)[i] = 0x3F803F80u;
+    fence_async_smem();  // read by the tensor core (async proxy)
   }
   if (warp == W_MMA) rcx::tmem_alloc_pair(tmem_slot, 512);
   rcx::tc_fence_before();
@@ -160,6 +183,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
         rcx::mbar_arrive_expect_tx(&bfull[zb], VEC * 4);
         rcx::bulk_g2s(sB2 + zb * VEC, a.bias + (size_t)net * a.N + pass * NP, NP * 4, &bfull[zb]);
         if (DOT) rcx::bulk_g2s(sB2 + zb * VEC + NP, a.w4 + (size_t)net * a.N + pass * NP, NP * 4, &bfull[zb]);
+        if (BFOLD) {  // this CTA's rows of the bias operand tile, completion on the leader's barrier
+          rcx::mbar_wait_sleep(&bkempty[zb], ((it >> 1) & 1) ^ 1);
+          rcx::mbar_arrive_expect_tx_cluster(rcx::map_cta(&bkfull[zb], 0), BK_BYTES);
+          rcx::tma_load_3d_pair(sBK + zb * BK_AL, &mapKa, &bkfull[zb], 0, pass * NP + rank * H1, net);
+          if (P2 > 0) rcx::tma_load_3d_pair(sBK + zb * BK_AL + H1 * 32, &mapKb, &bkfull[zb], 0, pass * NP + P1 + rank * H2, net);
+        }
         for (int c = 0; c < C; ++c) {
           rcx::mbar_wait_sleep(&empty[s], ph ^ 1);
           rcx::mbar_arrive_expect_tx_cluster(full0 + s * 8, NOP * (A_BYTES + B_BYTES));
@@ -188,7 +217,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
       int it = 0;
       for (int tile = cl; tile < total; tile += ncl, ++it) {
         TRACE(W_MMA, it, 0);
-        rcx::mbar_wait(c2empty, (it & 1) ^ 1);  // previous tile drained
+        if (!BFOLD) {
+          rcx::mbar_wait(c2empty, (it & 1) ^ 1);  // previous tile drained
+          rcx::mbar_wait(c2emptyB, (it & 1) ^ 1);
+        }
         TRACE(W_MMA, it, 1);
         rcx::tc_fence_after();
         for (int c = 0; c < C; ++c) {
@@ -197,9 +229,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
           const uint64_t da = rcm::desc_sw<RB>(sW + s * STAGE);
           const uint64_t db = rcm::desc_sw<RB>(sW + s * STAGE + NOP * A_BYTES);
           constexpr uint64_t ALO = A_BYTES >> 4, BLO = B_BYTES >> 4, BP2 = (H1 * RB) >> 4;
+          if (BFOLD && c == 0) {
+            // the accumulator starts at the bias (ones x b operand); piece 1 restarts as soon as the
+            // drain has copied it out, piece 2 (c2emptyB) follows
+            const int zb = it & 1;
+            rcx::mbar_wait(&bkfull[zb], (it >> 1) & 1);
+            const uint64_t d1 = rcm::desc_sw<32>(sOnes), dk = rcm::desc_sw<32>(sBK + zb * BK_AL);
+            // (the tensor pipe runs one accumulator chain at ~220 clk per MMA: after the first two
+            // piece-1 MMAs the pieces are interleaved again, as in the main loop)
+            rcx::mbar_wait(c2empty, (it & 1) ^ 1);
+            rcx::tc_fence_after();
+            rcm::mma_pair<false>(tmem, d1, dk, idp1, 0);
+            rcm::mma_pair<false>(tmem, da, db, idp1, 1);
+            if (P2 > 0) {
+              rcx::mbar_wait(c2emptyB, (it & 1) ^ 1);
+              rcx::tc_fence_after();
+              rcm::mma_pair<false>(tmem + P1, d1, dk + ((H1 * 32) >> 4), idp2, 0);
+              rcm::mma_pair<false>(tmem + P1, da, db + BP2, idp2, 1);
+            }
+#pragma unroll
+            for (int k = 1; k < KC / E::KATOM; ++k) {
+              rcm::mma_pair<false>(tmem, da + 2 * k, db + 2 * k, idp1, 1);
+              if (P2 > 0) rcm::mma_pair<false>(tmem + P1, da + 2 * k, db + BP2 + 2 * k, idp2, 1);
+            }
+            rcx::mma_commit_pair(&empty[s]);
+            rcx::mma_commit_pair(&bkempty[zb]);
+            if (++s == S) { s = 0; ph ^= 1; }
+            continue;
+          }
 #pragma unroll
           for (int k = 0; k < KC / E::KATOM; ++k) {  // 32-byte K atoms: descriptor start += 2
-            const uint32_t acc = (c | k) != 0;
+            const uint32_t acc = BFOLD || (c | k) != 0;
             rcm::mma_pair<TF32>(tmem, da + 2 * k, db + 2 * k, idp1, acc);
             if (P2 > 0) rcm::mma_pair<TF32>(tmem + P1, da + 2 * k, db + BP2 + 2 * k, idp2, acc);
             if (X3) {  // + a_lo b_hi + a_hi b_lo
@@ -222,7 +282,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     constexpr int NCH = NP / 16;
     constexpr int MAXCH = (NCH + 3) / 4;  // 16-column chunks per warp (7 at NP = 400)
     const int ch_lo = (NCH * sub) / 4, ch_hi = (NCH * (sub + 1)) / 4;
-    const uint32_t c2empty0 = rcx::map_cta(c2empty, 0);
+    const uint32_t c2empty0 = rcx::map_cta(c2empty, 0), c2emptyB0 = rcx::map_cta(c2emptyB, 0);
+    // bf16: this warp's groups of piece 1 and of piece 2 (released separately)
+    const int g1lo = P1G * sub / 4, n1 = P1G * (sub + 1) / 4 - g1lo;
+    const int g2lo = P1G + P2G * sub / 4, n2 = P1G + P2G * (sub + 1) / 4 - g2lo;
     uint8_t *stg_base = sST + warp * 2 * STG;
     uint32_t nst = 0;
     int it = 0;
@@ -246,7 +309,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
         if (ch_lo == ch_hi) {
           rcx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
+          if (lane == 0) rcx::mbar_arrive_cluster(c2empty0), rcx::mbar_arrive_cluster(c2emptyB0);
         }
         for (int cc = ch_lo; cc < ch_hi; cc += 2) {
           uint32_t v[32];
@@ -259,7 +322,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
           if (cc + 2 >= ch_hi) {
             rcx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
+            if (lane == 0) rcx::mbar_arrive_cluster(c2empty0), rcx::mbar_arrive_cluster(c2emptyB0);
             TRACE(warp, it, 2);
           }
 #pragma unroll
@@ -313,44 +376,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
         }
         if constexpr (DOT) a.opart[((size_t)(net * a.passes + pass) * 4 + sub) * a.cap + grow + lane] = dot;
       } else {
-        const int nch = ch_hi - ch_lo;
-        // Phase A (no MUFU): every accumulator column of this warp -> registers as 16-bit pairs of
-        // (acc + bias): bf16 for layer 2 (the GELU input was bf16 anyway: bit-identical), f16 for the
-        // fp32 layer-3 GELU.  Then release the accumulator, so the next tile's MMAs run under phase B.
-        uint32_t pk[MAXCH][8];
-  #pragma unroll
-        for (int c = 0; c < MAXCH; ++c) {
-          if (c < nch) {
-            uint32_t v[16];
-            rcx::tmem_ld16(tmem + tq + (ch_lo + c) * 16, v);
+        // Phase A (no MUFU): every accumulator column of this warp (bias included by the MMA) ->
+        // registers as 16-bit pairs: bf16 for layer 2 (the GELU input), f16 for the fp32 layer-3
+        // GELU.  Piece 1 is released first (its MMAs of the next tile restart), then piece 2, so
+        // the next tile's MMAs run under phase B.
+        constexpr int MAX1 = (P1G + 3) / 4, MAX2 = P2G > 0 ? (P2G + 3) / 4 : 1;
+        uint32_t pk1[MAX1][8], pk2[MAX2][8];
+        auto copy = [&](auto &pk, int glo, int n) {  // n groups from glo, two loads in flight at a time
+          constexpr int M = sizeof(pk) / sizeof(pk[0]);
+#pragma unroll
+          for (int i0 = 0; i0 < M; i0 += 2) {
+            uint32_t v[2][16];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+              if (i0 + i < M && i0 + i < n) rcx::tmem_ld16(tmem + tq + (glo + i0 + i) * 16, v[i]);
             rcx::tmem_ld_wait();
-            const float4 *bb = reinterpret_cast<const float4 *>(b2 + (ch_lo + c) * 16);
-  #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float4 b = bb[j];
-              const float x0 = __uint_as_float(v[4 * j]) + b.x, x1 = __uint_as_float(v[4 * j + 1]) + b.y;
-              const float x2 = __uint_as_float(v[4 * j + 2]) + b.z, x3 = __uint_as_float(v[4 * j + 3]) + b.w;
-              pk[c][2 * j] = DOT ? cvt_f16x2(x0, x1) : cvt_bf16x2(x0, x1);
-              pk[c][2 * j + 1] = DOT ? cvt_f16x2(x2, x3) : cvt_bf16x2(x2, x3);
-            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+              if (i0 + i < M)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  const float x0 = __uint_as_float(v[i][2 * j]), x1 = __uint_as_float(v[i][2 * j + 1]);
+                  pk[i0 + i][j] = DOT ? cvt_f16x2(x0, x1) : cvt_bf16x2(x0, x1);
+                }
           }
-        }
+        };
+        copy(pk1, g1lo, n1);
         rcx::tc_fence_before();
         __syncwarp();
         if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
+        copy(pk2, g2lo, n2);
+        rcx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) rcx::mbar_arrive_cluster(c2emptyB0);
         TRACE(warp, it, 2);
         // Phase B: GELU (MUFU) and the layer's output path
         if constexpr (DOT) {  // layer 3: GELU(acc + b3) . w4 in fp32
           const float *w4s = b2 + NP;
           float dot = 0.f;
   #pragma unroll
-          for (int c = 0; c < MAXCH; ++c) {
-            if (c < nch) {
-              const float4 *ww = reinterpret_cast<const float4 *>(w4s + (ch_lo + c) * 16);
+          for (int c = 0; c < MAX1 + MAX2; ++c) {
+            if (c < MAX1 ? c < n1 : c - MAX1 < n2) {
+              const uint32_t *p = c < MAX1 ? pk1[c] : pk2[c - MAX1];
+              const int gc = c < MAX1 ? g1lo + c : g2lo + c - MAX1;
+              const float4 *ww = reinterpret_cast<const float4 *>(w4s + gc * 16);
   #pragma unroll
               for (int j = 0; j < 4; ++j) {
                 const float4 w = ww[j];
-                const float2 a01 = f16x2_to_f2(pk[c][2 * j]), a23 = f16x2_to_f2(pk[c][2 * j + 1]);
+                const float2 a01 = f16x2_to_f2(p[2 * j]), a23 = f16x2_to_f2(p[2 * j + 1]);
                 dot = fmaf(rcm::gelu_f32(a01.x), w.x, dot);
                 dot = fmaf(rcm::gelu_f32(a01.y), w.y, dot);
                 dot = fmaf(rcm::gelu_f32(a23.x), w.z, dot);
@@ -361,11 +434,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
           a.opart[((size_t)(net * a.passes + pass) * 4 + sub) * a.cap + grow + lane] = dot;
         } else {  // layer 2: bf16 GELU -> [32 rows][32 B] staging (32-byte TMA swizzle) -> TMA store
   #pragma unroll
-          for (int c = 0; c < MAXCH; ++c) {
-            if (c < nch) {
+          for (int c = 0; c < MAX1 + MAX2; ++c) {
+            if (c < MAX1 ? c < n1 : c - MAX1 < n2) {
+              const uint32_t *p = c < MAX1 ? pk1[c] : pk2[c - MAX1];
+              const int gc = c < MAX1 ? g1lo + c : g2lo + c - MAX1;
               uint32_t g[8];
   #pragma unroll
-              for (int j = 0; j < 8; ++j) g[j] = gelu_bf16x2(pk[c][j]);
+              for (int j = 0; j < 8; ++j) g[j] = gelu_bf16x2(p[j]);
               uint8_t *stg = stg_base + (nst & 1) * 1024;
               if (lane == 0) bulk_wait_read1();  // the store that last used this buffer has read it
               __syncwarp();
@@ -375,7 +450,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
               fence_async_smem();
               __syncwarp();
               if (lane == 0) {
-                tma_store_3d(&mapOut, stg, pass * NP + (ch_lo + c) * 16, grow, net);
+                tma_store_3d(&mapOut, stg, pass * NP + gc * 16, grow, net);
                 bulk_commit();
               }
               ++nst;
@@ -402,7 +477,8 @@ template <int NP, bool DOT, int PREC>
 int launch_l2_pair_t(const CUtensorMap *M, L2Args a, cudaStream_t s) {
   constexpr int RB = row_bytes<PREC>();
   constexpr size_t STAGE = (rcm::Prec<PREC>::NOP * (128 * RB + (NP / 2) * RB) + 1023) & ~(size_t)1023;
-  const size_t fixed = 1024 + NEPI * 2 * stg_bytes<(PREC != 0)>() + 2 * (DOT ? 2 : 1) * NP * 4 + 512;
+  constexpr size_t BK = PREC == 0 ? 2 * ((((size_t)NP / 2) * 32 + 1023) & ~(size_t)1023) + 4096 : 0;  // b operand + ones
+  const size_t fixed = 1024 + NEPI * 2 * stg_bytes<(PREC != 0)>() + ((2 * (DOT ? 2 : 1) * NP * 4 + 1023) & ~(size_t)1023) + BK + 512;
   int stages = (int)((232448 - fixed) / STAGE);
   if (stages > 8) stages = 8;
   if (stages < 2) return rc_fail(RC_EUNSUPPORTED, "layer-2 GEMM: pass width %d does not fit", NP);
@@ -433,7 +509,7 @@ int launch_l2_pair_t(const CUtensorMap *M, L2Args a, cudaStream_t s) {
   const int total = a.nets * (a.m_tiles / 2) * a.passes;
   int clusters = resident;
   if (clusters > total) clusters = total;
-  l2_pair_kernel<NP, DOT, PREC><<<2 * clusters, L2_THREADS, smem, s>>>(M[0], M[1], M[2], M[3], M[4], M[5], M[6], M[7], a);
+  l2_pair_kernel<NP, DOT, PREC><<<2 * clusters, L2_THREADS, smem, s>>>(M[0], M[1], M[2], M[3], M[4], M[5], M[6], M[7], M[8], M[9], a);
   RC_LAUNCH_CHECK();
   return RC_OK;
 }

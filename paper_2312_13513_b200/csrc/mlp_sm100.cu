@@ -424,9 +424,17 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
     hi = f2tf32((float)w);
     if (lo) *lo = f2tf32((float)(w - (double)hi));
   };
-  // b2 as an extra K = 16 operand of the layer-2 MMAs (the A side is a tile of ones):
+  // b2, b3 as an extra K = 16 operand of the layer-2/3 MMAs (the A side is a tile of ones):
   // column 0 = bf16(b), column 1 = bf16(b - bf16(b)), so the accumulator starts at b to ~2^-17
-  std::vector<uint16_t> B2k(tf32 ? 0 : (size_t)nets * h2 * 16, 0);
+  std::vector<uint16_t> B2k(tf32 ? 0 : (size_t)nets * h2 * 16, 0), B3k(tf32 ? 0 : (size_t)nets * h3 * 16, 0);
+  auto bias_operand = [](double b, uint16_t *row) {
+    const uint16_t hi = f2bf((float)b);
+    uint32_t hb = (uint32_t)hi << 16;
+    float hf;
+    std::memcpy(&hf, &hb, 4);
+    row[0] = hi;
+    row[1] = f2bf((float)(b - (double)hf));
+  };
   std::vector<float> b1((size_t)nets * h1), b2((size_t)nets * h2), b3((size_t)nets * h3), w4((size_t)nets * h3), b4(nets);
   for (int i = 0; i < nets; ++i) {
     const double *p = d->params + i * P;
@@ -461,14 +469,7 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
     p += (size_t)h2 * h1;
     for (int r = 0; r < h2; ++r) {
       b2[(size_t)i * h2 + r] = (float)p[r];
-      if (!tf32) {
-        const uint16_t hi = f2bf((float)p[r]);
-        uint32_t hb = (uint32_t)hi << 16;
-        float hf;
-        std::memcpy(&hf, &hb, 4);
-        B2k[((size_t)i * h2 + r) * 16] = hi;
-        B2k[((size_t)i * h2 + r) * 16 + 1] = f2bf((float)(p[r] - (double)hf));
-      }
+      if (!tf32) bias_operand(p[r], &B2k[((size_t)i * h2 + r) * 16]);
     }
     p += h2;
     for (size_t e = 0; e < (size_t)h3 * h2; ++e) {
@@ -476,7 +477,10 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
       else W3[(size_t)i * h3 * h2 + e] = f2bf((float)p[e]);
     }
     p += (size_t)h3 * h2;
-    for (int r = 0; r < h3; ++r) b3[(size_t)i * h3 + r] = (float)p[r];
+    for (int r = 0; r < h3; ++r) {
+      b3[(size_t)i * h3 + r] = (float)p[r];
+      if (!tf32) bias_operand(p[r], &B3k[((size_t)i * h3 + r) * 16]);
+    }
     p += h3;
     for (int r = 0; r < h3; ++r) w4[(size_t)i * h3 + r] = (float)p[r];
     p += h3;
@@ -500,7 +504,7 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
             up((void **)&n->d_xmean, xm.data(), xm.size() * 4) && up((void **)&n->d_xinvstd, xi.data(), xi.size() * 4) &&
             up((void **)&n->d_ymean, d->y_mean, nets * 8) && up((void **)&n->d_ystd, d->y_std, nets * 8) &&
             up((void **)&n->d_species, d->species_of_net, nets * 4);
-  if (ok && !tf32) ok = up(&n->d_b2k, B2k.data(), B2k.size() * 2);
+  if (ok && !tf32) ok = up(&n->d_b2k, B2k.data(), B2k.size() * 2) && up(&n->d_b3k, B3k.data(), B3k.size() * 2);
   if (ok && x3)
     ok = up(&n->d_W1lo, L1v.data(), L1v.size() * 4) && up(&n->d_W2lo, L2v.data(), L2v.size() * 4) &&
          up(&n->d_W3lo, L3v.data(), L3v.size() * 4);
@@ -532,7 +536,7 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   const int Q1 = NP3 > 256 ? 256 : NP3, Q2 = NP3 - Q1;
   // layer 1: {z, W1, h1 store (32-row boxes of one 128-byte row), z lo, W1 lo, h1 lo store}
   // layers 2/3: {A, B piece 1, B piece 2, h2 store (32 x 16 boxes), lo copies of the same}
-  CUtensorMap m1[6], m2[8], m3[8];
+  CUtensorMap m1[6], m2[10], m3[10];
   const int sbox = 128 / EB;  // h1 store box width: one 128-byte row
   int rc;
   for (int part = 0; part < (x3 ? 2 : 1); ++part) {
@@ -567,6 +571,17 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   if (!x3) {  // the lo slots are never read: any valid map
     for (int k = 0; k < 3; ++k) m1[3 + k] = m1[k];
     for (int k = 0; k < 4; ++k) m2[4 + k] = m2[k], m3[4 + k] = m3[k];
+  }
+  // bf16: bias operand tiles of layers 2 and 3 (K = 16, 32-byte rows); unused (any valid map) otherwise
+  if (!tf32) {
+    if ((rc = make_map(&m2[8], n->d_b2k, 16, n->h2, nets, P1 / 2, 16, 2)) ||
+        (rc = make_map(&m2[9], n->d_b2k, 16, n->h2, nets, P2 > 0 ? P2 / 2 : P1 / 2, 16, 2)) ||
+        (rc = make_map(&m3[8], n->d_b3k, 16, n->h3, nets, Q1 / 2, 16, 2)) ||
+        (rc = make_map(&m3[9], n->d_b3k, 16, n->h3, nets, Q2 > 0 ? Q2 / 2 : Q1 / 2, 16, 2)))
+      return rc;
+  } else {
+    m2[8] = m2[9] = m2[0];
+    m3[8] = m3[9] = m3[0];
   }
   RC_CUDA_TRY(cudaMemsetAsync(qpart, 0, QPART_BLOCKS * 8, s));
   int64_t launches = 1;

@@ -66,7 +66,7 @@ struct rc_mlp {
   void *d_W1 = nullptr, *d_W2 = nullptr, *d_W3 = nullptr;   // [nets][N][K] bf16 or fp32(tf32-rounded)
   void *d_W1lo = nullptr, *d_W2lo = nullptr, *d_W3lo = nullptr;  // RC_TF32X3: tf32(W - W_hi)
   float *d_b1 = nullptr, *d_b2 = nullptr, *d_b3 = nullptr;  // [nets][N]
-  void *d_b2k = nullptr;  // bf16: b2 as a K = 16 MMA operand [nets][N][16] = (hi, lo, 0...) (fused layer-1/2 kernel)
+  void *d_b2k = nullptr, *d_b3k = nullptr;  // bf16: b2, b3 as K = 16 MMA operands [nets][N][16] = (hi, lo, 0...)
   float *d_w4 = nullptr;                                    // [nets][h3]
   float *d_b4 = nullptr;                                    // [nets]
   float *d_xmean = nullptr, *d_xinvstd = nullptr;           // [d_in]
