@@ -25,6 +25,7 @@ struct L2Args {
   const float *w4;         // layer-3 mode (nullptr: layer 2): [nets][N], layer 4 folded into the epilogue
   float *opart;            // layer-3 mode: [nets][passes*4][cap] partial dots
   int cap;
+  int ktail;               // MMA K atoms in the last K chunk when K is not a multiple of it (0: full chunk)
 };
 // fused layers 1+2 (mlp_l12_sm100.cu, bf16, h2 = 800): clusters of two CTA pairs share h1 chunks
 // maps: {z (KZ x 128 rows), W1 (KZ x 16 rows), W2 piece 1 (32 x 128 rows), W2 piece 2 (32 x 72 rows),
@@ -35,6 +36,9 @@ struct L12Args {
 };
 bool l12_supported(int h1, int h2, int kz);
 int launch_l12(int KZ, const CUtensorMap *maps, const L12Args &a, cudaStream_t s);
+// the same layers on one CTA pair per (row block, net, pass) tile, h1 recomputed per pass
+// (mlp_l12p_sm100.cu); maps as launch_l12 except W1: 3D [nets][h1][KZ], boxes of KZ x 32 rows
+int launch_l12p(int KZ, const CUtensorMap *maps, const L12Args &a, cudaStream_t s);
 
 // maps: {A, B piece 1, B piece 2, out store, A lo, B1 lo, B2 lo, out lo store, bias operand piece 1,
 //        bias operand piece 2} (lo: precision 2 only; bias operand tiles: bf16 only)

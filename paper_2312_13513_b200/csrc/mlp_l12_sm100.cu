@@ -191,7 +191,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
       }
     }
   } else if (warp == W_AUX && prank == 0) {
-    if (lane == 0) {  // ---------------------------------- layer-1 MMA issuer (pair leaders)
+    {  // ------------------------------ layer-1 MMA issuer (pair leaders; converged warp, elected lane issues)
       // Runs ahead of the layer-2 issuer by up to NA1 chunks (the layer-1 accumulators), so the
       // GELU + DSMEM exchange of a half-chunk overlaps several layer-2 chunk periods.
       constexpr uint32_t id1 = rcx::make_idesc(1u, 256, 64);
@@ -200,7 +200,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
       for (int tile = cl; tile < total; tile += ncl, ++it) {
         const int zb = it & 1, net = tile / pairs;
         if (net != cur_net) {
-          if (cur_net >= 0) rcx::mma_commit_pair_mask(w1empty, pair_mask);  // done with the previous net's W1
+          if (cur_net >= 0 && rcx::elect_one()) rcx::mma_commit_pair_mask(w1empty, pair_mask);  // previous net's W1 done
+          __syncwarp();
           rcx::mbar_wait(w1full, nw & 1);
           cur_net = net;
           ++nw;
@@ -216,15 +217,21 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           TR(4, it * C + c, 3);
           rcx::tc_fence_after();
           const uint64_t dw = rcm::desc_sw<KZ * 2>(sW1 + (c >> 1) * W1_CH);
+          if (rcx::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < KZ / 16; ++k) rcx::mma_bf16_pair(tmem + TMEM_ACC1 + b * 64, dz + 2 * k, dw + 2 * k, id1, k != 0);
-          rcx::mma_commit_pair_mask(&a1full[b], pair_mask);
+            for (int k = 0; k < KZ / 16; ++k)
+              rcx::mma_bf16_pair(tmem + TMEM_ACC1 + b * 64, dz + 2 * k, dw + 2 * k, id1, k != 0);
+            rcx::mma_commit_pair_mask(&a1full[b], pair_mask);
+          }
+          __syncwarp();
         }
-        rcx::mma_commit_pair_mask(&zempty[zb], pair_mask);
+        if (rcx::elect_one()) rcx::mma_commit_pair_mask(&zempty[zb], pair_mask);
+        __syncwarp();
       }
     }
   } else if (warp == W_MMA) {
-    if (lane == 0 && prank == 0) {  // --------------------------------- layer-2 MMA issuer (pair leaders)
+    if (prank == 0) {  // ------------------------------------------------ layer-2 MMA issuer (pair leaders)
+      // the whole warp runs the loop converged; one elected lane issues (descriptors stay uniform)
       constexpr uint32_t idp1 = rcx::make_idesc(1u, 256, P1), idp2 = rcx::make_idesc(1u, 256, P2);
       uint32_t G = 0;
       int it = 0;
@@ -236,46 +243,52 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           rcx::mbar_wait(&ready[s], (g / R) & 1);  // W2 stage and h1 chunk, both CTAs of the pair
           TR(0, g, 1);
           rcx::tc_fence_after();
-          uint8_t *A = sA + slot * SLOT;
-          uint8_t *B = sW + s * STAGE;
+          const uint64_t da = rcm::desc_sw<128>(sA + slot * SLOT), db = rcm::desc_sw<128>(sW + s * STAGE);
           if (c == 0) {
             // first chunk of a tile: the accumulator starts at b2 (one K = 16 MMA of a ones tile
             // against the b2 operand tile), and the drain releases it in two pieces, so the
             // piece-1 MMAs (columns [0, 256)) run while piece 2 is still being copied out
+            // (one accumulator chain advances ~220 clk per MMA: after the first two piece-1 MMAs
+            // the pieces are interleaved again, as in the main loop)
             const int zb = it & 1;
             rcx::mbar_wait(&zfull[zb], (it >> 1) & 1);
             const uint64_t d1 = rcm::desc_sw<32>(sOnes), dbk = rcm::desc_sw<32>(sBK + zb * BK_AL);
-            // (one accumulator chain advances ~220 clk per MMA: after the first two piece-1 MMAs the
-            // pieces are interleaved again, as in the main loop)
-            const uint64_t da = rcm::desc_sw<128>(A), db = rcm::desc_sw<128>(B);
             rcx::mbar_wait_sleep(c2empty, (it & 1) ^ 1);
             rcx::tc_fence_after();
-            rcx::mma_bf16_pair(tmem, d1, dbk, idp1, 0);
-            rcx::mma_bf16_pair(tmem, da, db, idp1, 1);
+            if (rcx::elect_one()) {
+              rcx::mma_bf16_pair(tmem, d1, dbk, idp1, 0);
+              rcx::mma_bf16_pair(tmem, da, db, idp1, 1);
+            }
+            __syncwarp();
             rcx::mbar_wait(c2emptyB, (it & 1) ^ 1);
             rcx::tc_fence_after();
-            rcx::mma_bf16_pair(tmem + P1, d1, dbk + ((H1 * 32) >> 4), idp2, 0);
-            rcx::mma_bf16_pair(tmem + P1, da, db + ((H1 * 128) >> 4), idp2, 1);
+            if (rcx::elect_one()) {
+              rcx::mma_bf16_pair(tmem + P1, d1, dbk + ((H1 * 32) >> 4), idp2, 0);
+              rcx::mma_bf16_pair(tmem + P1, da, db + ((H1 * 128) >> 4), idp2, 1);
 #pragma unroll
-            for (int k = 1; k < 4; ++k) {
-              rcx::mma_bf16_pair(tmem, da + 2 * k, db + 2 * k, idp1, 1);
-              rcx::mma_bf16_pair(tmem + P1, da + 2 * k, db + ((H1 * 128) >> 4) + 2 * k, idp2, 1);
+              for (int k = 1; k < 4; ++k) {
+                rcx::mma_bf16_pair(tmem, da + 2 * k, db + 2 * k, idp1, 1);
+                rcx::mma_bf16_pair(tmem + P1, da + 2 * k, db + ((H1 * 128) >> 4) + 2 * k, idp2, 1);
+              }
+              rcx::mma_commit_pair_mask(&freed[s], (uint16_t)0xF);
             }
-            rcx::mma_commit_pair_mask(&freed[s], (uint16_t)0xF);
+            __syncwarp();
             TR(0, g, 2);
             continue;
           }
+          if (rcx::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {  // K16 steps: 32-byte atoms along the 128-byte rows
-            const uint64_t da = rcm::desc_sw<128>(A) + 2 * k, db = rcm::desc_sw<128>(B) + 2 * k;
-            const uint32_t acc = 1;
-            rcx::mma_bf16_pair(tmem, da, db, idp1, acc);
-            rcx::mma_bf16_pair(tmem + P1, da, db + ((H1 * 128) >> 4), idp2, acc);
+            for (int k = 0; k < 4; ++k) {  // K16 steps: 32-byte atoms along the 128-byte rows
+              rcx::mma_bf16_pair(tmem, da + 2 * k, db + 2 * k, idp1, 1);
+              rcx::mma_bf16_pair(tmem + P1, da + 2 * k, db + ((H1 * 128) >> 4) + 2 * k, idp2, 1);
+            }
+            rcx::mma_commit_pair_mask(&freed[s], (uint16_t)0xF);  // all four CTAs wait for both pairs
           }
-          rcx::mma_commit_pair_mask(&freed[s], (uint16_t)0xF);  // all four CTAs wait for both pairs
+          __syncwarp();
           TR(0, g, 2);
         }
-        rcx::mma_commit_pair_mask(c2full, pair_mask);
+        if (rcx::elect_one()) rcx::mma_commit_pair_mask(c2full, pair_mask);
+        __syncwarp();
       }
     }
   } else if (warp == W_CPY) {
@@ -501,7 +514,7 @@ int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
 
 }  // namespace
 
-bool l12_supported(int h1, int h2, int kz) { return h1 % 64 == 0 && h2 == 2 * NP && (kz == 16 || kz == 32); }
+bool l12_supported(int h1, int h2, int kz) { return h1 % 64 == 0 && h1 >= 128 && h2 == 2 * NP && (kz == 16 || kz == 32); }
 
 #ifdef L12TRACE
 extern "C" __attribute__((visibility("default"))) int rc_debug_l12trace(void *host) {

@@ -209,7 +209,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
       }
     }
   } else if (warp == W_MMA) {
-    if (lane == 0 && leader) {  // ------------------------------------- MMA issuer (even CTA)
+    if (leader) {  // ------------- MMA issuer (even CTA; converged warp, one elected lane issues)
       constexpr uint32_t idp1 = rcx::make_idesc(E::FMT, 256, P1);
       constexpr uint32_t idp2 = rcx::make_idesc(E::FMT, 256, P2 > 0 ? P2 : 16);
       int s = 0;
@@ -229,6 +229,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
           const uint64_t da = rcm::desc_sw<RB>(sW + s * STAGE);
           const uint64_t db = rcm::desc_sw<RB>(sW + s * STAGE + NOP * A_BYTES);
           constexpr uint64_t ALO = A_BYTES >> 4, BLO = B_BYTES >> 4, BP2 = (H1 * RB) >> 4;
+          // the last K chunk may be partial (K = 800: 32 of 64); its zero-filled atoms are skipped
+          const int nk = (c == C - 1 && a.ktail) ? a.ktail : KC / E::KATOM;
           if (BFOLD && c == 0) {
             // the accumulator starts at the bias (ones x b operand); piece 1 restarts as soon as the
             // drain has copied it out, piece 2 (c2emptyB) follows
@@ -239,24 +241,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
             // piece-1 MMAs the pieces are interleaved again, as in the main loop)
             rcx::mbar_wait(c2empty, (it & 1) ^ 1);
             rcx::tc_fence_after();
-            rcm::mma_pair<false>(tmem, d1, dk, idp1, 0);
-            rcm::mma_pair<false>(tmem, da, db, idp1, 1);
+            if (rcx::elect_one()) {
+              rcm::mma_pair<false>(tmem, d1, dk, idp1, 0);
+              rcm::mma_pair<false>(tmem, da, db, idp1, 1);
+            }
+            __syncwarp();
             if (P2 > 0) {
               rcx::mbar_wait(c2emptyB, (it & 1) ^ 1);
               rcx::tc_fence_after();
-              rcm::mma_pair<false>(tmem + P1, d1, dk + ((H1 * 32) >> 4), idp2, 0);
-              rcm::mma_pair<false>(tmem + P1, da, db + BP2, idp2, 1);
             }
+            if (rcx::elect_one()) {
+              if (P2 > 0) {
+                rcm::mma_pair<false>(tmem + P1, d1, dk + ((H1 * 32) >> 4), idp2, 0);
+                rcm::mma_pair<false>(tmem + P1, da, db + BP2, idp2, 1);
+              }
 #pragma unroll
-            for (int k = 1; k < KC / E::KATOM; ++k) {
-              rcm::mma_pair<false>(tmem, da + 2 * k, db + 2 * k, idp1, 1);
-              if (P2 > 0) rcm::mma_pair<false>(tmem + P1, da + 2 * k, db + BP2 + 2 * k, idp2, 1);
+              for (int k = 1; k < KC / E::KATOM; ++k) {
+                if (k >= nk) break;
+                rcm::mma_pair<false>(tmem, da + 2 * k, db + 2 * k, idp1, 1);
+                if (P2 > 0) rcm::mma_pair<false>(tmem + P1, da + 2 * k, db + BP2 + 2 * k, idp2, 1);
+              }
+              rcx::mma_commit_pair(&empty[s]);
+              rcx::mma_commit_pair(&bkempty[zb]);
             }
-            rcx::mma_commit_pair(&empty[s]);
-            rcx::mma_commit_pair(&bkempty[zb]);
+            __syncwarp();
             if (++s == S) { s = 0; ph ^= 1; }
             continue;
           }
+          // (the full-chunk loop is kept free of the tail test: a per-MMA branch slows the issue)
+          if (rcx::elect_one()) {
+          if (nk == KC / E::KATOM) {
 #pragma unroll
           for (int k = 0; k < KC / E::KATOM; ++k) {  // 32-byte K atoms: descriptor start += 2
             const uint32_t acc = BFOLD || (c | k) != 0;
@@ -269,10 +283,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
               if (P2 > 0) rcm::mma_pair<TF32>(tmem + P1, da + 2 * k, db + BLO + BP2 + 2 * k, idp2, 1);
             }
           }
+          } else {
+#pragma unroll
+          for (int k = 0; k < KC / E::KATOM; ++k) {  // 32-byte K atoms: descriptor start += 2
+            if (k >= nk) break;  // partial last chunk (uniform branch, once per tile)
+            const uint32_t acc = BFOLD || (c | k) != 0;
+            rcm::mma_pair<TF32>(tmem, da + 2 * k, db + 2 * k, idp1, acc);
+            if (P2 > 0) rcm::mma_pair<TF32>(tmem + P1, da + 2 * k, db + BP2 + 2 * k, idp2, acc);
+            if (X3) {  // + a_lo b_hi + a_hi b_lo
+              rcm::mma_pair<TF32>(tmem, da + ALO + 2 * k, db + 2 * k, idp1, 1);
+              if (P2 > 0) rcm::mma_pair<TF32>(tmem + P1, da + ALO + 2 * k, db + BP2 + 2 * k, idp2, 1);
+              rcm::mma_pair<TF32>(tmem, da + 2 * k, db + BLO + 2 * k, idp1, 1);
+              if (P2 > 0) rcm::mma_pair<TF32>(tmem + P1, da + 2 * k, db + BLO + BP2 + 2 * k, idp2, 1);
+            }
+          }
+          }
           rcx::mma_commit_pair(&empty[s]);
+          }
+          __syncwarp();
           if (++s == S) { s = 0; ph ^= 1; }
         }
-        rcx::mma_commit_pair(c2full);
+        if (rcx::elect_one()) rcx::mma_commit_pair(c2full);
+        __syncwarp();
         TRACE(W_MMA, it, 2);
       }
     }
@@ -280,7 +312,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     const int q = warp & 3, sub = warp >> 2;
     const uint32_t tq = (uint32_t)(q * 32) << 16;
     constexpr int NCH = NP / 16;
-    constexpr int MAXCH = (NCH + 3) / 4;  // 16-column chunks per warp (7 at NP = 400)
     const int ch_lo = (NCH * sub) / 4, ch_hi = (NCH * (sub + 1)) / 4;
     const uint32_t c2empty0 = rcx::map_cta(c2empty, 0), c2emptyB0 = rcx::map_cta(c2emptyB, 0);
     // bf16: this warp's groups of piece 1 and of piece 2 (released separately)

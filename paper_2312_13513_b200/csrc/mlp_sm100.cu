@@ -129,6 +129,19 @@ __device__ __forceinline__ double ipow(double a, int e) {
   return r;
 }
 
+// b = y^lambda for 0 < y <= 1 with 1/lambda = n an integer (Box-Cox, R3): fp32 MUFU seed
+// (relative error ~1e-7), then two Newton steps on b^n = y, b <- b + (y / b^(n-1) - b) / n, each
+// squaring the relative error (x (n-1)/2): fp64-converged, ~30 instructions instead of pow()'s ~150.
+// Tiny y (fp32 seed out of range) and non-integer 1/lambda take pow().
+__device__ __forceinline__ double pow_lambda(double y, double lambda, int n) {
+  if (!(y > 0.0)) return 0.0;
+  if (n <= 0 || y < 1e-30) return pow(y, lambda);
+  double b = (double)exp2f((float)lambda * log2f((float)y));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) b = fma(y * rcx::rcp_f64(ipow(b, n - 1)) - b, lambda, b);
+  return b;
+}
+
 template <int NS>
 __global__ void __launch_bounds__(256) chem_epilogue_kernel(EpiArgs a, CellsDev c) {
   constexpr int CAP = NS ? NS : RC_MAX_NS;
@@ -151,38 +164,56 @@ __global__ void __launch_bounds__(256) chem_epilogue_kernel(EpiArgs a, CellsDev 
   }
   rcx::mbar_wait(&bar, 0);
   const double *hlo = s_tab + ThermoSeg::hlo(ns), *hhi = s_tab + ThermoSeg::hhi(ns), *tmid = s_tab + ThermoSeg::tmid(ns);
+  // P with its columns gathered by net: Pn[k][net] = P[k][species[net]] (the other columns multiply
+  // dY = 0), so the per-cell arrays are indexed by unrolled loop counters only (registers)
+  double *sPn = sP + ((ns * ns + 1) & ~1);
+  const int nn = a.n_nets;
+  for (int e = threadIdx.x; e < ns * nn; e += blockDim.x) sPn[e] = sP[(e / nn) * ns + a.species[e % nn]];
+  __syncthreads();
 
   double qsum = 0.0;
   int n_negout = 0, n_bad = 0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < a.rows; r += gridDim.x * blockDim.x) {
     const int64_t i = a.c0 + r;
     const double T = c.T[i], rho = c.rho[i];
-    double Yh[CAP], dY[CAP];
+    double Yh[CAP];
 #pragma unroll UR
     for (int k = 0; k < CAP; ++k)
       if (k < ns) {
         double y = c.Y[k * c.ld + i];
         Yh[k] = y > 0.0 ? y : 0.0;
-        dY[k] = 0.0;
       }
-    for (int net = 0; net < a.n_nets; ++net) {
-      float of = a.b4[net];
-      const float *op = a.opart + (size_t)net * a.nparts * a.cap + r;
-      for (int p = 0; p < a.nparts; ++p) of += op[(size_t)p * a.cap];
-      if (c.o) c.o[net * c.ld + i] = of;
-      const int s = a.species[net];
-      double ys = 0.0;
+    // all raw outputs of the cell first (independent loads in flight), then the transforms
+    constexpr int MAXNET = CAP;
+    float of[MAXNET];
+    double dY[MAXNET];  // by net
 #pragma unroll UR
-      for (int k = 0; k < CAP; ++k)
-        if (k == s) ys = Yh[k];
-      const double b = pow(ys, a.lambda);                         // b_s = Y^_s^lambda
-      const double ap = b + a.lambda * ((double)of * a.ystd[net] + a.ymean[net]);
-      const double ystar = ap > 0.0 ? ipow(ap, a.inv_lambda) : 0.0;  // inverse Box-Cox
+    for (int net = 0; net < MAXNET; ++net)
+      if (net < nn) {
+        const float *op = a.opart + (size_t)net * a.nparts * a.cap + r;
+        float v = a.b4[net];
+        if (a.nparts == 4) {
+          v += op[0];
+          v += op[(size_t)a.cap];
+          v += op[2 * (size_t)a.cap];
+          v += op[3 * (size_t)a.cap];
+        } else {
+          for (int p = 0; p < a.nparts; ++p) v += op[(size_t)p * a.cap];
+        }
+        of[net] = v;
+      }
 #pragma unroll UR
-      for (int k = 0; k < CAP; ++k)
-        if (k == s) dY[k] = ystar - ys;
-    }
-    // element projection dY <- P dY (fp64), sources
+    for (int net = 0; net < MAXNET; ++net)
+      if (net < nn) {
+        if (c.o) c.o[net * c.ld + i] = of[net];
+        const double y = __ldg(c.Y + (size_t)a.species[net] * c.ld + i);  // L1 hit: loaded above
+        const double ys = y > 0.0 ? y : 0.0;
+        const double b = pow_lambda(ys, a.lambda, a.inv_lambda);     // b_s = Y^_s^lambda
+        const double ap = b + a.lambda * ((double)of[net] * a.ystd[net] + a.ymean[net]);
+        const double ystar = ap > 0.0 ? ipow(ap, a.inv_lambda) : 0.0;  // inverse Box-Cox
+        dY[net] = ystar - ys;
+      }
+    // element projection dY <- P dY (fp64, species without a net contribute 0), sources
     double q = 0.0;
     bool neg = false, bad = false;
 #pragma unroll UR
@@ -190,8 +221,8 @@ __global__ void __launch_bounds__(256) chem_epilogue_kernel(EpiArgs a, CellsDev 
       if (k < ns) {
         double v = 0.0;
 #pragma unroll UR
-        for (int j = 0; j < CAP; ++j)
-          if (j < ns) v = fma(sP[k * ns + j], dY[j], v);
+        for (int net = 0; net < MAXNET; ++net)
+          if (net < nn) v = fma(sPn[k * nn + net], dY[net], v);
         neg |= (Yh[k] + v) < 0.0;
         const double w = rho * v * a.inv_dt;
         c.wdot[k * c.ld + i] = w;
@@ -524,6 +555,7 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   const bool tf32 = prec != 0, x3 = prec == 2;
   const int EB = tf32 ? 4 : 2;
   const int RB = x3 ? 64 : 128, KC = RB / EB;  // element bytes; K elements per swizzled operand row
+  const int KATOM = getenv("RC_NO_KTAIL") ? 1 << 20 : tf32 ? 8 : 16;  // K elements per MMA (32 bytes)
   const int nets = n->n_nets;
   // activations: hi copy at the start of each region, X3's lo copy right after it
   uint8_t *z = w + L.z, *h1 = w + L.h1, *h2 = w + L.h2;
@@ -559,7 +591,7 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   // fused layers 1+2 (bf16, paper widths); RC_NO_FUSE=1 forces the layer-wise path (tests, comparisons)
   const char *nf = getenv("RC_NO_FUSE");
   const bool fused = prec == 0 && l12_supported(n->h1, n->h2, KZ) && !(nf && nf[0] == '1');
-  CUtensorMap m12[7];
+  CUtensorMap m12[7], m12p[7];
   if (fused && ((rc = make_map(&m12[0], z, KZ, cap, 1, BM, KZ, EB)) ||
                 (rc = make_map_w1_groups(&m12[1], n->d_W1, KZ, n->h1, nets)) ||
                 (rc = make_map(&m12[2], n->d_W2, n->h1, n->h2, nets, 128, 64, EB)) ||
@@ -568,6 +600,12 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
                 (rc = make_map(&m12[5], n->d_b2k, 16, n->h2, nets, 128, 16, EB)) ||
                 (rc = make_map(&m12[6], n->d_b2k, 16, n->h2, nets, 72, 16, EB))))
     return rc;
+  const char *pe = getenv("RC_L12_PAIR");
+  const bool pairk = pe && pe[0] == '1';
+  if (fused) {
+    for (int k = 0; k < 7; ++k) m12p[k] = m12[k];
+    if ((rc = make_map(&m12p[1], n->d_W1, KZ, n->h1, nets, 32, KZ, EB))) return rc;
+  }
   if (!x3) {  // the lo slots are never read: any valid map
     for (int k = 0; k < 3; ++k) m1[3 + k] = m1[k];
     for (int k = 0; k < 4; ++k) m2[4 + k] = m2[k], m3[4 + k] = m3[k];
@@ -596,24 +634,38 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
       RC_LAUNCH_CHECK();
     }
     if (fused) {
-      // layers 1+2 in one kernel: h1 stays on chip (clusters of two CTA pairs share its chunks)
+      // layers 1+2 in one kernel: h1 stays on chip.  Default: clusters of two CTA pairs that share
+      // h1 chunks (132 SMs); RC_L12_PAIR=1: one CTA pair per (row block, net, pass) with h1
+      // recomputed per pass (all 148 SMs; measured 13% slower)
       L12Args g12{mt, nets, n->h1 / 64, n->h2, 0, 0, n->d_b2};
-      if ((rc = launch_l12(KZ, m12, g12, s))) return rc;
+      if ((rc = pairk ? launch_l12p(KZ, m12p, g12, s) : launch_l12(KZ, m12, g12, s))) return rc;
     } else {
       // layer 1: h1 = GELU(z W1^T) (b1 folded into z's constant-1 columns)
       L1Args g1{mt, (n->h1 + bn1 - 1) / bn1, nets, n->h1, 0, cap};
       if ((rc = launch_l1(KZ, prec, m1, g1, s))) return rc;
       // layer 2: h2 = GELU(h1 W2^T + b2), CTA-pair GEMM
-      L2Args la{mt, n->h2 / NP, nets, (n->h1 + KC - 1) / KC, n->h2, 0, n->d_b2, nullptr, nullptr, cap};
+      L2Args la{mt, n->h2 / NP, nets, (n->h1 + KC - 1) / KC, n->h2, 0, n->d_b2, nullptr, nullptr, cap, (n->h1 % KC) / KATOM};
       if ((rc = launch_l2_pair(NP, prec, m2, la, s))) return rc;
     }
     // layer 3 + folded layer 4: the same CTA-pair GEMM with the dot epilogue (K = h2, zero-filled to KC)
-    L2Args l3{mt, n->h3 / NP3, nets, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, n->d_w4, opart, cap};
+    L2Args l3{mt, n->h3 / NP3, nets, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, n->d_w4, opart, cap, (n->h2 % KC) / KATOM};
     if ((rc = launch_l2_pair(NP3, prec, m3, l3, s))) return rc;
     EpiArgs ea{c0, rows, cap, nets, 4 * (n->h3 / NP3), n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt, opart,
                n->d_b4, n->d_ymean, n->d_ystd, m->d_P, m->d_thermo, n->d_species, qpart};
-    const size_t esm = (size_t)ThermoSeg::size(m->ns) * 8 + (size_t)((m->ns * m->ns + 1) & ~1) * 8;
+    const size_t esm = (size_t)ThermoSeg::size(m->ns) * 8 + (size_t)((m->ns * m->ns + 1) & ~1) * 8 + (size_t)m->ns * nets * 8;
+    // one wave of resident blocks (grid-stride over the rows): a partial second wave would
+    // double the latency-bound kernel's time
+    static int eres[3] = {0, 0, 0};
+    const int ek = m->ns == 9 ? 0 : m->ns == 20 ? 1 : 2;
+    if (!eres[ek]) {
+      int per = 0;
+      const cudaError_t e = ek == 0 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, chem_epilogue_kernel<9>, 256, esm)
+                            : ek == 1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, chem_epilogue_kernel<20>, 256, esm)
+                                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, chem_epilogue_kernel<0>, 256, esm);
+      eres[ek] = (e == cudaSuccess && per > 0) ? per * mlp_num_sms() : mlp_num_sms();
+    }
     int eblocks = (rows + 255) / 256;
+    if (eblocks > eres[ek]) eblocks = eres[ek];
     if (eblocks > QPART_BLOCKS) eblocks = QPART_BLOCKS;
     ProfScope prof(RC_STAGE_EPILOGUE, s);
     if (m->ns == 9)

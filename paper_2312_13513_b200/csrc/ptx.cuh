@@ -229,6 +229,18 @@ __device__ __forceinline__ void bulk_s2s_cluster(uint32_t dst_cluster, const voi
       "r"(smem_u32(src)), "r"(bytes), "r"(bar_cluster)
       : "memory");
 }
+// one lane of the (converged) warp: issuing tcgen05 instructions from converged code lets the
+// compiler keep warp-uniform descriptors in uniform registers (a lane-0-only loop makes every MMA
+// a broadcast loop of R2UR moves)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, e;\n}"
+      : "=r"(p));
+  return p != 0;
+}
 // per-warpgroup register budget (all four warps of a warpgroup execute the same one)
 template <int N>
 __device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
