@@ -173,6 +173,19 @@ def test_layerwise_path_paper_shape(monkeypatch):
     print(f"C2 layer-wise bf16 errors: o {eo:.2e} wdot {ew:.2e} qdot {eq:.2e}")
 
 
+def test_pair_local_fused_kernel_paper_shape(monkeypatch):
+    """The pair-local fused layer-1/2 kernel (RC_L12_PAIR=1: one CTA pair per row block, net and
+    pass, h1 recomputed per pass) at the paper widths."""
+    monkeypatch.setenv("RC_L12_PAIR", "1")
+    c = inputs("C2", begin=0, end=65536)
+    g = Gpu("C2").run(c)
+    cols = np.unique((uniform(4445, np.arange(128)) * 65536).astype(np.int64))
+    sub = {k: (v[..., cols] if isinstance(v, np.ndarray) else v) for k, v in c.items()}
+    o = run_oracle("C2", sub)
+    eo, ew, eq = check_chem(g, o, mech("h2_9sp"), cols)
+    print(f"C2 pair-local fused bf16 errors: o {eo:.2e} wdot {ew:.2e} qdot {eq:.2e}")
+
+
 def test_ch4_paper_shape_sample():
     """C4 (CH4/air, 20 species, 19 nets, d_in 22): parity on a hashed sample."""
     cols = _sample("C4", 256)
