@@ -329,7 +329,7 @@ static int chem_checks(const rc_mech *m, const rc_mlp *n, const rc_cells *c, Cel
     return rc_fail(RC_EDTMISMATCH, "cells.dt=%g differs from the bundle's training dt=%g", c->dt, n->dt);
   if (c->n > 0 && (!ws || ((uintptr_t)ws & 255u)))
     return rc_fail(RC_EINVAL, "workspace must be non-NULL and 256-byte aligned");
-  size_t need = chem_workspace_bytes(m, n, c->n < 128 ? c->n : 128);  // smallest legal chunk
+  size_t need = chem_workspace_min_bytes(n, c->n);  // z of every cell + the smallest legal chunk
   if (c->n > 0 && ws_bytes < need) return rc_fail(RC_EINVAL, "workspace too small: %zu < %zu", ws_bytes, need);
   return RC_OK;
 }

@@ -376,7 +376,9 @@ struct WsLayout {
   int cap;
 };
 
-WsLayout ws_layout(const rc_mlp *n, int cap) {
+// z (the layer-1 A operand) is held for all `ncells` cells (one prologue launch per call; 32 B per
+// cell in bf16), the activations and partial outputs for one chunk of `cap` cells
+WsLayout ws_layout(const rc_mlp *n, int cap, int64_t ncells) {
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   WsLayout L;
   L.cap = cap;
@@ -384,7 +386,8 @@ WsLayout ws_layout(const rc_mlp *n, int cap) {
   L.qpart = o; o = al(o + QPART_BLOCKS * 8);
   // activation element bytes (RC_TF32X3 keeps a tf32 hi and a tf32 lo array of each)
   const size_t eb = n->precision == RC_BF16 ? 2 : 4, nc = n->precision == RC_TF32X3 ? 2 : 1;
-  L.z = o; o = al(o + nc * (size_t)cap * n->kpad1 * eb);
+  const size_t zrows = (size_t)((ncells + 255) / 256 * 256);
+  L.z = o; o = al(o + nc * zrows * n->kpad1 * eb);
   L.h1 = o; o = al(o + nc * (size_t)n->n_nets * cap * n->h1 * eb);
   L.h2 = o; o = al(o + nc * (size_t)n->n_nets * cap * n->h2 * eb);
   const int np3 = 4 * (n->h3 / l2_pass_width(n->h3));  // partial dots per row: 4 column quarters per pass
@@ -421,11 +424,13 @@ int launch_combine_reductions(const double *rp, const int64_t *dp, int k, double
 
 int cap_limit(const rc_mlp *n) { return n->precision == RC_TF32X3 ? std::min(MAX_CAP, 32768) : MAX_CAP; }
 
+size_t chem_workspace_min_bytes(const rc_mlp *n, int64_t ncells) { return ws_layout(n, 256, ncells).total; }
+
 size_t chem_workspace_bytes(const rc_mech *, const rc_mlp *n, int64_t ncells) {
   int64_t cap = (ncells + 255) / 256 * 256;  // chunks of CTA-pair (256-row) tiles
   if (cap > cap_limit(n)) cap = cap_limit(n);
   if (cap < 256) cap = 256;
-  return ws_layout(n, (int)cap).total;
+  return ws_layout(n, (int)cap, ncells).total;
 }
 
 int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
@@ -547,8 +552,8 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   if (c.n == 0) return RC_OK;
   // chunk capacity: largest multiple of 128 (<= MAX_CAP, <= n rounded up) whose layout fits the workspace
   int cap = (int)std::min<int64_t>((c.n + 255) / 256 * 256, cap_limit(n));
-  while (cap > 256 && ws_layout(n, cap).total > ws_bytes) cap -= 256;
-  WsLayout L = ws_layout(n, cap);
+  while (cap > 256 && ws_layout(n, cap, c.n).total > ws_bytes) cap -= 256;
+  WsLayout L = ws_layout(n, cap, c.n);
   if (L.total > ws_bytes) return rc_fail(RC_EINVAL, "workspace too small (%zu < %zu)", ws_bytes, L.total);
   uint8_t *w = static_cast<uint8_t *>(ws);
   const int prec = n->precision == RC_BF16 ? 0 : n->precision == RC_TF32 ? 1 : 2;
@@ -559,7 +564,8 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   const int nets = n->n_nets;
   // activations: hi copy at the start of each region, X3's lo copy right after it
   uint8_t *z = w + L.z, *h1 = w + L.h1, *h2 = w + L.h2;
-  const size_t zlo = (size_t)cap * n->kpad1 * EB, h1lo = (size_t)nets * cap * n->h1 * EB,
+  const int64_t zrows = (c.n + 255) / 256 * 256;  // z holds every cell of the call
+  const size_t zlo = (size_t)zrows * n->kpad1 * EB, h1lo = (size_t)nets * cap * n->h1 * EB,
                h2lo = (size_t)nets * cap * n->h2 * EB;
   auto *opart = reinterpret_cast<float *>(w + L.opart);
   auto *qpart = reinterpret_cast<double *>(w + L.qpart);
@@ -623,15 +629,24 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   }
   RC_CUDA_TRY(cudaMemsetAsync(qpart, 0, QPART_BLOCKS * 8, s));
   int64_t launches = 1;
+  {  // a3 for every cell of the call in one launch (HBM-bound: per-chunk launches were tail-dominated)
+    ProArgs pa{0, (int)c.n, (int)zrows, n->d_in, n->ns, KZ, (float)n->lambda_bc, (float)(1.0 / n->lambda_bc),
+               n->d_xmean, n->d_xinvstd, z, prec, (int64_t)(zlo / EB)};
+    ProfScope prof(RC_STAGE_PROLOGUE, s);
+    prologue_kernel<<<(unsigned)(zrows / 256), 256, 0, s>>>(pa, c);
+    RC_LAUNCH_CHECK();
+  }
   for (int64_t c0 = 0; c0 < c.n; c0 += cap) {
     const int rows = (int)std::min<int64_t>(cap, c.n - c0);
     const int mt = (rows + 2 * BM - 1) / (2 * BM) * 2;  // even: CTA pairs of 128-row tiles
-    ProArgs pa{c0, rows, mt * BM, n->d_in, n->ns, KZ, (float)n->lambda_bc, (float)(1.0 / n->lambda_bc), n->d_xmean,
-               n->d_xinvstd, z, prec, (int64_t)(zlo / EB)};
-    {
-      ProfScope prof(RC_STAGE_PROLOGUE, s);
-      prologue_kernel<<<(mt * BM + 255) / 256, 256, 0, s>>>(pa, c);
-      RC_LAUNCH_CHECK();
+    if (c0 > 0) {  // this chunk's rows of z: re-point the layer-1 A operand maps
+      const int zr = (int)std::min<int64_t>(cap, zrows - c0);
+      uint8_t *zc = z + (size_t)c0 * KZ * EB;
+      if ((rc = make_map(&m1[0], zc, KZ, zr, 1, BM, KZ, EB))) return rc;
+      if (x3 && (rc = make_map(&m1[3], zc + zlo, KZ, zr, 1, BM, KZ, EB))) return rc;
+      if (!x3) m1[3] = m1[0];
+      if (fused && (rc = make_map(&m12[0], zc, KZ, zr, 1, BM, KZ, EB))) return rc;
+      if (fused) m12p[0] = m12[0];
     }
     if (fused) {
       // layers 1+2 in one kernel: h1 stays on chip.  Default: clusters of two CTA pairs that share

@@ -120,6 +120,7 @@ int launch_transport(const rc_mech *m, const CellsDev &c, cudaStream_t s);
 
 struct ChemWs;  // defined in mlp_sm100.cu
 size_t chem_workspace_bytes(const rc_mech *m, const rc_mlp *n, int64_t ncells);
+size_t chem_workspace_min_bytes(const rc_mlp *n, int64_t ncells);  // the smallest chunk (256 cells)
 int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, size_t ws_bytes, cudaStream_t s);
 int launch_combine_reductions(const double *rp, const int64_t *dp, int k, double *red, int64_t *diag, cudaStream_t s);
 int mlp_upload(rc_mlp *n, const rc_mlp_desc *d);
