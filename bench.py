@@ -303,7 +303,7 @@ def run_ours(a):
             "data": "synthetic (seeded manifold states, random-init paper-shape MLP weights)",
             "config": {"workload": f"{cfg.name}: {cfg.note}", "cells_per_gpu": int(n), "cells_total": int(total_cells),
                        "mech": cfg.mech, "hidden": list(cfg.hidden), "nets": nets, "parallelism": f"cells dp{world}",
-                       "l2": "working set > L2 (activations of 131072-cell chunks x 8 nets ~5 GB; "
+                       "l2": "working set > L2 (h2 of 262144-cell chunks x 8 nets 3.4 GB, z 32 MB; "
                              "cell state 0.2 GB) - no flush needed",
                        "precision": a.precision},
             "roofline": {"kernel": ("fused L1+L2 (z -> h1 1600 on chip -> h2 800, tcgen05 bf16, 4-CTA clusters)"

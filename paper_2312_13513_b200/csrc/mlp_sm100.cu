@@ -32,12 +32,14 @@
 namespace {
 
 constexpr int BM = 128;       // UMMA M (one CTA, cta_group::1)
-// cells per chunk (the activation working set: ~39 KB per cell for the paper MLP in bf16, 5 GB at
-// 131072 cells; larger chunks amortise the per-chunk prologue/epilogue launches and tails)
+// cells per chunk (the activation working set: h2 = 12.8 KB per cell for the paper MLP in bf16 on
+// the fused path, 3.4 GB at 262144 cells; the layer-wise path adds h1).  Larger chunks amortise the
+// per-chunk launches and persistent-grid tails: 262144 measured +1.5% over 131072 on C2
+// (tools/capsweep.sh); 524288 no further gain
 int max_cap() {
   static int v = [] {
-    const char *e = getenv("RC_MAX_CAP");  // experiments (tools/capvar.sh)
-    int x = e ? atoi(e) : 131072;
+    const char *e = getenv("RC_MAX_CAP");  // experiments (tools/capsweep.sh)
+    int x = e ? atoi(e) : 262144;
     return x < 256 ? 256 : x / 256 * 256;
   }();
   return v;
@@ -378,6 +380,12 @@ struct WsLayout {
 
 // z (the layer-1 A operand) is held for all `ncells` cells (one prologue launch per call; 32 B per
 // cell in bf16), the activations and partial outputs for one chunk of `cap` cells
+// the fused layer-1/2 kernel runs (bf16, paper widths, not disabled by RC_NO_FUSE=1): no h1 buffer
+bool fused_path(const rc_mlp *n) {
+  const char *nf = getenv("RC_NO_FUSE");
+  return n->precision == RC_BF16 && l12_supported(n->h1, n->h2, n->kpad1) && !(nf && nf[0] == '1');
+}
+
 WsLayout ws_layout(const rc_mlp *n, int cap, int64_t ncells) {
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   WsLayout L;
@@ -388,7 +396,7 @@ WsLayout ws_layout(const rc_mlp *n, int cap, int64_t ncells) {
   const size_t eb = n->precision == RC_BF16 ? 2 : 4, nc = n->precision == RC_TF32X3 ? 2 : 1;
   const size_t zrows = (size_t)((ncells + 255) / 256 * 256);
   L.z = o; o = al(o + nc * zrows * n->kpad1 * eb);
-  L.h1 = o; o = al(o + nc * (size_t)n->n_nets * cap * n->h1 * eb);
+  L.h1 = o; o = al(o + (fused_path(n) ? 0 : nc * (size_t)n->n_nets * cap * n->h1 * eb));
   L.h2 = o; o = al(o + nc * (size_t)n->n_nets * cap * n->h2 * eb);
   const int np3 = 4 * (n->h3 / l2_pass_width(n->h3));  // partial dots per row: 4 column quarters per pass
   L.opart = o; o = al(o + (size_t)n->n_nets * np3 * cap * 4);
@@ -595,8 +603,7 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
     a3[3] = a2[3];  // unused by the dot epilogue
   }
   // fused layers 1+2 (bf16, paper widths); RC_NO_FUSE=1 forces the layer-wise path (tests, comparisons)
-  const char *nf = getenv("RC_NO_FUSE");
-  const bool fused = prec == 0 && l12_supported(n->h1, n->h2, KZ) && !(nf && nf[0] == '1');
+  const bool fused = fused_path(n);
   CUtensorMap m12[7], m12p[7];
   if (fused && ((rc = make_map(&m12[0], z, KZ, cap, 1, BM, KZ, EB)) ||
                 (rc = make_map_w1_groups(&m12[1], n->d_W1, KZ, n->h1, nets)) ||
