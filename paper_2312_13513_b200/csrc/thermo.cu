@@ -35,7 +35,7 @@ __device__ __forceinline__ void warp_max_T(double *dst, double T) {
 }
 
 template <int NS, bool UNIFORM>
-__global__ void __launch_bounds__(256) thermo_kernel(const double *__restrict__ tab, int ns_rt, CellsDev c) {
+__global__ void __launch_bounds__(256, 4) thermo_kernel(const double *__restrict__ tab, int ns_rt, CellsDev c) {
   extern __shared__ __align__(16) double s_tab[];
   __shared__ __align__(8) uint64_t bar;
   const int ns = NS ? NS : ns_rt;

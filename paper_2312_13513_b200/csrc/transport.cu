@@ -28,7 +28,7 @@ __device__ __forceinline__ double poly5(const double *c, double L) {
 }
 
 template <int NS>
-__global__ void __launch_bounds__(128) transport_kernel(const double *__restrict__ tab, int ns_rt, CellsDev c) {
+__global__ void __launch_bounds__(128, NS == 9 ? 4 : 1) transport_kernel(const double *__restrict__ tab, int ns_rt, CellsDev c) {
   extern __shared__ __align__(16) double s_tab[];
   __shared__ __align__(8) uint64_t bar;
   const int ns = NS ? NS : ns_rt;
