@@ -309,3 +309,26 @@ def test_sub_batches_in_place_and_combined_reductions():
     assert r[0] == whole["red"][0]
     assert r[1] == pytest.approx(whole["red"][1], rel=1e-13)
     assert np.array_equal(diag.cpu().numpy(), whole["diag"])
+
+
+def test_chunking_is_invisible_per_cell():
+    """The MLP runs in chunks sized to the workspace (z for every cell + one chunk of
+    activations): a third of rc_workspace_bytes gives several chunks with a ragged last one.
+    Per-cell outputs are bitwise those of the one-chunk call; below the minimum (z of every
+    cell + a 256-cell chunk) the call fails with RC_EINVAL before any launch."""
+    import paper_2312_13513_b200 as rc
+    n = 65536 + 300
+    c = inputs("C2", begin=0, end=n)
+    G = Gpu("C2")
+    one = G.run(c)
+    full = rc.aligned_workspace(G.mlp, n)
+    part = full[: (full.numel() // 3) // 256 * 256]
+    several = G.run(c, ws=part)
+    for k in ("T", "cp", "rho", "mu", "lambda", "qdot"):
+        assert np.array_equal(several[k], one[k]), k
+    for k in ("D", "wdot", "o"):
+        assert np.array_equal(several[k], one[k]), k
+    assert several["red"][1] == pytest.approx(one["red"][1], rel=1e-12)
+    with pytest.raises(rc.RcError) as e:
+        G.run(c, ws=full[: 1 << 20])
+    assert e.value.code == rc._rc.RC_EINVAL
