@@ -31,7 +31,7 @@ struct L2Args {
 // maps: {z (KZ x 128 rows), W1 (KZ x 16 rows), W2 piece 1 (32 x 128 rows), W2 piece 2 (32 x 72 rows),
 //        h2 store (16 x 32), b2 as K = 16 operand piece 1 (16 x 128 rows), piece 2 (16 x 72 rows)}
 struct L12Args {
-  int m_tiles, nets, chunks, N, stages, lead_in;
+  int m_tiles, nets, chunks, N, stages;
   const float *bias;  // b2 [nets][N]
 };
 bool l12_supported(int h1, int h2, int kz);

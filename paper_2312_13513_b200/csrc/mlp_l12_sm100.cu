@@ -3,34 +3,28 @@
 //
 //   h2 = GELU( GELU(z W1^T) W2^T + b2 )      (W1 stored halved, b1 folded, as in layer 1)
 //
-// A cluster of four CTAs = two CTA pairs owns a 256-cell row block.  Pair p
-// computes the layer-2 outputs of pass p (400 of the 800 columns) with the
-// cta_group::2 GEMM of the layer-2 kernel (M = 256, N = 256 + 144, K chunks of
-// 64).  Both pairs need every 64-column chunk of h1 for all 256 rows, so each
-// pair produces half of it: pair p computes columns [32p, 32p + 32) of the chunk
-// (a cta_group::2 MMA, M = 256, N = 32, K = 16/32, into a double-buffered TMEM
-// accumulator), eight epilogue warps per CTA apply GELU and write the 128 x 32
-// bf16 half-chunk into the CTA's A slot, and a forwarder thread copies it with
-// one 8 KB DSMEM bulk copy into the same slot of the CTA with the same rows in
-// the other pair.  Each A slot is therefore [half-chunk 0 | half-chunk 1], both
-// 64-byte-swizzled [128 rows][32 cols] tiles, which is how the layer-2 MMAs read
-// it (K steps 0-1 from the first half, 2-3 from the second).
-//
-// Per CTA and chunk period this costs on average 4096 GELUs (256 clk of MUFU)
-// against 800 clk of layer-2 MMA, instead of a separate layer-1 pass writing and
-// then re-reading 3.2 KB of h1 per cell and net.
+// A cluster of four CTAs = two CTA pairs owns a 256-cell row block.  Pair p computes the
+// layer-2 outputs of pass p (400 of the 800 columns) with the cta_group::2 GEMM of the layer-2
+// kernel (M = 256, N = 256 + 144, K chunks of 64).  Both pairs need every 64-column chunk of h1
+// for all 256 rows, so the pairs take turns: chunk c is produced by pair c % 2 (a cta_group::2
+// M = 256, N = 64, K = KZ layer-1 MMA into a 64-column TMEM accumulator; eight producer warps per
+// CTA apply GELU and write the 128 x 64 bf16 chunk, 128-byte swizzled, into the CTA's A slot) and
+// a copier thread sends it with one 16 KB DSMEM bulk copy into the same slot of the CTA with the
+// same rows in the other pair.  Per CTA and chunk period this costs on average 4096 GELUs (256
+// clk of MUFU) against ~900 clk of layer-2 MMA, instead of a separate layer-1 pass writing and
+// then re-reading 3.2 KB of h1 per cell and net.  DESIGN.md 6.1 has the measured timeline.
 //
 // Barriers (per CTA; "leader" = even CTA of a pair, which issues the MMAs):
-//   full/empty[S]   W2 + W1 stages (pair TMA, leader counts both CTAs' bytes)
-//   zfull/zempty[2] z tile of the row block (pair TMA)
-//   a1full/a1empty[2] layer-1 accumulators (commit -> pair; 16 producer warps of the pair)
-//   own[R]          this CTA's half-chunk written (8 local producer warps)
-//   peer[R]         the other pair's half-chunk arrived (DSMEM bulk copy, 8 KB)
-//   afull[R]        slot complete in both CTAs of the pair (2 forwarders -> leader)
-//   aempty[R]       slot consumed by both pairs (commit multicast to all four CTAs)
-//   c2full/c2empty  layer-2 accumulator, bfull/bempty the b2 slice (as the layer-2 kernel)
-// Warps: 0..15 epilogue (0..7 also produce h1), 16 TMA producer, 17 layer-2 MMA
-// issuer, 18 half-chunk copier, 19 layer-1 MMA issuer (even CTA) / forwarder (odd CTA).
+//   ready[R]        chunk g's W2 stage and A slot g % R complete (leader: both CTAs' W2 bytes,
+//                   the slot's writer (own copier or incoming copy bytes), the odd forwarder)
+//   freed[R]        both pairs' layer-2 MMAs of the chunk done (commit multicast to all four CTAs)
+//   own[R]          the 8 local producer warps wrote this pair's chunk
+//   zfull/zempty[2] z tile + b2 operand tile of a tile (pair TMA; prefetched half a tile ahead)
+//   a1full/a1empty  layer-1 accumulator (commit -> pair; 16 producer warps of the pair)
+//   w1full/w1empty  this CTA's W1 rows of a net
+//   c2full, c2empty/c2emptyB  layer-2 accumulator, released in two pieces by the drain warps
+// Warps: 0..7 h1 producers, 8..15 acc2 drain, 16 TMA producer, 17 layer-2 MMA issuer,
+// 18 chunk copier, 19 layer-1 MMA issuer (even CTA) / slot forwarder (odd CTA).
 #include <cuda_bf16.h>
 
 #include <cstdio>
@@ -474,12 +468,6 @@ int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
   const size_t smem = 1024 + R * (SLOT + STAGE) + 2 * Z_AL + w1 + (NEPI - NPROD) * 2 * 1024 + 2 * 7168 + 4096 + 1024;
   if (smem > 232448) return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel: shared memory");
   a.stages = R;
-  static int li = -1;
-  if (li < 0) {
-    const char *e = getenv("RC_L12_LEADIN");  // experiments (tools/l12var.sh)
-    li = e ? atoi(e) : R;
-  }
-  a.lead_in = li < 0 ? 0 : (li > R ? R : li);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(l12_kernel<KZ, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);

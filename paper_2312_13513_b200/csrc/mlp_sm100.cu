@@ -659,7 +659,7 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
       // layers 1+2 in one kernel: h1 stays on chip.  Default: clusters of two CTA pairs that share
       // h1 chunks (132 SMs); RC_L12_PAIR=1: one CTA pair per (row block, net, pass) with h1
       // recomputed per pass (all 148 SMs; measured 13% slower)
-      L12Args g12{mt, nets, n->h1 / 64, n->h2, 0, 0, n->d_b2};
+      L12Args g12{mt, nets, n->h1 / 64, n->h2, 0, n->d_b2};
       if ((rc = pairk ? launch_l12p(KZ, m12p, g12, s) : launch_l12(KZ, m12, g12, s))) return rc;
     } else {
       // layer 1: h1 = GELU(z W1^T) (b1 folded into z's constant-1 columns)
