@@ -23,6 +23,8 @@ done
 RC_NO_FUSE=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"l1_kernel|l2_pair_kernel" -s 4 -c 2 \
   -o $O/prof_layerwise_$TAG -f python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_layerwise_$TAG.log 2>&1
 echo "ncu layer-wise rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"thermo_kernel" -s 1 -c 1 \
+  -o $O/prof_thermo_$TAG -f python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_thermo_$TAG.log 2>&1; echo "ncu thermo rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"thermo_kernel|transport_kernel|chem_epilogue|prologue" -s 2 -c 4 \
   -o $O/prof_fp64_$TAG -f python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_fp64_$TAG.log 2>&1; echo "ncu fp64 rc=$?"
 ls -la $O | tail -20
