@@ -70,6 +70,11 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
                const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ CUtensorMap mapBa,
                const __grid_constant__ CUtensorMap mapBb, L12Args a) {
   constexpr uint32_t Z_BYTES = 128 * KZ * 2, W1_CH = 32 * KZ * 2;  // W1: 32 rows per CTA and chunk
+  // KZ = 16: this CTA's W1 rows of all its pair's chunks of a net (13 KB, one 5D box per net);
+  // KZ = 32 (CH4): a 4-deep ring of per-chunk W1 rows (8 KB instead of 26 KB, so the W2/A ring
+  // stays 4 deep)
+  constexpr bool W1RING = KZ == 32;
+  constexpr int RW = 4;
   constexpr uint32_t STAGE_BYTES = W2T;                             // TMA bytes per CTA
   constexpr uint32_t BK_BYTES = (NP / 2) * 32, BK_AL = 7168;        // b2 as a K = 16 operand: 200 rows x 32 B
   constexpr uint32_t STAGE = (W2T + 1023u) & ~1023u;                // layout size
@@ -83,7 +88,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
   uint8_t *sA = sW + S * STAGE;              // R x SLOT
   uint8_t *sZ = sA + R * SLOT;               // 2 x Z_BYTES
   uint8_t *sW1 = sZ + 2 * ((Z_BYTES + 1023u) & ~1023u);  // this CTA's W1 rows of its pair's chunks of the net
-  uint8_t *sST = sW1 + ((((a.chunks + 1) / 2) * W1_CH + 1023u) & ~1023u);  // 8 drain warps x 2 x 1 KB h2 staging
+  uint8_t *sST = sW1 + (W1RING ? RW * W1_CH : ((((a.chunks + 1) / 2) * W1_CH + 1023u) & ~1023u));  // 8 drain warps x 2 x 1 KB h2 staging
   uint8_t *sBK = sST + (NEPI - NPROD) * 2 * 1024;  // 2 x b2 operand tile (with the z tile of the same buffer)
   uint8_t *sOnes = sBK + 2 * BK_AL;                // 128 rows x 16 bf16 ones: the A side of the b2 MMA
   uint64_t *bar = reinterpret_cast<uint64_t *>(sOnes + 4096);
@@ -92,8 +97,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
   //   slot i (chunks of this pair).  freed[i]: both pairs consumed chunk i's slot and stage.
   uint64_t *ready = bar, *freed = ready + R, *zfull = freed + R, *zempty = zfull + 2, *a1full = zempty + 2,
            *a1empty = a1full + NA1, *own = a1empty + NA1, *c2full = own + R, *c2empty = c2full + 1,
-           *c2emptyB = c2empty + 1, *w1full = c2emptyB + 1, *w1empty = w1full + 1;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(w1empty + 1);
+           *c2emptyB = c2empty + 1, *w1full = c2emptyB + 1, *w1empty = w1full + RW;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(w1empty + RW);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = rcx::cluster_rank();
@@ -113,8 +118,10 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
       rcx::mbar_init(&freed[r], 2);
       rcx::mbar_init(&own[r], NPROD);
     }
-    rcx::mbar_init(w1full, 2);
-    rcx::mbar_init(w1empty, 1);
+    for (int j = 0; j < RW; ++j) {
+      rcx::mbar_init(&w1full[j], 2);
+      rcx::mbar_init(&w1empty[j], 1);
+    }
     for (int z = 0; z < 2; ++z) {
       rcx::mbar_init(&zfull[z], 2);
       rcx::mbar_init(&zempty[z], 1);
@@ -164,9 +171,24 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
         TR(5, it, 1);
       };
       if (cl < total) load_zb(cl, 0);
+      // W1RING: this CTA's rows of the pair's own chunks (c % 2 == pr), loaded up to 6 global chunks
+      // ahead of the W2 stream (the ring entry of own chunk k is released by its layer-1 MMA)
+      const uint32_t nchunks = (uint32_t)(cl < total ? (total - 1 - cl) / ncl + 1 : 0) * C;
+      uint32_t wg = (uint32_t)pr, nwr = 0;  // next own chunk (global index), own W1 loads issued
+      auto load_w1_upto = [&](uint32_t gmax) {
+        for (; wg <= gmax && wg < nchunks; ++nwr) {
+          const int wt = cl + (int)(wg / C) * ncl, wc = (int)(wg % C);
+          const int j = (int)(nwr % RW);
+          rcx::mbar_wait_sleep(&w1empty[j], ((nwr / RW) & 1) ^ 1);
+          rcx::mbar_arrive_expect_tx_cluster(w1full0 + j * 8, W1_CH);
+          rcx::tma_load_3d_pair(sW1 + j * W1_CH, &mapW1, &w1full[j], 0, wc * 64 + prank * 32, wt / pairs);
+          // next own chunk: c + 2 in the tile, else the first own chunk of the next tile
+          wg = (wc + 2 < C) ? wg + 2 : (wg / C + 1) * C + (uint32_t)pr;
+        }
+      };
       for (int tile = cl; tile < total; tile += ncl, ++it) {
         const int net = tile / pairs;
-        if (net != cur_net) {  // this CTA's W1 rows of all chunks of the new net (one 5D box)
+        if (!W1RING && net != cur_net) {  // this CTA's W1 rows of all chunks of the new net (one 5D box)
           rcx::mbar_wait_sleep(w1empty, (nw & 1) ^ 1);
           rcx::mbar_arrive_expect_tx_cluster(w1full0, ((C + 1) / 2) * W1_CH);
           rcx::tma_load_5d_pair(sW1, &mapW1, w1full, 0, 0, pr * 2 + prank, 0, net);  // rows c*64 + 32 prank, c%2 == pr
@@ -175,6 +197,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
         }
         for (int c = 0; c < C; ++c, ++g) {
           const int s = (int)(g % S);
+          if (W1RING) load_w1_upto(g + 6);
           rcx::mbar_wait_sleep(&freed[s], ((g / S) & 1) ^ 1);
           rcx::mbar_arrive_expect_tx_cluster(ready0 + s * 8, STAGE_BYTES);
           uint8_t *st = sW + s * STAGE;
@@ -193,7 +216,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
       int it = 0, cur_net = -1;
       for (int tile = cl; tile < total; tile += ncl, ++it) {
         const int zb = it & 1, net = tile / pairs;
-        if (net != cur_net) {
+        if (!W1RING && net != cur_net) {
           if (cur_net >= 0 && rcx::elect_one()) rcx::mma_commit_pair_mask(w1empty, pair_mask);  // previous net's W1 done
           __syncwarp();
           rcx::mbar_wait(w1full, nw & 1);
@@ -209,13 +232,16 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           TR(4, it * C + c, 2);
           rcx::mbar_wait(&a1empty[b], ((g / NA1) & 1) ^ 1);
           TR(4, it * C + c, 3);
+          const int j = (int)(g % RW);  // W1RING entry of this own chunk (g counts own chunks)
+          if (W1RING) rcx::mbar_wait(&w1full[j], (g / RW) & 1);
           rcx::tc_fence_after();
-          const uint64_t dw = rcm::desc_sw<KZ * 2>(sW1 + (c >> 1) * W1_CH);
+          const uint64_t dw = rcm::desc_sw<KZ * 2>(W1RING ? sW1 + j * W1_CH : sW1 + (c >> 1) * W1_CH);
           if (rcx::elect_one()) {
 #pragma unroll
             for (int k = 0; k < KZ / 16; ++k)
               rcx::mma_bf16_pair(tmem + TMEM_ACC1 + b * 64, dz + 2 * k, dw + 2 * k, id1, k != 0);
             rcx::mma_commit_pair_mask(&a1full[b], pair_mask);
+            if (W1RING) rcx::mma_commit_pair_mask(&w1empty[j], pair_mask);
           }
           __syncwarp();
         }
@@ -461,10 +487,10 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
 
 template <int KZ>
 int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
-  constexpr int R = KZ == 16 ? 4 : 3;
+  constexpr int R = 4;
   constexpr size_t Z_AL = ((size_t)128 * KZ * 2 + 1023) & ~(size_t)1023;
   constexpr size_t STAGE = ((size_t)W2T + 1023) & ~(size_t)1023;
-  const size_t w1 = ((size_t)((a.chunks + 1) / 2) * 32 * KZ * 2 + 1023) & ~(size_t)1023;
+  const size_t w1 = KZ == 32 ? 4 * (size_t)32 * KZ * 2 : ((size_t)((a.chunks + 1) / 2) * 32 * KZ * 2 + 1023) & ~(size_t)1023;
   const size_t smem = 1024 + R * (SLOT + STAGE) + 2 * Z_AL + w1 + (NEPI - NPROD) * 2 * 1024 + 2 * 7168 + 4096 + 1024;
   if (smem > 232448) return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel: shared memory");
   a.stages = R;

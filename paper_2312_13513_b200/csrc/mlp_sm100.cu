@@ -609,7 +609,8 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   const bool fused = fused_path(n);
   CUtensorMap m12[7], m12p[7];
   if (fused && ((rc = make_map(&m12[0], z, KZ, cap, 1, BM, KZ, EB)) ||
-                (rc = make_map_w1_groups(&m12[1], n->d_W1, KZ, n->h1, nets)) ||
+                (rc = KZ == 32 ? make_map(&m12[1], n->d_W1, KZ, n->h1, nets, 32, KZ, EB)  // per-chunk W1 ring
+                               : make_map_w1_groups(&m12[1], n->d_W1, KZ, n->h1, nets)) ||
                 (rc = make_map(&m12[2], n->d_W2, n->h1, n->h2, nets, 128, 64, EB)) ||
                 (rc = make_map(&m12[3], n->d_W2, n->h1, n->h2, nets, 72, 64, EB)) ||
                 (rc = make_map(&m12[4], h2, n->h2, cap, nets, 32, 16, EB)) ||
