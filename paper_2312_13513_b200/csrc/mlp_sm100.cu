@@ -148,7 +148,7 @@ __device__ __forceinline__ double pow_lambda(double y, double lambda, int n) {
 #define EPI_MINB 4  // 64 registers, 32 warps/SM: C3 epilogue 7.1 -> 4.65 ms (tools/ab_cfg.sh)
 #endif
 template <int NS>
-__global__ void __launch_bounds__(256, NS == 9 ? EPI_MINB : 1) chem_epilogue_kernel(EpiArgs a, CellsDev c) {
+__global__ void __launch_bounds__(256, NS == 9 ? EPI_MINB : NS == 20 ? 2 : 1) chem_epilogue_kernel(EpiArgs a, CellsDev c) {
   constexpr int CAP = NS ? NS : RC_MAX_NS;
   constexpr int UR = NS ? NS : 1;
   const int ns = NS ? NS : a.ns;
