@@ -145,11 +145,13 @@ def local_cells(cfg, rank, world, strong):
     return (np.arange(rank * n, (rank + 1) * n, dtype=np.int64) % n), n * world
 
 
-def algorithmic(cfg, bundle, ns, n):
-    """Per-step algorithmic work: bytes for the HBM-bound
-    stages, FLOPs for the MLP, FP64 flops for transport."""
+def algorithmic(cfg, bundle, ns, n, precision="bf16"):
+    """Per-step algorithmic work: bytes for the HBM-bound stages (the
+    minimum each must move), FLOPs for the MLP, FP64 flops for transport."""
     d, (h1, h2, h3) = bundle["d_in"], bundle["hidden"]
     nets = bundle["n_nets"]
+    eb = {"bf16": 2, "tf32": 4, "tf32x3": 8}[precision]  # MLP activation bytes (tf32x3: hi + lo)
+    kz = 16 if d + 2 <= 16 else 32                          # layer-1 input row (d inputs, 2 bias columns)
     flops_net = 2 * (d * h1 + h1 * h2 + h2 * h3 + h3)
     npair = ns * (ns + 1) // 2
     return {
@@ -161,9 +163,11 @@ def algorithmic(cfg, bundle, ns, n):
         "L2_flops": n * nets * 2 * h1 * h2,
         "L3_flops": n * nets * 2 * (h2 * h3 + h3),
         "mlp_flops": n * nets * flops_net,
-        "L1_bytes": n * nets * h1 * 2,                # h1 activations written (bf16)
-        "epilogue_bytes": n * (3 * 8 + ns * 8 + ns * 8 + 8),
-        "prologue_bytes": n * ((2 + ns) * 8 + 64 * 2),
+        "L1_bytes": n * nets * h1 * eb,               # h1 activations written
+        # in: raw outputs o (fp32 per net), T, rho, Y; out: wdot, qdot
+        "epilogue_bytes": n * (nets * 4 + 2 * 8 + ns * 8 + ns * 8 + 8),
+        # in: T, p, Y; out: the layer-1 input row
+        "prologue_bytes": n * ((2 + ns) * 8 + kz * eb),
     }
 
 
@@ -243,7 +247,7 @@ def run_ours(a):
     if rank == 0:
         pk, pk_src = peaks()
         f64, f64_src = fp64_peak()
-        alg = algorithmic(cfg, bundle, ns, n)
+        alg = algorithmic(cfg, bundle, ns, n, a.precision)
         K = a.steps
 
         def per(stage):
