@@ -67,12 +67,17 @@ __global__ void __launch_bounds__(256) prologue_kernel(ProArgs a, CellsDev c) {
   for (int j = 0; j < 32; ++j) x[j] = 0.f;
   if (r < a.rows) {
     const int64_t i = a.c0 + r;
+    // every load of the cell first (the kernel is HBM-latency bound), then the transforms
+    double yd[30];
+#pragma unroll
+    for (int k = 0; k < 30; ++k)
+      if (k < a.ns) yd[k] = c.Y[k * c.ld + i];
     x[0] = ((float)c.T[i] - a.xmean[0]) * a.xinvstd[0];
     x[1] = ((float)c.p[i] - a.xmean[1]) * a.xinvstd[1];
 #pragma unroll
     for (int k = 0; k < 30; ++k)
       if (k < a.ns) {
-        float y = (float)c.Y[k * c.ld + i];
+        float y = (float)yd[k];
         y = y > 0.f ? y : 0.f;                                       // Y^ = max(Y, 0)
         // Y^^lambda with the MUFU lg2/ex2 (relative error ~1e-7, far below the bf16/tf32 rounding of z)
         float b = 0.f;
