@@ -319,7 +319,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           if ((c & 1) != pr) continue;
           const int slot = (int)(g % R);
           // own[] is indexed by this pair's chunk count (the pair skips every other chunk)
-          rcx::mbar_wait(&own[my % R], (my / R) & 1);  // the local producers wrote the chunk
+          rcx::mbar_wait_sleep(&own[my % R], (my / R) & 1);  // the local producers wrote the chunk
           ++my;
           rcx::mbar_arrive(&ready[slot]);
           uint8_t *src = sA + slot * SLOT;
@@ -337,7 +337,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           const int slot = (int)(g % R);
           const uint32_t par = (g / R) & 1;
           TR(2, g, 0);
-          rcx::mbar_wait(&ready[slot], par);  // the chunk is in this CTA's slot
+          rcx::mbar_wait_sleep(&ready[slot], par);  // the chunk is in this CTA's slot
           TR(2, g, 2);
           rcx::mbar_arrive_cluster(ready_lead + slot * 8);
         }
@@ -356,7 +356,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
       if ((int)((g % C) & 1) != pr) continue;  // the other pair's chunk
       const uint32_t b = lg % NA1, my = lg;
       if (warp == 0) TR(1, g, 0);
-      rcx::mbar_wait(&a1full[b], (lg / NA1) & 1);
+      rcx::mbar_wait_sleep(&a1full[b], (lg / NA1) & 1);
       if (warp == 0) TR(1, g, 1);
       rcx::tc_fence_after();
       uint32_t v[2][16];
@@ -374,7 +374,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
         for (int j = 0; j < 8; ++j)
           pk[h][j] = rcm::gelu_half_bf16x2(cvt_bf16x2(__uint_as_float(v[h][2 * j]), __uint_as_float(v[h][2 * j + 1])));
       const int slot = (int)(g % R);
-      rcx::mbar_wait(&freed[slot], ((g / R) & 1) ^ 1);  // both pairs are done with the slot
+      rcx::mbar_wait_sleep(&freed[slot], ((g / R) & 1) ^ 1);  // both pairs are done with the slot
       if (warp == 0) TR(1, g, 2);
       // columns [32 ph, 32 ph + 32) of the chunk = 16-byte units 4 ph .. 4 ph + 3 of the 128-byte row
       uint8_t *r = sA + slot * SLOT + row * 128;
