@@ -583,7 +583,7 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   const bool tf32 = prec != 0, x3 = prec == 2;
   const int EB = tf32 ? 4 : 2;
   const int RB = x3 ? 64 : 128, KC = RB / EB;  // element bytes; K elements per swizzled operand row
-  const int KATOM = getenv("RC_NO_KTAIL") ? 1 << 20 : tf32 ? 8 : 16;  // K elements per MMA (32 bytes)
+  const int KATOM = tf32 ? 8 : 16;  // K elements per MMA (32 bytes)
   const int nets = n->n_nets;
   // activations: hi copy at the start of each region, X3's lo copy right after it
   uint8_t *z = w + L.z, *h1 = w + L.h1, *h2 = w + L.h2;
