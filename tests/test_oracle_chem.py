@@ -147,3 +147,64 @@ def test_inverse_box_cox_single_net(orc, h2mech):
             dY[s] = (a ** (1 / lam) if a > 0 else 0.0) - Yh[s]
         np.testing.assert_allclose(r["wdot"][:, i], r["rho"][i] * (P @ dY) / b["dt"], rtol=1e-11,
                                    atol=1e-13 * np.abs(r["wdot"][:, i]).max())
+
+
+def _torch_net(b, net):
+    """torch.nn float64 Sequential with net `net`'s weights (GELU MLP)."""
+    d, hid = b["d_in"], b["hidden"]
+    dims = [d, *hid, 1]
+    layers = []
+    for l in range(4):
+        layers.append(torch.nn.Linear(dims[l], dims[l + 1]))
+        if l < 3:
+            layers.append(torch.nn.GELU(approximate="none"))
+    seq = torch.nn.Sequential(*layers).double()
+    W = split_params(b, net)
+    with torch.no_grad():
+        for l in range(4):
+            seq[2 * l].weight.copy_(torch.from_numpy(np.array(W[2 * l])))
+            seq[2 * l].bias.copy_(torch.from_numpy(np.array(W[2 * l + 1])))
+    return seq
+
+
+@pytest.mark.parametrize("hidden,cfg,n", [((64, 32, 16), "C1", 200), ((1600, 800, 400), "C2", 64)])
+def test_step_field_path_matches_torch(orc, h2mech, hidden, cfg, n):
+    """Pins orc_step's own MLP path (dense_t over transposed W1..W3, oracle.c) and the
+    z-score of step 6: the o the GPU is compared
+    against equals torch float64 Linear/GELU(erf) applied to z computed here from the
+    definition x = [T, p, (max(Y,0)^lambda - 1)/lambda], z = (x - mu_x)/sigma_x.
+    A transposed weight index, a dropped /sigma_x or a wrong Box-Cox fails it."""
+    b = make_bundle("h2_9sp", hidden=hidden)
+    om, mlp = orc.Mech(h2mech), orc.Mlp(b)
+    c = make_cells(cfg, 0, n) if cfg == "C1" else make_cells(cfg, 300_000, 300_000 + n)
+    r = orc.step(om, mlp, c["T_true"], c["p"], c["Y"], mode="T", transport=False)
+    lam = b["lambda_bc"]
+    x = np.vstack([c["T_true"][None], c["p"][None], (np.maximum(c["Y"], 0.0) ** lam - 1.0) / lam])   # [d_in][n]
+    z = (x - b["x_mean"][:, None]) / b["x_std"][:, None]
+    assert np.abs(z).max() < 50 and np.abs(z).std() > 0.1          # a real spread of inputs, not a saturated net
+    for net in range(b["n_nets"]):
+        with torch.no_grad():
+            ref = _torch_net(b, net)(torch.from_numpy(np.ascontiguousarray(z.T))).numpy()[:, 0]
+        np.testing.assert_allclose(r["o"][net], ref, rtol=1e-12, atol=1e-13 * np.abs(ref).max())
+
+
+def test_step_zscore_hand_computable(orc, h2mech):
+    """x_mean = cell 0's own x and x_std = 1 make z(cell 0) = 0 exactly, so o(cell 0) =
+    torch(0); x_mean = 0, x_std = 2 make z = x/2 (second point).  Pins the z-score
+    (reading R4) independently of the bundle statistics."""
+    b = make_bundle("h2_9sp", hidden=(64, 32, 16))
+    c = make_cells("C1", 500, 532)
+    lam = b["lambda_bc"]
+    x = np.vstack([c["T_true"][None], c["p"][None], (np.maximum(c["Y"], 0.0) ** lam - 1.0) / lam])
+    om = orc.Mech(h2mech)
+    for xm, xs in ((x[:, 0].copy(), np.ones(b["d_in"])), (np.zeros(b["d_in"]), np.full(b["d_in"], 2.0))):
+        bb = dict(b, x_mean=xm, x_std=xs)
+        r = orc.step(om, orc.Mlp(bb), c["T_true"], c["p"], c["Y"], mode="T", transport=False)
+        z0 = (x[:, 0] - xm) / xs
+        if xs[0] == 1.0:
+            assert np.all(np.abs(z0) <= 1e-12 * np.abs(x[:, 0]))
+            z0 = np.zeros(b["d_in"])
+        for net in (0, 3, 7):
+            with torch.no_grad():
+                ref = _torch_net(bb, net)(torch.from_numpy(z0)[None]).item()
+            assert r["o"][net, 0] == pytest.approx(ref, rel=1e-12, abs=1e-14)
