@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--precision", default="bf16", choices=["bf16", "tf32", "tf32x3"])
     ap.add_argument("--strong", action="store_true", help="partition the config's cells (strong scaling)")
+    ap.add_argument("--layerwise", action="store_true", help="rc_mlp_desc.flags = RC_MLP_LAYERWISE (comparison path)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle baseline")
@@ -190,7 +191,7 @@ def run_ours(a):
     bundle = make_bundle(cfg.mech, hidden=cfg.hidden)
     mech = rc.Mechanism(mech_d)
     prec = {"bf16": rc.RC_BF16, "tf32": rc.RC_TF32, "tf32x3": rc.RC_TF32X3}[a.precision]
-    mlp = rc.MLPBundle(mech, bundle, prec)
+    mlp = rc.MLPBundle(mech, bundle, prec, flags=rc._rc.RC_MLP_LAYERWISE if a.layerwise else 0)
     ns, nets = mech_d["ns"], bundle["n_nets"]
     idx, n_global = local_cells(cfg, rank, world, a.strong)
     n = idx.size
@@ -372,14 +373,18 @@ def run_e2e(a, rc, mech, mlp, bundle, host, st, ws, n, ns, world, stream):
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
     in_done = [torch.cuda.Event() for _ in range(B)]
     cmp_done = [torch.cuda.Event() for _ in range(B)]
-    for e in cmp_done:
+    out_done = [torch.cuda.Event() for _ in range(B)]
+    for e in cmp_done + out_done:
         e.record(stream)
     h2d = sum(t.numel() for _, hin, _ in batches for t in hin.values()) * 8
     d2h = sum(t.numel() for _, _, hout in batches for t in hout.values()) * 8
 
     def step():
         for b, (sb, hin, hout) in enumerate(batches):
-            s_in.wait_event(cmp_done[b])                   # the previous step's compute has read batch b
+            # batch b's buffers are reused: the previous step's compute has read its inputs AND the
+            # previous D2H has read its outputs (T included) before the H2D / compute rewrite them;
+            # compute waits on in_done[b], which is recorded after this wait, so it is ordered too
+            s_in.wait_event(out_done[b])
             with torch.cuda.stream(s_in):
                 sb.h[:nb].copy_(hin["h"], non_blocking=True)
                 sb.T[:nb].copy_(hin["T"], non_blocking=True)
@@ -394,6 +399,7 @@ def run_e2e(a, rc, mech, mlp, bundle, host, st, ws, n, ns, world, stream):
                 for k, v in hout.items():
                     src = getattr(sb, k)
                     v.copy_(src[:nb] if src.dim() == 1 else src[:, :nb], non_blocking=True)
+                out_done[b].record(s_out)
         rc.rc_combine_reductions(red_parts, diag_parts, red, diag, stream)
         reduce_a6(red, diag)
 

@@ -53,6 +53,7 @@ enum {
 
 enum { RC_MODE_H = 0, RC_MODE_T = 1 };               /* rc_cells.mode */
 enum { RC_BF16 = 0, RC_TF32 = 1, RC_TF32X3 = 2 };     /* rc_mlp_desc.precision */
+enum { RC_MLP_LAYERWISE = 1 };                        /* rc_mlp_desc.flags */
 
 /* Diagnostic counters in rc_cells.diag[] (int64, accumulated with atomics). */
 enum {
@@ -118,6 +119,9 @@ typedef struct {
                                      RC_TF32X3: fp32-accurate GEMMs as three tf32 MMAs per product
                                      (a_hi b_hi + a_lo b_hi + a_hi b_lo), activations kept as tf32
                                      hi/lo pairs, exact-erf GELU (gate 1e-3 on o and wdot) */
+  int32_t flags;                  /* 0, or RC_MLP_LAYERWISE: run layers 1 and 2 as separate kernels
+                                     (h1 through the workspace) even where the fused layer-1/2 kernel
+                                     applies -- the comparison path; results agree to rounding */
 } rc_mlp_desc;
 
 int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *desc, rc_mlp **out);

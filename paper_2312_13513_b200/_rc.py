@@ -16,6 +16,7 @@ SO = os.environ.get("RC_LIB") or os.path.join(HERE, "librc_b200.so")  # RC_LIB: 
 RC_OK, RC_EINVAL, RC_ENOMEM, RC_ECUDA, RC_EALIGN, RC_EUNSUPPORTED, RC_EDTMISMATCH = 0, -1, -2, -3, -4, -5, -6
 RC_MODE_H, RC_MODE_T = 0, 1
 RC_BF16, RC_TF32, RC_TF32X3 = 0, 1, 2
+RC_MLP_LAYERWISE = 1
 DIAG_NAMES = ["newton_bisect", "newton_maxit", "nonfinite", "negY_in", "negY_out"]
 
 
@@ -35,7 +36,8 @@ class rc_mech_desc(C.Structure):
 class rc_mlp_desc(C.Structure):
     _fields_ = [("n_nets", C.c_int32), ("hidden", C.c_int32 * 3), ("species_of_net", C.c_void_p),
                 ("params", C.c_void_p), ("x_mean", C.c_void_p), ("x_std", C.c_void_p), ("y_mean", C.c_void_p),
-                ("y_std", C.c_void_p), ("lambda_bc", C.c_double), ("dt", C.c_double), ("precision", C.c_int32)]
+                ("y_std", C.c_void_p), ("lambda_bc", C.c_double), ("dt", C.c_double), ("precision", C.c_int32),
+                ("flags", C.c_int32)]
 
 
 class rc_cells(C.Structure):
@@ -132,13 +134,13 @@ class Mechanism:
 class MLPBundle:
     """rc_mlp handle from a bundle dict (keys of workload.make_bundle)."""
 
-    def __init__(self, mech: Mechanism, b: dict, precision: int = RC_BF16):
+    def __init__(self, mech: Mechanism, b: dict, precision: int = RC_BF16, flags: int = 0):
         self.keep = {k: _np(b[k], np.float64) for k in ["params", "x_mean", "x_std", "y_mean", "y_std"]}
         self.keep["species_of_net"] = _np(b["species_of_net"], np.int32)
         d = rc_mlp_desc(int(b["n_nets"]), (C.c_int32 * 3)(*b["hidden"]), self.keep["species_of_net"].ctypes.data,
                         self.keep["params"].ctypes.data, self.keep["x_mean"].ctypes.data,
                         self.keep["x_std"].ctypes.data, self.keep["y_mean"].ctypes.data,
-                        self.keep["y_std"].ctypes.data, float(b["lambda_bc"]), float(b["dt"]), int(precision))
+                        self.keep["y_std"].ctypes.data, float(b["lambda_bc"]), float(b["dt"]), int(precision), int(flags))
         h = C.c_void_p()
         check(lib().rc_mlp_create(mech.h, C.byref(d), C.byref(h)))
         self.h = h

@@ -8,36 +8,53 @@
 
 namespace rcm {
 
-// GELU, tanh form, packed bf16x2 on the FMA pipe + one MUFU op per pair:
-// 0.5 x (1 + tanh(x (c0 + c1 x^2))), c0 = sqrt(2/pi), c1 = 0.044715 c0.  Its
-// deviation from the oracle's exact-erf GELU (< 1e-3 absolute) is of the order
-// of the bf16 rounding of the activations it produces (MLP numerics).
-__device__ __forceinline__ uint32_t gelu_bf16x2(uint32_t x) {
-  const uint32_t c0 = 0x3F4C3F4Cu;  // bf16(0.7978846) x2
-  const uint32_t c1 = 0x3D123D12u;  // bf16(0.0356774) x2
-  const uint32_t hf = 0x3F003F00u;  // 0.5 x2
-  uint32_t xx, t, u, th, hx, r;
-  asm("mul.rn.bf16x2 %0, %1, %1;" : "=r"(xx) : "r"(x));
-  asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(t) : "r"(xx), "r"(c1), "r"(c0));
-  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(u) : "r"(t), "r"(x));
-  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(th) : "r"(u));
-  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(hx) : "r"(x), "r"(hf));
-  asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(hx), "r"(th), "r"(hx));
+// GELU of the bf16 path, tanh form 0.5 x (1 + tanh(x (c0 + c1 x^2))), c0 = sqrt(2/pi),
+// c1 = 0.044715 c0, evaluated in packed f16x2 arithmetic (one MUFU tanh per element) on the
+// accumulator parked as f16 pairs, then rounded ONCE to bf16.  f16 carries 11 significant bits,
+// so the pre-GELU parking and the GELU arithmetic add ~2^-11 relative error against the 2^-9 of
+// the single bf16 output rounding: measured in emulation (tests/_emulate.py, R17) this
+// sits within 3% of an exact-erf fp32 GELU with one rounding, where the round-1 bf16x2 arithmetic
+// (accumulator rounded to bf16 before GELU, every op in bf16) was 1.3-1.6x the rounding floor.
+// Range: inputs are parked with .satfinite (|x| <= 65504); x^2 or the tanh argument overflowing
+// to +-inf gives tanh = +-1, i.e. GELU = x or 0, the correct limits.
+__device__ __forceinline__ uint32_t cvt_f16x2(float lo, float hi) {  // .satfinite: range guard
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
-// The same GELU applied to y = x/2 (the layer-1 weights are stored halved, which is
-// exact in bf16): x (c0 + c1 x^2) = y (2 c0 + 8 c1 y^2) and 0.5 x (1 + t) = y + y t,
-// so the result equals gelu_bf16x2(2y) bit for bit with one multiply fewer.
-__device__ __forceinline__ uint32_t gelu_half_bf16x2(uint32_t y) {
-  const uint32_t c0 = 0x3FCC3FCCu;  // 2 bf16(0.7978846) x2
-  const uint32_t c1 = 0x3E923E92u;  // 8 bf16(0.0356774) x2
-  uint32_t yy, t, u, th, r;
-  asm("mul.rn.bf16x2 %0, %1, %1;" : "=r"(yy) : "r"(y));
-  asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(t) : "r"(yy), "r"(c1), "r"(c0));
-  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(u) : "r"(t), "r"(y));
-  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(th) : "r"(u));
-  asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(y), "r"(th), "r"(y));
+__device__ __forceinline__ uint32_t f16x2_to_bf16x2(uint32_t v) {  // exact widen, one RNE rounding
+  uint32_t r;
+  asm("{\n\t.reg .f16 l, h;\n\t.reg .f32 fl, fh;\n\tmov.b32 {l, h}, %1;\n\tcvt.f32.f16 fl, l;\n\t"
+      "cvt.f32.f16 fh, h;\n\tcvt.rn.bf16x2.f32 %0, fh, fl;\n}"
+      : "=r"(r) : "r"(v));
   return r;
+}
+// f16x2 pre-activations x -> bf16x2 GELU(x)
+__device__ __forceinline__ uint32_t gelu_f16x2_bf16x2(uint32_t x) {
+  const uint32_t c0 = 0x3A623A62u;  // f16(0.7978846) x2
+  const uint32_t c1 = 0x28912891u;  // f16(0.0356774) x2
+  const uint32_t hf = 0x38003800u;  // 0.5 x2
+  uint32_t xx, t, u, th, hx, r;
+  asm("mul.rn.f16x2 %0, %1, %1;" : "=r"(xx) : "r"(x));
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(t) : "r"(xx), "r"(c1), "r"(c0));
+  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(u) : "r"(t), "r"(x));
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(th) : "r"(u));
+  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(hx) : "r"(x), "r"(hf));
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(hx), "r"(th), "r"(hx));
+  return f16x2_to_bf16x2(r);
+}
+// The same GELU applied to y = x/2 (the layer-1 weights and b1 are stored halved, exact in
+// bf16): x (c0 + c1 x^2) = y (2 c0 + 8 c1 y^2) and 0.5 x (1 + t) = y + y t, one multiply fewer.
+__device__ __forceinline__ uint32_t gelu_half_f16x2_bf16x2(uint32_t y) {
+  const uint32_t c0 = 0x3E623E62u;  // f16(2 * 0.7978846) x2
+  const uint32_t c1 = 0x34913491u;  // f16(8 * 0.0356774) x2
+  uint32_t yy, t, u, th, r;
+  asm("mul.rn.f16x2 %0, %1, %1;" : "=r"(yy) : "r"(y));
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(t) : "r"(yy), "r"(c1), "r"(c0));
+  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(u) : "r"(t), "r"(y));
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(th) : "r"(u));
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(y), "r"(th), "r"(y));
+  return f16x2_to_bf16x2(r);
 }
 // fp32 GELU (same tanh form, MUFU tanh.approx.f32): used where the activation
 // feeds an fp32 reduction directly (layer 3 -> the folded layer-4 dot)

@@ -36,9 +36,6 @@ struct L12Args {
 };
 bool l12_supported(int h1, int h2, int kz);
 int launch_l12(int KZ, const CUtensorMap *maps, const L12Args &a, cudaStream_t s);
-// the same layers on one CTA pair per (row block, net, pass) tile, h1 recomputed per pass
-// (mlp_l12p_sm100.cu); maps as launch_l12 except W1: 3D [nets][h1][KZ], boxes of KZ x 32 rows
-int launch_l12p(int KZ, const CUtensorMap *maps, const L12Args &a, cudaStream_t s);
 
 // maps: {A, B piece 1, B piece 2, out store, A lo, B1 lo, B2 lo, out lo store, bias operand piece 1,
 //        bias operand piece 2} (lo: precision 2 only; bias operand tiles: bf16 only)

@@ -46,7 +46,6 @@ constexpr uint32_t W2T = (NP / 2) * 128;      // W2 chunk tile of one CTA: 200 r
 constexpr uint32_t TMEM_ACC1 = 448;          // acc2 uses [0, 400)
 
 using rcm::cvt_bf16x2;
-using rcm::gelu_bf16x2;
 
 #ifdef L12TRACE  // timing experiment: clock64 stamps of cluster 0, first 64 chunks (tools/l12trace.py)
 // [cta rank][role: 0 MMA, 1 producer warp 0, 2 forwarder, 3 drain (by tile), 4 layer-1 issuer, 5 TMA (by tile)][chunk][event]
@@ -372,7 +371,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
       for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          pk[h][j] = rcm::gelu_half_bf16x2(cvt_bf16x2(__uint_as_float(v[h][2 * j]), __uint_as_float(v[h][2 * j + 1])));
+          pk[h][j] = rcm::gelu_half_f16x2_bf16x2(rcm::cvt_f16x2(__uint_as_float(v[h][2 * j]), __uint_as_float(v[h][2 * j + 1])));
       const int slot = (int)(g % R);
       rcx::mbar_wait_sleep(&freed[slot], ((g / R) & 1) ^ 1);  // both pairs are done with the slot
       if (warp == 0) TR(1, g, 2);
@@ -418,7 +417,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
         for (int h = 0; h < n; ++h)
 #pragma unroll
           for (int j = 0; j < 8; ++j)
-            pk[c + h][j] = cvt_bf16x2(__uint_as_float(v[16 * h + 2 * j]), __uint_as_float(v[16 * h + 2 * j + 1]));
+            pk[c + h][j] = rcm::cvt_f16x2(__uint_as_float(v[16 * h + 2 * j]), __uint_as_float(v[16 * h + 2 * j + 1]));
       };
       // piece 1: two rounds of two 32-column loads in flight
 #pragma unroll
@@ -456,7 +455,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
         if (c < nch) {
           uint32_t gg[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) gg[j] = gelu_bf16x2(pk[c][j]);
+          for (int j = 0; j < 8; ++j) gg[j] = rcm::gelu_f16x2_bf16x2(pk[c][j]);
           uint8_t *stg = stg_base + (nst & 1) * 1024;
           if (lane == 0) rcm::bulk_wait_read1();
           __syncwarp();
@@ -485,18 +484,25 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
   }
 }
 
+constexpr int L12_RING = 4;  // W2 stage / h1 slot ring depth
+// dynamic shared memory of the fused kernel; KZ = 16 keeps the W1 rows of a whole net (grows with h1)
+size_t l12_smem(int KZ, int chunks) {
+  const size_t Z_AL = ((size_t)128 * KZ * 2 + 1023) & ~(size_t)1023;
+  const size_t STAGE = ((size_t)W2T + 1023) & ~(size_t)1023;
+  const size_t w1 = KZ == 32 ? 4 * (size_t)32 * KZ * 2 : ((size_t)((chunks + 1) / 2) * 32 * KZ * 2 + 1023) & ~(size_t)1023;
+  return 1024 + L12_RING * (SLOT + STAGE) + 2 * Z_AL + w1 + (NEPI - NPROD) * 2 * 1024 + 2 * 7168 + 4096 + 1024;
+}
+constexpr size_t L12_SMEM_MAX = 232448;
+
 template <int KZ>
 int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
-  constexpr int R = 4;
-  constexpr size_t Z_AL = ((size_t)128 * KZ * 2 + 1023) & ~(size_t)1023;
-  constexpr size_t STAGE = ((size_t)W2T + 1023) & ~(size_t)1023;
-  const size_t w1 = KZ == 32 ? 4 * (size_t)32 * KZ * 2 : ((size_t)((a.chunks + 1) / 2) * 32 * KZ * 2 + 1023) & ~(size_t)1023;
-  const size_t smem = 1024 + R * (SLOT + STAGE) + 2 * Z_AL + w1 + (NEPI - NPROD) * 2 * 1024 + 2 * 7168 + 4096 + 1024;
-  if (smem > 232448) return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel: shared memory");
+  constexpr int R = L12_RING;
+  const size_t smem = l12_smem(KZ, a.chunks);
+  if (smem > L12_SMEM_MAX) return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel: shared memory");
   a.stages = R;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(l12_kernel<KZ, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaFuncSetAttribute(l12_kernel<KZ, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L12_SMEM_MAX);
     attr = true;
   }
   // persistent grid: only as many clusters of four as can be resident at once (a 4-CTA cluster
@@ -516,7 +522,6 @@ int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
     cfg.numAttrs = 1;
     if (cudaOccupancyMaxActiveClusters(&resident, l12_kernel<KZ, R>, &cfg) != cudaSuccess || resident <= 0)
       resident = mlp_num_sms() / 4;
-    if (getenv("RC_VERBOSE")) fprintf(stderr, "fused layer-1/2 kernel: %d resident clusters of 4\n", resident);
   }
   const int total = a.nets * (a.m_tiles / 2);
   int clusters = resident;
@@ -528,7 +533,12 @@ int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
 
 }  // namespace
 
-bool l12_supported(int h1, int h2, int kz) { return h1 % 64 == 0 && h1 >= 128 && h2 == 2 * NP && (kz == 16 || kz == 32); }
+// decided at create / workspace-sizing time (mlp_sm100.cu fused_path), so a shape the fused kernel
+// cannot hold (e.g. KZ = 16 with h1 >= 2496: the whole-net W1 rows outgrow shared memory) takes the
+// layer-wise path from the start instead of failing after the prologue launch
+bool l12_supported(int h1, int h2, int kz) {
+  return h1 % 64 == 0 && h1 >= 128 && h2 == 2 * NP && (kz == 16 || kz == 32) && l12_smem(kz, h1 / 64) <= L12_SMEM_MAX;
+}
 
 #ifdef L12TRACE
 extern "C" __attribute__((visibility("default"))) int rc_debug_l12trace(void *host) {

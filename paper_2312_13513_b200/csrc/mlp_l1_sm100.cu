@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(L1_THREADS, 1)
           uint32_t pk[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            pk[k] = rcm::gelu_half_bf16x2(rcm::cvt_bf16x2(__uint_as_float(v[c][2 * k]), __uint_as_float(v[c][2 * k + 1])));
+            pk[k] = rcm::gelu_half_f16x2_bf16x2(rcm::cvt_f16x2(__uint_as_float(v[c][2 * k]), __uint_as_float(v[c][2 * k + 1])));
           rcm::stage_sw128(stg, lane, 2 * c, pk);
         }
         rcm::fence_async_smem();
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(L1_THREADS, 1)
           uint32_t pk[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j)
-            pk[j] = rcm::gelu_half_bf16x2(rcm::cvt_bf16x2(__uint_as_float(v[c][2 * j]), __uint_as_float(v[c][2 * j + 1])));
+            pk[j] = rcm::gelu_half_f16x2_bf16x2(rcm::cvt_f16x2(__uint_as_float(v[c][2 * j]), __uint_as_float(v[c][2 * j + 1])));
           rcm::stage_sw128(stg, lane, 2 * c, pk);
         }
       }

@@ -36,16 +36,9 @@ constexpr int BM = 128;       // UMMA M (one CTA, cta_group::1)
 // the fused path, 3.4 GB at 262144 cells; the layer-wise path adds h1).  Larger chunks amortise the
 // per-chunk launches and persistent-grid tails: 262144 measured +1.5% over 131072 on C2
 // (tools/capsweep.sh); 524288 no further gain
-int max_cap() {
-  static int v = [] {
-    const char *e = getenv("RC_MAX_CAP");  // experiments (tools/capsweep.sh)
-    int x = e ? atoi(e) : 262144;
-    return x < 256 ? 256 : x / 256 * 256;
-  }();
-  return v;
-}
-#define MAX_CAP max_cap()
-constexpr int QPART_BLOCKS = 148 * 4;
+// (tools/capsweep.sh varies it through the workspace size: the chunk is the largest that fits)
+constexpr int MAX_CAP = 262144;
+constexpr int QPART_BLOCKS = 1024;  // q-dot block partials (>= the epilogue's resident grid)
 
 
 // ------------------------------------------------------------------ prologue (a3)
@@ -395,10 +388,9 @@ struct WsLayout {
 
 // z (the layer-1 A operand) is held for all `ncells` cells (one prologue launch per call; 32 B per
 // cell in bf16), the activations and partial outputs for one chunk of `cap` cells
-// the fused layer-1/2 kernel runs (bf16, paper widths, not disabled by RC_NO_FUSE=1): no h1 buffer
+// the fused layer-1/2 kernel runs (bf16, widths it holds, not RC_MLP_LAYERWISE): no h1 buffer
 bool fused_path(const rc_mlp *n) {
-  const char *nf = getenv("RC_NO_FUSE");
-  return n->precision == RC_BF16 && l12_supported(n->h1, n->h2, n->kpad1) && !(nf && nf[0] == '1');
+  return n->precision == RC_BF16 && l12_supported(n->h1, n->h2, n->kpad1) && !(n->flags & RC_MLP_LAYERWISE);
 }
 
 WsLayout ws_layout(const rc_mlp *n, int cap, int64_t ncells) {
@@ -617,9 +609,9 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
       return rc;
     a3[3] = a2[3];  // unused by the dot epilogue
   }
-  // fused layers 1+2 (bf16, paper widths); RC_NO_FUSE=1 forces the layer-wise path (tests, comparisons)
+  // fused layers 1+2 (bf16, paper widths); RC_MLP_LAYERWISE forces the layer-wise path (comparisons)
   const bool fused = fused_path(n);
-  CUtensorMap m12[7], m12p[7];
+  CUtensorMap m12[7];
   if (fused && ((rc = make_map(&m12[0], z, KZ, cap, 1, BM, KZ, EB)) ||
                 (rc = KZ == 32 ? make_map(&m12[1], n->d_W1, KZ, n->h1, nets, 32, KZ, EB)  // per-chunk W1 ring
                                : make_map_w1_groups(&m12[1], n->d_W1, KZ, n->h1, nets)) ||
@@ -629,12 +621,6 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
                 (rc = make_map(&m12[5], n->d_b2k, 16, n->h2, nets, 128, 16, EB)) ||
                 (rc = make_map(&m12[6], n->d_b2k, 16, n->h2, nets, 72, 16, EB))))
     return rc;
-  const char *pe = getenv("RC_L12_PAIR");
-  const bool pairk = pe && pe[0] == '1';
-  if (fused) {
-    for (int k = 0; k < 7; ++k) m12p[k] = m12[k];
-    if ((rc = make_map(&m12p[1], n->d_W1, KZ, n->h1, nets, 32, KZ, EB))) return rc;
-  }
   if (!x3) {  // the lo slots are never read: any valid map
     for (int k = 0; k < 3; ++k) m1[3 + k] = m1[k];
     for (int k = 0; k < 4; ++k) m2[4 + k] = m2[k], m3[4 + k] = m3[k];
@@ -669,14 +655,11 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
       if (x3 && (rc = make_map(&m1[3], zc + zlo, KZ, zr, 1, BM, KZ, EB))) return rc;
       if (!x3) m1[3] = m1[0];
       if (fused && (rc = make_map(&m12[0], zc, KZ, zr, 1, BM, KZ, EB))) return rc;
-      if (fused) m12p[0] = m12[0];
     }
     if (fused) {
-      // layers 1+2 in one kernel: h1 stays on chip.  Default: clusters of two CTA pairs that share
-      // h1 chunks (132 SMs); RC_L12_PAIR=1: one CTA pair per (row block, net, pass) with h1
-      // recomputed per pass (all 148 SMs; measured 13% slower)
+      // layers 1+2 in one kernel: h1 stays on chip; clusters of two CTA pairs share h1 chunks
       L12Args g12{mt, nets, n->h1 / 64, n->h2, 0, n->d_b2};
-      if ((rc = pairk ? launch_l12p(KZ, m12p, g12, s) : launch_l12(KZ, m12, g12, s))) return rc;
+      if ((rc = launch_l12(KZ, m12, g12, s))) return rc;
     } else {
       // layer 1: h1 = GELU(z W1^T) (b1 folded into z's constant-1 columns)
       L1Args g1{mt, (n->h1 + bn1 - 1) / bn1, nets, n->h1, 0, cap};

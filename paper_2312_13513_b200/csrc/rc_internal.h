@@ -58,6 +58,7 @@ struct rc_mech {
 
 struct rc_mlp {
   int n_nets, d_in, h1, h2, h3, precision, ns, device;
+  int flags;                      // rc_mlp_desc.flags (RC_MLP_LAYERWISE)
   int kpad1;                      // padded K of layer 1 (64 bf16 / 32 fp32)
   double lambda_bc, dt;
   int inv_lambda;                 // 1/lambda as an integer power

@@ -6,6 +6,19 @@ import numpy as np
 import oracle
 from workload import CONFIGS, load_mech, make_bundle, make_cells, make_cells_at
 
+# Parity gates (BASELINE.json north_star; R17/R18 for the derived ones)
+FP64_TOL = 1e-10          # thermo / transport / epilogue fp64 outputs, elementwise relative
+BF16_TOL = 2e-2           # bf16 MLP output o, relative Frobenius (north_star)
+TF32_TOL = 1e-3           # TF32 MLP output o (north_star: "relative 1e-3 of the output norm")
+# wdot / qdot: an MLP that does nothing but round its operands (bf16 or tf32 RNE, fp32 accumulate,
+# exact GELU; tests/_emulate.py) already reaches wdot 1.9-2.0e-2 (bf16) and 1.1-1.3e-3 (tf32) on
+# the C2 parity samples: the O2 net's |o| is ~5x below the norm of o with random init weights and
+# dominates wdot.  The derived gates are 1.5x that rounding floor (tests/test_emulation_gates.py
+# re-derives it on CPU); the kernels are also held to EMU_FACTOR x the floor on every sample.
+BF16_DERIVED_TOL = 3e-2
+TF32_DERIVED_TOL = 2e-3
+EMU_FACTOR = 1.5
+
 _cache = {}
 
 
@@ -31,10 +44,10 @@ def inputs(cfg, idx=None, begin=0, end=None):
     return c
 
 
-def run_oracle(cfg, c, chem=True, transport=True, nthreads=0):
+def run_oracle(cfg, c, chem=True, transport=True, nthreads=0, b=None):
     m = mech(CONFIGS[cfg].mech)
     om = oracle.Mech(m)
-    ob = oracle.Mlp(bundle(CONFIGS[cfg].mech, CONFIGS[cfg].hidden)) if chem else None
+    ob = oracle.Mlp(b if b is not None else bundle(CONFIGS[cfg].mech, CONFIGS[cfg].hidden)) if chem else None
     return oracle.step(om, ob, c["T_guess"], c["p"], c["Y"], h=c["h"], transport=transport, chem=chem,
                        nthreads=nthreads)
 
@@ -42,13 +55,13 @@ def run_oracle(cfg, c, chem=True, transport=True, nthreads=0):
 class Gpu:
     """Handles for one config on the current CUDA device."""
 
-    def __init__(self, cfg, precision=0):
+    def __init__(self, cfg, precision=0, b=None):
         import paper_2312_13513_b200 as rc
         self.rc = rc
         self.cfg = cfg
         m = mech(CONFIGS[cfg].mech)
         self.mech = rc.Mechanism(m)
-        b = bundle(CONFIGS[cfg].mech, CONFIGS[cfg].hidden)
+        b = b if b is not None else bundle(CONFIGS[cfg].mech, CONFIGS[cfg].hidden)
         self.mlp = rc.MLPBundle(self.mech, b, precision)
         self.ns = m["ns"]
         self.n_nets = b["n_nets"]

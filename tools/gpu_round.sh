@@ -13,15 +13,15 @@ timeout 900 python bench.py > $O/bench_$TAG.json 2> $O/bench_$TAG.err; echo "ben
 cat $O/bench_$TAG.json; tail -3 $O/bench_$TAG.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_$TAG.csv \
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "ncu list rc=$?"
-# l12_kernel: fused layers 1+2; l2_pair_kernel: layer 3 (DOT); l1_kernel / layer-2 pair: RC_NO_FUSE=1 run
+# l12_kernel: fused layers 1+2; l2_pair_kernel: layer 3 (DOT); l1_kernel / layer-2 pair: bench.py --layerwise run
 for K in l12_kernel l2_pair_kernel; do
   C=1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 2 -c $C \
     -o $O/prof_${K}_$TAG -f python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_${K}_$TAG.log 2>&1
   echo "ncu $K rc=$?"
 done
-RC_NO_FUSE=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"l1_kernel|l2_pair_kernel" -s 4 -c 2 \
-  -o $O/prof_layerwise_$TAG -f python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_layerwise_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"l1_kernel|l2_pair_kernel" -s 4 -c 2 \
+  -o $O/prof_layerwise_$TAG -f python bench.py --layerwise --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_layerwise_$TAG.log 2>&1
 echo "ncu layer-wise rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"thermo_kernel" -s 1 -c 1 \
   -o $O/prof_thermo_$TAG -f python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_thermo_$TAG.log 2>&1; echo "ncu thermo rc=$?"

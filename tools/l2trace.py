@@ -27,7 +27,7 @@ f.restype, f.argtypes = C.c_int, [C.c_void_p]
 print("copy rc", f(buf.ctypes.data))
 for dot, name in ((0, "layer 2"), (1, "layer 3 (dot)")):
     b = buf[dot]
-    if not (b > 0).any():  # layer 2 runs in the fused kernel unless RC_NO_FUSE=1
+    if not (b > 0).any():  # layer 2 runs in the fused kernel unless bench.py --layerwise
         continue
     t0 = b[b > 0].min()
     b = np.where(b > 0, b - t0, -1)
