@@ -21,6 +21,41 @@ int rc_fail(int code, const char *fmt, ...) {
   return code;
 }
 void rc_count_launch(int n) { g_launches += n; }
+
+int rc_sm_count() {
+  static std::mutex mu;
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 1;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+int rc_resident_blocks(const void *kernel, int threads, size_t smem) {
+  struct Key { const void *k; int t; size_t s; int dev; int v; };
+  static std::mutex mu;
+  static std::vector<Key> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    for (const Key &e : cache)
+      if (e.k == kernel && e.t == threads && e.s == smem && e.dev == dev) return e.v;
+  }
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem) != cudaSuccess || per < 1) per = 1;
+  const int v = per * rc_sm_count();
+  std::lock_guard<std::mutex> g(mu);
+  cache.push_back(Key{kernel, threads, smem, dev, v});
+  return v;
+}
 void rc_reset_launches() { g_launches = 0; }
 
 // ---------------------------------------------------------------------------
@@ -166,19 +201,23 @@ extern "C" int rc_mech_create(const rc_mech_desc *d, rc_mech **out) {
     th[ThermoSeg::invW(ns) + k] = 1.0 / m->W[k];
     th[ThermoSeg::tmid(ns) + k] = d->T_mid[k];
   }
-  // transport segment: fits + Wilke constants (W_j/W_k)^(1/4), 1/sqrt(8(1+W_k/W_j))
+  // transport segment: fits (diff rows padded to 6) + the factorised Wilke matrices (rc_internal.h)
   auto &tr = m->transport_host;
   tr.assign(TransportSeg::size(ns), 0.0);
   const int np = ns * (ns + 1) / 2;
   std::memcpy(&tr[TransportSeg::visc(ns)], d->visc, sizeof(double) * 5 * ns);
   std::memcpy(&tr[TransportSeg::cond(ns)], d->cond, sizeof(double) * 5 * ns);
-  std::memcpy(&tr[TransportSeg::diff(ns)], d->diff, sizeof(double) * 5 * np);
+  for (int q = 0; q < np; ++q)
+    for (int j = 0; j < 5; ++j) tr[TransportSeg::diff(ns) + 6 * q + j] = d->diff[5 * q + j];
+  const int nse = TransportSeg::nse(ns);
   for (int k = 0; k < ns; ++k) {
     tr[TransportSeg::W(ns) + k] = m->W[k];
     tr[TransportSeg::invW(ns) + k] = 1.0 / m->W[k];
     for (int j = 0; j < ns; ++j) {
-      tr[TransportSeg::c1(ns) + k * ns + j] = std::sqrt(std::sqrt(m->W[j] / m->W[k]));
-      tr[TransportSeg::c2(ns) + k * ns + j] = 1.0 / std::sqrt(8.0 * (1.0 + m->W[k] / m->W[j]));
+      const double c1 = std::sqrt(std::sqrt(m->W[j] / m->W[k])), c2 = 1.0 / std::sqrt(8.0 * (1.0 + m->W[k] / m->W[j]));
+      tr[TransportSeg::M(ns, 0) + k * nse + j] = c2;
+      tr[TransportSeg::M(ns, 1) + k * nse + j] = 2.0 * c2 * c1;
+      tr[TransportSeg::M(ns, 2) + k * nse + j] = c2 * c1 * c1;
     }
   }
   // element projection P = I - E^T (E E^T)^-1 E, E_ek = a_ek A_e / W_k (R6)

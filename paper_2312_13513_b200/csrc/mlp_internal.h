@@ -23,7 +23,7 @@ struct L2Args {
   int m_tiles, passes, nets, chunks, N, stages;
   const float *bias;       // [nets][N]
   const float *w4;         // layer-3 mode (nullptr: layer 2): [nets][N], layer 4 folded into the epilogue
-  float *opart;            // layer-3 mode: [nets][passes*4][cap] partial dots
+  float *opart;            // layer-3 mode: [nets][passes][cap] dots (column quarters summed in-kernel)
   int cap;
   int ktail;               // MMA K atoms in the last K chunk when K is not a multiple of it (0: full chunk)
 };

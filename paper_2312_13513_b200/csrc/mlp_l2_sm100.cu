@@ -316,6 +316,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     const int g1lo = P1G * sub / 4, n1 = P1G * (sub + 1) / 4 - g1lo;
     const int g2lo = P1G + P2G * sub / 4, n2 = P1G + P2G * (sub + 1) / 4 - g2lo;
     uint8_t *stg_base = sST + warp * 2 * STG;
+    // layer 3 (DOT): the four warps of a lane quadrant (q, q+4, q+8, q+12) each hold the dot over one
+    // column quarter of their 32 rows; they meet at named barrier 1+q and warp sub 0 stores the row
+    // sums ((p0 + p1) + p2) + p3 (fixed order), so the epilogue reads one fp32 per net and row
+    // instead of four.  The reduction buffer [2 tile parities][4][128] floats lives in the store
+    // staging, which the dot epilogue does not use; the barrier of tile t+1 orders sub 0's reads
+    // of parity (t & 1) before any write of tile t+2.
+    auto emit_o = [&](float dot, int it_, int net_, int pass_, int grow_) {
+      float *red = reinterpret_cast<float *>(sST) + (it_ & 1) * 512;
+      red[sub * 128 + q * 32 + lane] = dot;
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + q) : "memory");
+      if (sub == 0) {
+        const float *r = red + q * 32 + lane;
+        a.opart[(size_t)(net_ * a.passes + pass_) * a.cap + grow_ + lane] = ((r[0] + r[128]) + r[256]) + r[384];
+      }
+    };
     uint32_t nst = 0;
     int it = 0;
     for (int tile = cl; tile < total; tile += ncl, ++it) {
@@ -403,7 +418,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
             }
           }
         }
-        if constexpr (DOT) a.opart[((size_t)(net * a.passes + pass) * 4 + sub) * a.cap + grow + lane] = dot;
+        if constexpr (DOT) emit_o(dot, it, net, pass, grow);
       } else {
         // Phase A (no MUFU): every accumulator column of this warp (bias included by the MMA) ->
         // registers as 16-bit pairs: bf16 for layer 2 (the GELU input), f16 for the fp32 layer-3
@@ -460,7 +475,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
               }
             }
           }
-          a.opart[((size_t)(net * a.passes + pass) * 4 + sub) * a.cap + grow + lane] = dot;
+          emit_o(dot, it, net, pass, grow);
         } else {  // layer 2: bf16 GELU -> [32 rows][32 B] staging (32-byte TMA swizzle) -> TMA store
   #pragma unroll
           for (int c = 0; c < MAX1 + MAX2; ++c) {

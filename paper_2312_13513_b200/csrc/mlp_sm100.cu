@@ -27,6 +27,7 @@
 #include "mlp_internal.h"
 #include "ptx.cuh"
 #include "rc_internal.h"
+#include "stream.cuh"
 
 
 namespace {
@@ -52,40 +53,11 @@ struct ProArgs {
   int64_t lo_off;   // elements
 };
 
-__global__ void __launch_bounds__(256) prologue_kernel(ProArgs a, CellsDev c) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= a.rows_pad) return;
-  float x[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) x[j] = 0.f;
-  if (r < a.rows) {
-    const int64_t i = a.c0 + r;
-    // every load of the cell first (the kernel is HBM-latency bound), then the transforms
-    double yd[30];
-#pragma unroll
-    for (int k = 0; k < 30; ++k)
-      if (k < a.ns) yd[k] = c.Y[k * c.ld + i];
-    x[0] = ((float)c.T[i] - a.xmean[0]) * a.xinvstd[0];
-    x[1] = ((float)c.p[i] - a.xmean[1]) * a.xinvstd[1];
-#pragma unroll
-    for (int k = 0; k < 30; ++k)
-      if (k < a.ns) {
-        float y = (float)yd[k];
-        y = y > 0.f ? y : 0.f;                                       // Y^ = max(Y, 0)
-        // Y^^lambda with the MUFU lg2/ex2 (relative error ~1e-7, far below the bf16/tf32 rounding of z)
-        float b = 0.f;
-        if (y > 0.f) {
-          float l2, e2;
-          asm("lg2.approx.f32 %0, %1;" : "=f"(l2) : "f"(y));
-          asm("ex2.approx.f32 %0, %1;" : "=f"(e2) : "f"(a.lambda * l2));
-          b = e2;
-        }
-        x[2 + k] = ((b - 1.f) * a.inv_lambda - a.xmean[2 + k]) * a.xinvstd[2 + k];  // Box-Cox, z-score
-      }
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j == a.d_in || j == a.d_in + 1) x[j] = 1.f;
-  }
+constexpr int PRO_TILE = 256;                 // cells per stage = consumer threads
+constexpr int PRO_THREADS = PRO_TILE + 32;    // + the producer warp (stream.cuh run_ws)
+
+// one z row (d_in transformed inputs, two 1.0 bias columns, zeros) -> bf16 or tf32 (hi[, lo])
+__device__ __forceinline__ void store_z_row(const ProArgs &a, int64_t r, const float (&x)[32]) {
   if (a.tf32) {
     float4 *dst = reinterpret_cast<float4 *>(static_cast<float *>(a.z) + (size_t)r * a.kz);
     float4 *lo = reinterpret_cast<float4 *>(static_cast<float *>(a.z) + a.lo_off + (size_t)r * a.kz);
@@ -115,15 +87,64 @@ __global__ void __launch_bounds__(256) prologue_kernel(ProArgs a, CellsDev c) {
   }
 }
 
+// a3 for every cell of the call: T, p, Y streamed through the TMA tile ring (stream.cuh), one
+// thread per cell writes its z row; rows [rows, rows_pad) of the 256-row tiles are zero
+__global__ void __launch_bounds__(PRO_THREADS) prologue_kernel(ProArgs a, CellsDev c, int stages) {
+  extern __shared__ __align__(16) uint8_t pro_smem[];
+  __shared__ __align__(8) uint64_t bars[16];
+  const rcs::Ring<PRO_TILE> ring{pro_smem, bars, 2 + a.ns, 0, stages};
+  if (threadIdx.x == 0) ring.init(PRO_TILE / 32);
+  __syncthreads();
+  auto src8 = [&](int r) -> const double * {
+    return (r == 0 ? c.T : r == 1 ? c.p : c.Y + (size_t)(r - 2) * c.ld) + a.c0;
+  };
+  auto src4 = [&](int) -> const float * { return nullptr; };
+  ring.run_ws(a.rows, src8, src4, [&](int st, int64_t tile, int jt) {
+    const int64_t r = tile * PRO_TILE + jt;
+    if (r >= a.rows) return;
+    const double *S8 = ring.row8(st, 0) + jt;  // fp64 row q of this cell: S8[q * PRO_TILE]
+    float x[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = 0.f;
+    x[0] = ((float)S8[0] - a.xmean[0]) * a.xinvstd[0];
+    x[1] = ((float)S8[PRO_TILE] - a.xmean[1]) * a.xinvstd[1];
+#pragma unroll
+    for (int k = 0; k < 30; ++k)
+      if (k < a.ns) {
+        float y = (float)S8[(2 + k) * PRO_TILE];
+        y = y > 0.f ? y : 0.f;                                       // Y^ = max(Y, 0)
+        // Y^^lambda with the MUFU lg2/ex2 (relative error ~1e-7, far below the bf16/tf32 rounding of z)
+        float b = 0.f;
+        if (y > 0.f) {
+          float l2, e2;
+          asm("lg2.approx.f32 %0, %1;" : "=f"(l2) : "f"(y));
+          asm("ex2.approx.f32 %0, %1;" : "=f"(e2) : "f"(a.lambda * l2));
+          b = e2;
+        }
+        x[2 + k] = ((b - 1.f) * a.inv_lambda - a.xmean[2 + k]) * a.xinvstd[2 + k];  // Box-Cox, z-score
+      }
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j == a.d_in || j == a.d_in + 1) x[j] = 1.f;
+    store_z_row(a, r, x);
+  });
+  float x0[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) x0[j] = 0.f;
+  for (int64_t r = a.rows + (int64_t)blockIdx.x * PRO_THREADS + threadIdx.x; r < a.rows_pad; r += (int64_t)gridDim.x * PRO_THREADS)
+    store_z_row(a, r, x0);
+}
+
 // ------------------------------------------------------------------ epilogue (a5)
 struct EpiArgs {
   int64_t c0;
-  int rows, cap, n_nets, nparts, inv_lambda, ns;
+  int rows, cap, n_nets, passes, inv_lambda, ns;
   double lambda, inv_dt;
-  const float *opart, *b4;
+  const float *opart, *b4;     // raw net outputs [nets][passes][cap] (column quarters summed by layer 3)
   const double *ymean, *ystd, *P, *thermo;
   const int *species;
   double *qpart;  // [gridDim.x], accumulated across chunks in stream order
+  double binom[17];  // C(n, m), m = 0..n, n = inv_lambda <= 16 (factorised inverse Box-Cox)
 };
 
 __device__ __forceinline__ double ipow(double a, int e) {
@@ -136,105 +157,140 @@ __device__ __forceinline__ double ipow(double a, int e) {
   return r;
 }
 
-// b = y^lambda for 0 < y <= 1 with 1/lambda = n an integer (Box-Cox, R3): fp32 MUFU seed
-// (relative error ~1e-7), then two Newton steps on b^n = y, b <- b + (y / b^(n-1) - b) / n, each
-// squaring the relative error (x (n-1)/2): fp64-converged, ~30 instructions instead of pow()'s ~150.
-// Tiny y (fp32 seed out of range) and non-integer 1/lambda take pow().
-__device__ __forceinline__ double pow_lambda(double y, double lambda, int n) {
-  if (!(y > 0.0)) return 0.0;
-  if (n <= 0 || y < 1e-30) return pow(y, lambda);
-  double b = (double)exp2f((float)lambda * log2f((float)y));
-#pragma unroll
-  for (int it = 0; it < 2; ++it) b = fma(y * rcx::rcp_f64(ipow(b, n - 1)) - b, lambda, b);
-  return b;
+// Inverse Box-Cox increment: dY = Y* - Y^ with Y* = a^n,
+// a = b + lambda Delta, b = Y^^lambda, n = 1/lambda.  In exact arithmetic
+// dY = Y^ ((1 + u)^n - 1) with u = lambda Delta / b (and Y* = 0, dY = -Y^ when a <= 0, i.e.
+// u <= -1), and (1 + u)^n - 1 = sum_{m=1..n} C(n, m) u^m by Horner: the relative error of dY
+// is that of u, i.e. of b, with no cancellation between Y* and Y^ (the "factorised" dY of
+// SURVEY.md §8(a) a5).  b = Y^^lambda: fp32 MUFU seed (~1e-7) + one fp64 Newton step on
+// b^n = Y^ (error x (n-1)/2 squared: ~5e-14).  Tiny Y^ (fp32 seed out of range) and a
+// non-integer or large 1/lambda take the direct pow() form.
+// the general form: Y^ = 0 (b = 0), Y^ below the fp32 seed's range, or 1/lambda not 10
+__device__ __noinline__ double inv_boxcox_dy_general(double ys, double delta, const EpiArgs &a) {
+  const int n = a.inv_lambda;
+  const double ld = a.lambda * delta;
+  if (!(ys > 0.0)) return ld > 0.0 ? (n > 0 ? ipow(ld, n) : pow(ld, 1.0 / a.lambda)) : 0.0;  // b = 0
+  if (n <= 0 || n > 16 || ys < 1e-30) {
+    const double b = pow(ys, a.lambda), ap = b + ld;
+    return (ap > 0.0 ? pow(ap, 1.0 / a.lambda) : 0.0) - ys;
+  }
+  double b = (double)exp2f((float)a.lambda * log2f((float)ys));
+  b = fma(ys * rcx::rcp_f64(ipow(b, n - 1)) - b, a.lambda, b);
+  const double u = ld * rcx::rcp_f64(b);
+  if (u <= -1.0) return -ys;
+  double g = 0.0;
+  for (int m = n; m >= 1; --m) g = fma(g, u, a.binom[m]);
+  return ys * (g * u);
 }
 
-#ifndef EPI_MINB
-#define EPI_MINB 4  // 64 registers, 32 warps/SM: C3 epilogue 7.1 -> 4.65 ms (tools/ab_cfg.sh)
-#endif
+// lambda_BC = 0.1 (R3, n = 10) with Y^ >= 1e-30: MUFU seed, one Newton step, 9-FMA Horner
+__device__ __forceinline__ double inv_boxcox_dy(double ys, double delta, const EpiArgs &a) {
+  if (a.inv_lambda != 10 || !(ys >= 1e-30)) return inv_boxcox_dy_general(ys, delta, a);
+  float l2, e2;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"((float)ys));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e2) : "f"(0.1f * l2));
+  double b = (double)e2;
+  const double b2 = b * b, b4 = b2 * b2, b8 = b4 * b4;
+  b = fma(ys * rcx::rcp_f64(b8 * b) - b, 0.1, b);  // Newton on b^10 = Y^
+  const double u = (a.lambda * delta) * rcx::rcp_f64(b);
+  constexpr double C10[10] = {10.0, 45.0, 120.0, 210.0, 252.0, 210.0, 120.0, 45.0, 10.0, 1.0};
+  double g = C10[9];
+#pragma unroll
+  for (int m = 8; m >= 0; --m) g = fma(g, u, C10[m]);
+  return u <= -1.0 ? -ys : ys * (g * u);
+}
+
+__device__ __forceinline__ double2 lds2_epi(const double *p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(rcx::smem_u32(p)));
+  return v;
+}
+
+constexpr int EPI_TILE = 128;                 // cells per stage = consumer threads
+constexpr int EPI_THREADS = EPI_TILE + 32;    // + the producer warp (stream.cuh run_ws)
+
 template <int NS>
-__global__ void __launch_bounds__(256, NS == 9 ? EPI_MINB : NS == 20 ? 2 : 1) chem_epilogue_kernel(EpiArgs a, CellsDev c) {
+__global__ void __launch_bounds__(EPI_THREADS, NS == 9 ? 3 : NS == 20 ? 2 : 1) chem_epilogue_kernel(EpiArgs a, CellsDev c, int stages) {
   constexpr int CAP = NS ? NS : RC_MAX_NS;
   constexpr int UR = NS ? NS : 1;
+  constexpr int NETUNR = NS == 9 ? 8 : 1;
   const int ns = NS ? NS : a.ns;
-  extern __shared__ __align__(16) double s_tab[];  // thermo segment, then P
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ double red_s[8];
-  const uint32_t tb = (uint32_t)ThermoSeg::size(ns) * 8u, pb = (uint32_t)(((ns * ns + 1) & ~1) * 8);
-  double *sP = s_tab + ThermoSeg::size(ns);
+  const int nn = a.n_nets;
+  extern __shared__ __align__(16) double s_tab[];  // thermo segment | P | P columns by net | species | ring
+  __shared__ __align__(8) uint64_t bars[1 + 16];
+  __shared__ double red_s[EPI_THREADS / 32];
+  const int nse = (ns + 1) & ~1;
+  const int tsz = ThermoSeg::size(ns), psz = (ns * ns + 1) & ~1, pnsz = nn * nse + 32;
+  double *sP = s_tab + tsz, *sPn = sP + psz;
+  int *sSpec = reinterpret_cast<int *>(sPn + nn * nse);
+  const rcs::Ring<EPI_TILE> ring{reinterpret_cast<uint8_t *>(sPn + pnsz), bars + 1, 2 + ns, nn * a.passes, stages};
   if (threadIdx.x == 0) {
-    rcx::mbar_init(&bar, 1);
-    rcx::fence_mbar_init();
+    rcx::mbar_init(&bars[0], 1);
+    ring.init(EPI_TILE / 32);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    rcx::mbar_arrive_expect_tx(&bar, tb + pb);
-    rcx::bulk_g2s(s_tab, a.thermo, tb, &bar);
-    rcx::bulk_g2s(sP, a.P, pb, &bar);
+    rcx::mbar_arrive_expect_tx(&bars[0], (uint32_t)(tsz + psz) * 8u);
+    rcx::bulk_g2s(s_tab, a.thermo, (uint32_t)tsz * 8u, &bars[0]);
+    rcx::bulk_g2s(sP, a.P, (uint32_t)psz * 8u, &bars[0]);
   }
-  rcx::mbar_wait(&bar, 0);
+  // stage rows: fp64 T, rho, Y_0..Y_{ns-1} of the chunk's cells; fp32 raw outputs per (net, pass)
+  auto src8 = [&](int r) -> const double * {
+    return (r == 0 ? c.T : r == 1 ? c.rho : c.Y + (size_t)(r - 2) * c.ld) + a.c0;
+  };
+  auto src4 = [&](int r) -> const float * { return a.opart + (size_t)r * a.cap; };
+  rcx::mbar_wait(&bars[0], 0);
   const double *hlo = s_tab + ThermoSeg::hlo(ns), *hhi = s_tab + ThermoSeg::hhi(ns), *tmid = s_tab + ThermoSeg::tmid(ns);
-  // P with its columns gathered by net: Pn[k][net] = P[k][species[net]] (the other columns multiply
-  // dY = 0), so the per-cell arrays are indexed by unrolled loop counters only (registers)
-  double *sPn = sP + ((ns * ns + 1) & ~1);
-  const int nn = a.n_nets;
-  for (int e = threadIdx.x; e < ns * nn; e += blockDim.x) sPn[e] = sP[(e / nn) * ns + a.species[e % nn]];
+  // the columns of P gathered by net and stored contiguously: Pn[net][k] = P[k][species[net]]
+  // (the other columns multiply dY = 0), padded to an even length for 16-byte loads
+  for (int e = threadIdx.x; e < nn * nse; e += blockDim.x) {
+    const int net = e / nse, k = e % nse;
+    sPn[e] = k < ns ? sP[k * ns + a.species[net]] : 0.0;
+  }
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) sSpec[e] = a.species[e];
   __syncthreads();
 
   double qsum = 0.0;
   int n_negout = 0, n_bad = 0;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < a.rows; r += gridDim.x * blockDim.x) {
+  ring.run_ws(a.rows, src8, src4, [&](int st, int64_t tile, int jt) {
+    const int r = (int)(tile * EPI_TILE) + jt;
+    if (r >= a.rows) return;
     const int64_t i = a.c0 + r;
-    const double T = c.T[i], rho = c.rho[i];
-    double Yh[CAP];
+    const double *S8 = ring.row8(st, 0) + jt;  // fp64 row q of this cell: S8[q * EPI_TILE]
+    const float *S4 = ring.row4(st, 0) + jt;
+    const double T = S8[0], rho = S8[EPI_TILE];
+    // net loop: dY of net's species (inverse Box-Cox), accumulated straight into the projection
+    // v = P dY as an outer product with column `species[net]` of P (species without a net
+    // contribute 0); the loop stays rolled for large mechanisms (instruction-cache footprint)
+    double v[CAP];
 #pragma unroll UR
     for (int k = 0; k < CAP; ++k)
-      if (k < ns) {
-        double y = c.Y[k * c.ld + i];
-        Yh[k] = y > 0.0 ? y : 0.0;
-      }
-    // all raw outputs of the cell first (independent loads in flight), then the transforms
-    constexpr int MAXNET = CAP;
-    float of[MAXNET];
-    double dY[MAXNET];  // by net
+      if (k < ns) v[k] = 0.0;
+#pragma unroll NETUNR
+    for (int net = 0; net < nn; ++net) {
+      float o = a.b4[net];
+      for (int ps = 0; ps < a.passes; ++ps) o += S4[(net * a.passes + ps) * EPI_TILE];
+      if (c.o) c.o[net * c.ld + i] = o;
+      const double y = S8[(2 + sSpec[net]) * EPI_TILE];
+      const double dy = inv_boxcox_dy(y > 0.0 ? y : 0.0, (double)o * a.ystd[net] + a.ymean[net], a);
+      const double *pc = sPn + net * nse;  // column species[net] of P, contiguous in k
 #pragma unroll UR
-    for (int net = 0; net < MAXNET; ++net)
-      if (net < nn) {
-        const float *op = a.opart + (size_t)net * a.nparts * a.cap + r;
-        float v = a.b4[net];
-        if (a.nparts == 4) {
-          v += op[0];
-          v += op[(size_t)a.cap];
-          v += op[2 * (size_t)a.cap];
-          v += op[3 * (size_t)a.cap];
-        } else {
-          for (int p = 0; p < a.nparts; ++p) v += op[(size_t)p * a.cap];
+      for (int k = 0; k < CAP; k += 2)
+        if (k < ns) {
+          const double2 pp = lds2_epi(pc + k);
+          v[k] = fma(pp.x, dy, v[k]);
+          if (k + 1 < ns) v[k + 1] = fma(pp.y, dy, v[k + 1]);
         }
-        of[net] = v;
-      }
-#pragma unroll UR
-    for (int net = 0; net < MAXNET; ++net)
-      if (net < nn) {
-        if (c.o) c.o[net * c.ld + i] = of[net];
-        const double y = __ldg(c.Y + (size_t)a.species[net] * c.ld + i);  // L1 hit: loaded above
-        const double ys = y > 0.0 ? y : 0.0;
-        const double b = pow_lambda(ys, a.lambda, a.inv_lambda);     // b_s = Y^_s^lambda
-        const double ap = b + a.lambda * ((double)of[net] * a.ystd[net] + a.ymean[net]);
-        const double ystar = ap > 0.0 ? ipow(ap, a.inv_lambda) : 0.0;  // inverse Box-Cox
-        dY[net] = ystar - ys;
-      }
-    // element projection dY <- P dY (fp64, species without a net contribute 0), sources
+    }
+    // sources
     double q = 0.0;
     bool neg = false, bad = false;
 #pragma unroll UR
     for (int k = 0; k < CAP; ++k)
       if (k < ns) {
-        double v = 0.0;
-#pragma unroll UR
-        for (int net = 0; net < MAXNET; ++net)
-          if (net < nn) v = fma(sPn[k * nn + net], dY[net], v);
-        neg |= (Yh[k] + v) < 0.0;
-        const double w = rho * v * a.inv_dt;
+        const double y = S8[(2 + k) * EPI_TILE];
+        neg |= ((y > 0.0 ? y : 0.0) + v[k]) < 0.0;
+        const double w = rho * v[k] * a.inv_dt;
         c.wdot[k * c.ld + i] = w;
         const double *h = (T <= tmid[k]) ? hlo + 6 * k : hhi + 6 * k;
         const double hk = fma(T, fma(T, fma(T, fma(T, fma(T, h[4], h[3]), h[2]), h[1]), h[0]), h[5]);
@@ -246,7 +302,7 @@ __global__ void __launch_bounds__(256, NS == 9 ? EPI_MINB : NS == 20 ? 2 : 1) ch
     qsum += q;
     n_negout += neg;
     n_bad += bad;
-  }
+  });
   if (c.diag) {
     unsigned v1 = __reduce_add_sync(0xffffffffu, (unsigned)n_negout);
     unsigned v2 = __reduce_add_sync(0xffffffffu, (unsigned)n_bad);
@@ -369,16 +425,7 @@ int make_map_w1_groups(CUtensorMap *m, const void *W1, int KZ, int h1, int nets)
 }
 
 }  // namespace
-int mlp_num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int mlp_num_sms() { return rc_sm_count(); }
 namespace {
 
 struct WsLayout {
@@ -405,7 +452,7 @@ WsLayout ws_layout(const rc_mlp *n, int cap, int64_t ncells) {
   L.z = o; o = al(o + nc * zrows * n->kpad1 * eb);
   L.h1 = o; o = al(o + (fused_path(n) ? 0 : nc * (size_t)n->n_nets * cap * n->h1 * eb));
   L.h2 = o; o = al(o + nc * (size_t)n->n_nets * cap * n->h2 * eb);
-  const int np3 = 4 * (n->h3 / l2_pass_width(n->h3));  // partial dots per row: 4 column quarters per pass
+  const int np3 = n->h3 / l2_pass_width(n->h3);  // raw outputs per row: one per layer-3 pass
   L.opart = o; o = al(o + (size_t)n->n_nets * np3 * cap * 4);
   L.total = o;
   return L;
@@ -563,6 +610,36 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
   return RC_OK;
 }
 
+namespace {
+double binom(int n, int m) {
+  double r = 1.0;
+  for (int q = 1; q <= m; ++q) r = r * (n - m + q) / q;
+  return r;
+}
+
+template <int NS>
+int launch_epilogue_t(const rc_mech *m, const EpiArgs &ea, const CellsDev &c, cudaStream_t s) {
+  const int ns = m->ns, nn = ea.n_nets;
+  const int stages = 3;
+  const size_t smem = (size_t)(ThermoSeg::size(ns) + ((ns * ns + 1) & ~1) + nn * ((ns + 1) & ~1) + 32) * 8 +
+                      rcs::Ring<EPI_TILE>::smem_bytes(2 + ns, nn * ea.passes, stages);
+  const int64_t ntiles = (ea.rows + EPI_TILE - 1) / EPI_TILE;
+  int64_t grid = rc_resident_blocks((const void *)chem_epilogue_kernel<NS>, EPI_THREADS, smem);
+  if (grid > ntiles) grid = ntiles;
+  if (grid > QPART_BLOCKS) grid = QPART_BLOCKS;
+  ProfScope prof(RC_STAGE_EPILOGUE, s);
+  chem_epilogue_kernel<NS><<<(unsigned)grid, EPI_THREADS, smem, s>>>(ea, c, stages);
+  RC_LAUNCH_CHECK();
+  return RC_OK;
+}
+
+int launch_epilogue(const rc_mech *m, const EpiArgs &ea, const CellsDev &c, cudaStream_t s) {
+  if (m->ns == 9) return launch_epilogue_t<9>(m, ea, c, s);
+  if (m->ns == 20) return launch_epilogue_t<20>(m, ea, c, s);
+  return launch_epilogue_t<0>(m, ea, c, s);
+}
+}  // namespace
+
 int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, size_t ws_bytes, cudaStream_t s) {
   if (c.n == 0) return RC_OK;
   // chunk capacity: largest multiple of 128 (<= MAX_CAP, <= n rounded up) whose layout fits the workspace
@@ -642,7 +719,13 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
     ProArgs pa{0, (int)c.n, (int)zrows, n->d_in, n->ns, KZ, (float)n->lambda_bc, (float)(1.0 / n->lambda_bc),
                n->d_xmean, n->d_xinvstd, z, prec, (int64_t)(zlo / EB)};
     ProfScope prof(RC_STAGE_PROLOGUE, s);
-    prologue_kernel<<<(unsigned)(zrows / 256), 256, 0, s>>>(pa, c);
+    const int pstages = 3;
+    const size_t psmem = rcs::Ring<PRO_TILE>::smem_bytes(2 + n->ns, 0, pstages);
+    int64_t pgrid = rc_resident_blocks((const void *)prologue_kernel, PRO_THREADS, psmem);
+    const int64_t ptiles = (c.n + PRO_TILE - 1) / PRO_TILE;
+    if (pgrid > ptiles) pgrid = ptiles;
+    if (pgrid < 1) pgrid = 1;  // n == 0 cannot reach here; padding rows only would need one CTA
+    prologue_kernel<<<(unsigned)pgrid, PRO_THREADS, psmem, s>>>(pa, c, pstages);
     RC_LAUNCH_CHECK();
   }
   for (int64_t c0 = 0; c0 < c.n; c0 += cap) {
@@ -671,31 +754,10 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
     // layer 3 + folded layer 4: the same CTA-pair GEMM with the dot epilogue (K = h2, zero-filled to KC)
     L2Args l3{mt, n->h3 / NP3, nets, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, n->d_w4, opart, cap, (n->h2 % KC) / KATOM};
     if ((rc = launch_l2_pair(NP3, prec, m3, l3, s))) return rc;
-    EpiArgs ea{c0, rows, cap, nets, 4 * (n->h3 / NP3), n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt, opart,
-               n->d_b4, n->d_ymean, n->d_ystd, m->d_P, m->d_thermo, n->d_species, qpart};
-    const size_t esm = (size_t)ThermoSeg::size(m->ns) * 8 + (size_t)((m->ns * m->ns + 1) & ~1) * 8 + (size_t)m->ns * nets * 8;
-    // one wave of resident blocks (grid-stride over the rows): a partial second wave would
-    // double the latency-bound kernel's time
-    static int eres[3] = {0, 0, 0};
-    const int ek = m->ns == 9 ? 0 : m->ns == 20 ? 1 : 2;
-    if (!eres[ek]) {
-      int per = 0;
-      const cudaError_t e = ek == 0 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, chem_epilogue_kernel<9>, 256, esm)
-                            : ek == 1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, chem_epilogue_kernel<20>, 256, esm)
-                                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, chem_epilogue_kernel<0>, 256, esm);
-      eres[ek] = (e == cudaSuccess && per > 0) ? per * mlp_num_sms() : mlp_num_sms();
-    }
-    int eblocks = (rows + 255) / 256;
-    if (eblocks > eres[ek]) eblocks = eres[ek];
-    if (eblocks > QPART_BLOCKS) eblocks = QPART_BLOCKS;
-    ProfScope prof(RC_STAGE_EPILOGUE, s);
-    if (m->ns == 9)
-      chem_epilogue_kernel<9><<<eblocks, 256, esm, s>>>(ea, c);
-    else if (m->ns == 20)
-      chem_epilogue_kernel<20><<<eblocks, 256, esm, s>>>(ea, c);
-    else
-      chem_epilogue_kernel<0><<<eblocks, 256, esm, s>>>(ea, c);
-    RC_LAUNCH_CHECK();
+    EpiArgs ea{c0, rows, cap, nets, n->h3 / NP3, n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt, opart,
+               n->d_b4, n->d_ymean, n->d_ystd, m->d_P, m->d_thermo, n->d_species, qpart, {}};
+    for (int q = 0; q <= 16; ++q) ea.binom[q] = q <= n->inv_lambda ? binom(n->inv_lambda, q) : 0.0;
+    if ((rc = launch_epilogue(m, ea, c, s))) return rc;
     launches += 5;
   }
   if (c.red) {

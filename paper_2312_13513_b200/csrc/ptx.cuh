@@ -95,6 +95,16 @@ __device__ __forceinline__ double rcp_f64(double x) {
   return fma(y, e, y);
 }
 
+// MUFU seed + ONE Newton step: relative error ~ (seed error)^2, ~1e-13, for uses whose result
+// only has to hold the 1e-10 fp64 parity gate (transport) or that feed an iteration that corrects
+// itself (the Newton update of thermo, where any approximate 1/cp still converges)
+__device__ __forceinline__ double rcp_f64_fast(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
 // ---------------------------------------------------------------- TMA
 // 1D bulk copy global -> shared, completion counted on an mbarrier (bytes % 16 == 0)
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {

@@ -34,15 +34,19 @@ struct ThermoSeg {        // doubles, offsets relative to the segment start
 };
 
 struct TransportSeg {
-  // visc[ns][5] cond[ns][5] diff[np][5] W[ns] invW[ns] c1[ns][ns] c2[ns][ns]
+  // visc[ns][5] cond[ns][5] diff[np][6] (5 fit coefficients + pad: 16-byte aligned pairs)
+  // W[nse] invW[nse] and the factorised Wilke matrices M0, M1, M2 [ns][nse] (nse = ns rounded
+  // up to even, rows 16-byte aligned): with c1_kj = (W_j/W_k)^(1/4), c2_kj = 1/sqrt(8(1+W_k/W_j)),
+  // M0 = c2, M1 = 2 c2 c1, M2 = c2 c1^2, so that sum_j X_j Phi_kj = A_k + s_k (B_k + s_k C_k)
+  // with A = M0 X, B = M1 (X/s), C = M2 (X/s^2) and s_k = sqrt(mu_k)
+  __host__ __device__ static int nse(int ns) { return (ns + 1) & ~1; }
   __host__ __device__ static int visc(int) { return 0; }
   __host__ __device__ static int cond(int ns) { return 5 * ns; }
   __host__ __device__ static int diff(int ns) { return 10 * ns; }
-  __host__ __device__ static int W(int ns) { return 10 * ns + 5 * (ns * (ns + 1) / 2); }
-  __host__ __device__ static int invW(int ns) { return W(ns) + ns; }
-  __host__ __device__ static int c1(int ns) { return W(ns) + 2 * ns; }
-  __host__ __device__ static int c2(int ns) { return c1(ns) + ns * ns; }
-  __host__ __device__ static int size(int ns) { return (c2(ns) + ns * ns + 1) & ~1; }
+  __host__ __device__ static int W(int ns) { return 10 * ns + 6 * (ns * (ns + 1) / 2); }
+  __host__ __device__ static int invW(int ns) { return W(ns) + nse(ns); }
+  __host__ __device__ static int M(int ns, int q) { return W(ns) + 2 * nse(ns) + q * ns * nse(ns); }
+  __host__ __device__ static int size(int ns) { return M(ns, 3); }
 };
 
 struct rc_mech {
@@ -79,6 +83,10 @@ struct rc_mlp {
 // errors / bookkeeping
 // ---------------------------------------------------------------------------
 int rc_fail(int code, const char *fmt, ...);
+// SMs of the current device, and the resident CTAs of `kernel` at (threads, dynamic smem) over the
+// whole device (occupancy x SMs; persistent grids are sized with it).  Cached per device/kernel/config.
+int rc_sm_count();
+int rc_resident_blocks(const void *kernel, int threads, size_t smem);
 void rc_count_launch(int n = 1);
 void rc_reset_launches();
 // per-stage CUDA-event timing (rc_profile_*); no-op unless enabled

@@ -2,16 +2,19 @@
 // polynomials, then cp and rho (§3.1 "Newton's method and
 // high-order temperature polynomials"; R8, R9).
 //
-// HBM-bound design: one thread per cell, component-major
-// coalesced fp64 loads of (h, T, p, Y_k) -> 96 B/cell in, 24 B/cell out for the
-// H2 set.  The species table is staged once per CTA into shared memory with a
-// single bulk-TMA copy.  To keep the per-iteration cost independent of ns the
-// mass-fraction-weighted NASA coefficients of the mixture are formed once per
-// range (12 ns DFMA), so each Newton iteration is two Horner polynomials and a
-// division instead of a loop over species ("computation consolidation",
-// PAPER.md:180).
+// HBM-bound design: component-major fp64 (h, T, p, Y_k) in,
+// 96 B/cell for the H2 set, 24 B/cell out.  A persistent grid streams 128-cell
+// tiles through a ring of shared-memory stages filled by one bulk-TMA copy per
+// SoA row (stream.cuh), so 2-3 tiles per CTA are always in flight while one
+// thread per cell runs the Newton iteration from shared memory.  The species
+// table is staged once per CTA with one bulk copy.  To keep the per-iteration
+// cost independent of ns the mass-fraction-weighted NASA coefficients of the
+// mixture are formed once per range (12 ns DFMA), so each Newton iteration is
+// two Horner polynomials and a reciprocal instead of a loop over species
+// ("computation consolidation").
 #include "ptx.cuh"
 #include "rc_internal.h"
+#include "stream.cuh"
 
 namespace {
 
@@ -34,22 +37,32 @@ __device__ __forceinline__ void warp_max_T(double *dst, double T) {
     atomicMax((unsigned long long *)dst, (unsigned long long)__double_as_longlong(v));
 }
 
+constexpr int THERMO_TILE = 256;                  // cells per stage = consumer threads per CTA
+constexpr int THERMO_THREADS = THERMO_TILE + 32;  // + the producer warp (stream.cuh run_ws)
+
 template <int NS, bool UNIFORM>
-__global__ void __launch_bounds__(256, 4) thermo_kernel(const double *__restrict__ tab, int ns_rt, CellsDev c) {
+__global__ void __launch_bounds__(THERMO_THREADS, 3) thermo_kernel(const double *__restrict__ tab, int ns_rt, CellsDev c, int stages) {
   extern __shared__ __align__(16) double s_tab[];
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bars[1 + 16];
   const int ns = NS ? NS : ns_rt;
-  const uint32_t bytes = (uint32_t)ThermoSeg::size(ns) * 8u;
+  const int tsz = ThermoSeg::size(ns);
+  const bool hmode = c.mode == RC_MODE_H;
+  // stage rows (fp64): T, p, Y_0..Y_{ns-1}, then h (h-mode only)
+  const rcs::Ring<THERMO_TILE> ring{reinterpret_cast<uint8_t *>(s_tab + tsz), bars + 1, 2 + ns + (hmode ? 1 : 0), 0, stages};
   if (threadIdx.x == 0) {
-    rcx::mbar_init(&bar, 1);
-    rcx::fence_mbar_init();
+    rcx::mbar_init(&bars[0], 1);
+    ring.init(THERMO_TILE / 32);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    rcx::mbar_arrive_expect_tx(&bar, bytes);
-    rcx::bulk_g2s(s_tab, tab, bytes, &bar);
+    rcx::mbar_arrive_expect_tx(&bars[0], (uint32_t)tsz * 8u);
+    rcx::bulk_g2s(s_tab, tab, (uint32_t)tsz * 8u, &bars[0]);
   }
-  rcx::mbar_wait(&bar, 0);
+  auto src8 = [&](int r) -> const double * {
+    return r == 0 ? c.T : r == 1 ? c.p : r < 2 + ns ? c.Y + (size_t)(r - 2) * c.ld : c.h;
+  };
+  auto src4 = [&](int) -> const float * { return nullptr; };
+  rcx::mbar_wait(&bars[0], 0);
 
   const double Tmin = s_tab[0], Tmax = s_tab[1], Tmid = s_tab[2];
   const double *hlo = s_tab + ThermoSeg::hlo(ns), *hhi = s_tab + ThermoSeg::hhi(ns);
@@ -59,16 +72,18 @@ __global__ void __launch_bounds__(256, 4) thermo_kernel(const double *__restrict
 
   int n_bisect = 0, n_maxit = 0, n_neg = 0, n_bad = 0;
   double Tloc_max = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n; i += (int64_t)gridDim.x * blockDim.x) {
-    // mixture NASA coefficients per range and 1/W = sum Y_k / W_k.  All Y loads are issued
-    // up front; the table is read with volatile shared loads next to their use, because a
-    // fully unrolled loop would otherwise hoist the whole coefficient table into registers.
+  ring.run_ws(c.n, src8, src4, [&](int st, int64_t tile, int j) {
+    const int64_t i = tile * THERMO_TILE + j;
+    if (i >= c.n) return;
+    // mixture NASA coefficients per range and 1/W = sum Y_k / W_k.  The table is read with
+    // volatile shared loads next to their use: a fully unrolled loop would otherwise hoist the
+    // whole coefficient table into registers.
     double Y[CAP];
     bool neg = false;
 #pragma unroll UR
     for (int k = 0; k < CAP; ++k)
       if (k < ns) {
-        Y[k] = c.Y[k * c.ld + i];
+        Y[k] = ring.row8(st, 2 + k)[j];
         neg |= Y[k] < 0.0;
       }
     double Hl[6] = {0, 0, 0, 0, 0, 0}, Hh[6] = {0, 0, 0, 0, 0, 0}, sW = 0.0;
@@ -76,23 +91,25 @@ __global__ void __launch_bounds__(256, 4) thermo_kernel(const double *__restrict
     for (int k = 0; k < CAP; ++k)
       if (k < ns) {
 #pragma unroll
-        for (int j = 0; j < 6; j += 2) {
-          const double2 lo = lds_f64x2(hlo + 6 * k + j), hi = lds_f64x2(hhi + 6 * k + j);
-          Hl[j] = fma(Y[k], lo.x, Hl[j]);
-          Hl[j + 1] = fma(Y[k], lo.y, Hl[j + 1]);
-          Hh[j] = fma(Y[k], hi.x, Hh[j]);
-          Hh[j + 1] = fma(Y[k], hi.y, Hh[j + 1]);
+        for (int q = 0; q < 6; q += 2) {
+          const double2 lo = lds_f64x2(hlo + 6 * k + q), hi = lds_f64x2(hhi + 6 * k + q);
+          Hl[q] = fma(Y[k], lo.x, Hl[q]);
+          Hl[q + 1] = fma(Y[k], lo.y, Hl[q + 1]);
+          Hh[q] = fma(Y[k], hi.x, Hh[q]);
+          Hh[q + 1] = fma(Y[k], hi.y, Hh[q + 1]);
         }
         sW = fma(Y[k], invW[k], sW);
       }
-    const double p = c.p[i];
+    const double p = ring.row8(st, 1)[j];
     auto eval = [&](double T, double &h, double &cp) {
       if constexpr (UNIFORM) {
         const bool lo = T <= Tmid;
         double a0 = lo ? Hl[0] : Hh[0], a1 = lo ? Hl[1] : Hh[1], a2 = lo ? Hl[2] : Hh[2];
         double a3 = lo ? Hl[3] : Hh[3], a4 = lo ? Hl[4] : Hh[4], a5 = lo ? Hl[5] : Hh[5];
-        h = fma(T, fma(T, fma(T, fma(T, fma(T, a4, a3), a2), a1), a0), a5);
-        cp = fma(T, fma(T, fma(T, fma(T, 5.0 * a4, 4.0 * a3), 3.0 * a2), 2.0 * a1), a0);
+        // Estrin form (dependency depth 3 instead of 5: the Newton iteration is a latency chain)
+        const double T2 = T * T;
+        h = fma(T2 * T2, fma(T, a4, a3), fma(T2, fma(T, a2, a1), fma(T, a0, a5)));
+        cp = fma(T2 * T2, 5.0 * a4, fma(T2, fma(T, 4.0 * a3, 3.0 * a2), fma(T, 2.0 * a1, a0)));
       } else {  // per-species ranges (T_mid differs between species)
         h = 0.0;
         cp = 0.0;
@@ -107,16 +124,16 @@ __global__ void __launch_bounds__(256, 4) thermo_kernel(const double *__restrict
           }
       }
     };
-    double T = c.T[i], hT, cpT;
-    if (c.mode == RC_MODE_H) {
-      const double hs = c.h[i];
+    double T = ring.row8(st, 0)[j], hT, cpT;
+    if (hmode) {
+      const double hs = ring.row8(st, 2 + ns)[j];
       T = fmin(fmax(T, Tmin), Tmax);
       int clamp_hits = 0;
       bool done = false;
 #pragma unroll 1
       for (int it = 1; it <= 50; ++it) {
         eval(T, hT, cpT);
-        double Tn = T + (hs - hT) * rcx::rcp_f64(cpT);
+        double Tn = T + (hs - hT) * rcx::rcp_f64_fast(cpT);
         bool clamped = false;
         if (Tn < Tmin) { Tn = Tmin; clamped = true; }
         if (Tn > Tmax) { Tn = Tmax; clamped = true; }
@@ -140,14 +157,14 @@ __global__ void __launch_bounds__(256, 4) thermo_kernel(const double *__restrict
       c.T[i] = T;
     }
     eval(T, hT, cpT);
-    if (c.mode == RC_MODE_T && c.h) c.h[i] = hT;
+    if (!hmode && c.h) c.h[i] = hT;
     const double rho = p / (RC_RU * T * sW);
     if (c.cp) c.cp[i] = cpT;
     if (c.rho) c.rho[i] = rho;
     n_neg += neg;
     n_bad += !(isfinite(T) && isfinite(cpT) && isfinite(rho));
     Tloc_max = fmax(Tloc_max, (T > 0.0 && T < 1e300) ? T : 0.0);
-  }
+  });
   if (c.diag) {
     warp_count_add(c.diag + RC_DIAG_NEWTON_BISECT, n_bisect);
     warp_count_add(c.diag + RC_DIAG_NEWTON_MAXIT, n_maxit);
@@ -157,24 +174,28 @@ __global__ void __launch_bounds__(256, 4) thermo_kernel(const double *__restrict
   if (c.red) warp_max_T(c.red, Tloc_max);
 }
 
+template <int NS, bool U>
+int launch_thermo_t(const rc_mech *m, const CellsDev &c, cudaStream_t s) {
+  const int rows = 2 + m->ns + (c.mode == RC_MODE_H ? 1 : 0);
+  // 3 stages: two tiles in flight per CTA behind the one being computed
+  const int stages = 3;
+  const size_t smem = (size_t)ThermoSeg::size(m->ns) * 8 + rcs::Ring<THERMO_TILE>::smem_bytes(rows, 0, stages);
+  const int64_t ntiles = (c.n + THERMO_TILE - 1) / THERMO_TILE;
+  int64_t grid = rc_resident_blocks((const void *)thermo_kernel<NS, U>, THERMO_THREADS, smem);
+  if (grid > ntiles) grid = ntiles;
+  thermo_kernel<NS, U><<<(unsigned)grid, THERMO_THREADS, smem, s>>>(m->d_thermo, m->ns, c, stages);
+  RC_LAUNCH_CHECK();
+  return RC_OK;
+}
+
 }  // namespace
 
 int launch_thermo(const rc_mech *m, const CellsDev &c, cudaStream_t s) {
   if (c.n == 0) return RC_OK;
-  const int threads = 256;
-  int64_t blocks = (c.n + threads - 1) / threads;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  const size_t smem = (size_t)ThermoSeg::size(m->ns) * 8;
   const bool u = m->uniform_tmid;
   ProfScope prof(RC_STAGE_THERMO, s);
-  if (m->ns == 9 && u)
-    thermo_kernel<9, true><<<(unsigned)blocks, threads, smem, s>>>(m->d_thermo, m->ns, c);
-  else if (m->ns == 20 && u)
-    thermo_kernel<20, true><<<(unsigned)blocks, threads, smem, s>>>(m->d_thermo, m->ns, c);
-  else if (u)
-    thermo_kernel<0, true><<<(unsigned)blocks, threads, smem, s>>>(m->d_thermo, m->ns, c);
-  else
-    thermo_kernel<0, false><<<(unsigned)blocks, threads, smem, s>>>(m->d_thermo, m->ns, c);
-  RC_LAUNCH_CHECK();
-  return RC_OK;
+  if (m->ns == 9 && u) return launch_thermo_t<9, true>(m, c, s);
+  if (m->ns == 20 && u) return launch_thermo_t<20, true>(m, c, s);
+  if (u) return launch_thermo_t<0, true>(m, c, s);
+  return launch_thermo_t<0, false>(m, c, s);
 }
