@@ -158,8 +158,10 @@ def algorithmic(cfg, bundle, ns, n, precision="bf16"):
     return {
         "thermo_bytes": n * ((3 + ns) * 8 + 3 * 8),
         "transport_bytes": n * ((2 + ns) * 8 + (2 + ns) * 8),
-        # fits 11 ns, Wilke 7 ns^2, pairs 10 per pair (poly 8 + 2 fma), D_k 3 ns + ns^2 (numerators)
-        "transport_fp64_flops": n * (11 * ns + 7 * ns * ns + 10 * npair + 3 * ns + ns * ns + 40),
+        # FP64-pipe instructions of the factorised algorithm, x 2 flop per DFMA slot:
+        # Wilke 3 ns nse (A, B, C sums), binary pairs 8 per pair j < k (4 Horner + 2 reciprocal
+        # + 2 FMA), 32 per species (fits, reciprocals, sums, D_k), 120 per cell (ln T, sqrt, p/T^1.5)
+        "transport_fp64_flops": n * 2 * (3 * ns * ((ns + 1) // 2 * 2) + 8 * (npair - ns) + 32 * ns + 120),
         "L1_flops": n * nets * 2 * d * h1,
         "L2_flops": n * nets * 2 * h1 * h2,
         "L3_flops": n * nets * 2 * (h2 * h3 + h3),
@@ -262,7 +264,7 @@ def run_ours(a):
         kernels = {}
         for st_name, work, unit, bound, peak in [
             ("thermo", alg["thermo_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),
-            ("transport", alg["transport_fp64_flops"], "TFLOP/s", "alu", f64),
+            ("transport", alg["transport_fp64_flops"], "TFLOP/s", "fp64", f64),
             ("prologue", alg["prologue_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),
             ("L1", alg["L1_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),  # K=16: bound by the h1 write, not the MMA
             ("L2", alg["L2_flops"], "TFLOP/s", "tensor", tpeak),

@@ -206,11 +206,13 @@ __device__ __forceinline__ double2 lds2_epi(const double *p) {
   return v;
 }
 
-constexpr int EPI_TILE = 128;                 // cells per stage = consumer threads
-constexpr int EPI_THREADS = EPI_TILE + 32;    // + the producer warp (stream.cuh run_ws)
+// cells per stage = consumer threads (+ the producer warp, stream.cuh run_ws): 256 (two CTAs of
+// eight consumer warps per SM) unless the Ns = 20 register/shared footprint needs 128
+template <int NS> constexpr int epi_tile() { return NS == 20 ? 128 : 256; }
 
 template <int NS>
-__global__ void __launch_bounds__(EPI_THREADS, NS == 9 ? 3 : NS == 20 ? 2 : 1) chem_epilogue_kernel(EpiArgs a, CellsDev c, int stages) {
+__global__ void __launch_bounds__(epi_tile<NS>() + 32, NS == 0 ? 1 : 2) chem_epilogue_kernel(EpiArgs a, CellsDev c, int stages) {
+  constexpr int EPI_TILE = epi_tile<NS>(), EPI_THREADS = EPI_TILE + 32;
   constexpr int CAP = NS ? NS : RC_MAX_NS;
   constexpr int UR = NS ? NS : 1;
   constexpr int NETUNR = NS == 9 ? 8 : 1;
@@ -622,7 +624,8 @@ int launch_epilogue_t(const rc_mech *m, const EpiArgs &ea, const CellsDev &c, cu
   const int ns = m->ns, nn = ea.n_nets;
   const int stages = 3;
   const size_t smem = (size_t)(ThermoSeg::size(ns) + ((ns * ns + 1) & ~1) + nn * ((ns + 1) & ~1) + 32) * 8 +
-                      rcs::Ring<EPI_TILE>::smem_bytes(2 + ns, nn * ea.passes, stages);
+                      rcs::Ring<epi_tile<NS>()>::smem_bytes(2 + ns, nn * ea.passes, stages);
+  constexpr int EPI_TILE = epi_tile<NS>(), EPI_THREADS = EPI_TILE + 32;
   const int64_t ntiles = (ea.rows + EPI_TILE - 1) / EPI_TILE;
   int64_t grid = rc_resident_blocks((const void *)chem_epilogue_kernel<NS>, EPI_THREADS, smem);
   if (grid > ntiles) grid = ntiles;

@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(THERMO_THREADS, 3) thermo_kernel(const double 
   ring.run_ws(c.n, src8, src4, [&](int st, int64_t tile, int j) {
     const int64_t i = tile * THERMO_TILE + j;
     if (i >= c.n) return;
+    const double *S8 = ring.row8(st, 0) + j;  // fp64 row q of this cell: S8[q * THERMO_TILE]
     // mixture NASA coefficients per range and 1/W = sum Y_k / W_k.  The table is read with
     // volatile shared loads next to their use: a fully unrolled loop would otherwise hoist the
     // whole coefficient table into registers.
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(THERMO_THREADS, 3) thermo_kernel(const double 
 #pragma unroll UR
     for (int k = 0; k < CAP; ++k)
       if (k < ns) {
-        Y[k] = ring.row8(st, 2 + k)[j];
+        Y[k] = S8[(2 + k) * THERMO_TILE];
         neg |= Y[k] < 0.0;
       }
     double Hl[6] = {0, 0, 0, 0, 0, 0}, Hh[6] = {0, 0, 0, 0, 0, 0}, sW = 0.0;
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(THERMO_THREADS, 3) thermo_kernel(const double 
         }
         sW = fma(Y[k], invW[k], sW);
       }
-    const double p = ring.row8(st, 1)[j];
+    const double p = S8[THERMO_TILE];
     auto eval = [&](double T, double &h, double &cp) {
       if constexpr (UNIFORM) {
         const bool lo = T <= Tmid;
@@ -124,9 +125,9 @@ __global__ void __launch_bounds__(THERMO_THREADS, 3) thermo_kernel(const double 
           }
       }
     };
-    double T = ring.row8(st, 0)[j], hT, cpT;
+    double T = S8[0], hT, cpT;
     if (hmode) {
-      const double hs = ring.row8(st, 2 + ns)[j];
+      const double hs = S8[(2 + ns) * THERMO_TILE];
       T = fmin(fmax(T, Tmin), Tmax);
       int clamp_hits = 0;
       bool done = false;

@@ -85,13 +85,14 @@ __global__ void __launch_bounds__(TR_TILE, NS == 9 ? 3 : NS == 20 ? 2 : 1)
     const int jt = threadIdx.x;
     const int64_t i = tile * TR_TILE + jt;
     if (i >= c.n) return;
-    const double T = ring.row8(st, 0)[jt], p = ring.row8(st, 1)[jt];
+    const double *S8 = ring.row8(st, 0) + jt;  // fp64 row q of this cell: S8[q * TR_TILE]
+    const double T = S8[0], p = S8[TR_TILE];
     double X[CAPE], s[CAP], u[CAPE], v[CAPE];
     double sW = 0.0;
 #pragma unroll UR
     for (int k = 0; k < CAP; ++k)
       if (k < ns) {
-        X[k] = ring.row8(st, 2 + k)[jt];
+        X[k] = S8[(2 + k) * TR_TILE];
         sW = fma(X[k], invW[k], sW);
       }
     if (ns & 1) X[ns] = u[ns] = v[ns] = 0.0;  // pad slot: M rows are zero there
