@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--precision", default="bf16", choices=["bf16", "tf32", "tf32x3"])
     ap.add_argument("--strong", action="store_true", help="partition the config's cells (strong scaling)")
     ap.add_argument("--layerwise", action="store_true", help="rc_mlp_desc.flags = RC_MLP_LAYERWISE (comparison path)")
+    ap.add_argument("--pasr", action="store_true", help="LES: PaSR scaling of wdot with per-cell tau_mix (NEXT-4)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle baseline")
@@ -200,6 +201,9 @@ def run_ours(a):
     host = make_cells_at(cfg, idx)
     st = rc.CellState(n, ns, nets, outputs=("cp", "rho", "mu", "lam", "D", "wdot", "qdot"))
     st.load(host["T_true"], host["p"], host["Y"])
+    if a.pasr:
+        from workload import tau_mix_at
+        st.set_tau_mix(tau_mix_at(cfg, idx))
     stream = torch.cuda.current_stream()
     # h of each cell from the previous step's state: h(T_true, Y) by the library's own T-mode thermo
     rc.rc_thermo(mech, st.cells(rc.RC_MODE_T, chem=False, transport=False), stream)
@@ -312,7 +316,7 @@ def run_ours(a):
                        "mech": cfg.mech, "hidden": list(cfg.hidden), "nets": nets, "parallelism": f"cells dp{world}",
                        "l2": "working set > L2 (h2 of 262144-cell chunks x 8 nets 3.4 GB, z 32 MB; "
                              "cell state 0.2 GB) - no flush needed",
-                       "precision": a.precision},
+                       "precision": a.precision, **({"les_pasr": True} if a.pasr else {})},
             "roofline": {"kernel": ("fused L1+L2 (z -> h1 1600 on chip -> h2 800, tcgen05 bf16, 4-CTA clusters)"
                                     if fused else "L2 GEMM (h1 1600 -> h2 800, tcgen05)"), "bound": "tensor",
                          "achieved": l2.get("achieved"), "peak": tpeak, "unit": "TFLOP/s",

@@ -151,6 +151,16 @@ typedef struct {
   double *red;                    /* [2] device: red[0] = max over cells of T (atomic max,
                                      caller/rc_step zeroes), red[1] = sum qdot (written by chem) */
   int64_t *diag;                  /* [RC_DIAG_COUNT] device counters (atomic adds), may be NULL */
+  const double *tau_mix;          /* [ld] s, optional (NULL = laminar / quasi-DNS).  LES partially-stirred
+                                     reactor ("the partially-stirred reactor (PaSR) model
+                                     ... to account for the SGS turbulence-chemistry interaction"; its
+                                     equations are not in the paper -- DESIGN.md reading R19): the
+                                     subgrid mixing time of each cell (from the caller's SGS model).
+                                     rc_chem then scales wdot and qdot of the cell by
+                                     kappa = tau_c / (tau_c + tau_mix), with the chemical time
+                                     tau_c = sum_k C+_k / (1/2 sum_k |wdot_k| / W_k),
+                                     C+_k = rho max(Y_k, 0) / W_k, from the cell's unscaled wdot
+                                     (kappa = 1 where wdot = 0).  tau_mix >= 0. */
 } rc_cells;
 
 /* Workspace bytes rc_chem / rc_step use for n cells: the layer-1 input rows of

@@ -43,7 +43,7 @@ class _Cells(C.Structure):
     _fields_ = [("n", C.c_int64), ("ld", C.c_int64), ("mode", C.c_int32), ("h", C.c_void_p), ("T", C.c_void_p),
                 ("p", C.c_void_p), ("Y", C.c_void_p), ("cp", C.c_void_p), ("rho", C.c_void_p), ("mu", C.c_void_p),
                 ("lam", C.c_void_p), ("D", C.c_void_p), ("o", C.c_void_p), ("wdot", C.c_void_p),
-                ("qdot", C.c_void_p), ("red", C.c_double * 2), ("diag", C.c_int64 * 5)]
+                ("qdot", C.c_void_p), ("red", C.c_double * 2), ("diag", C.c_int64 * 5), ("tau_mix", C.c_void_p)]
 
 
 _lib = None
@@ -63,6 +63,7 @@ def lib():
             ("orc_binary_D", d, [vp, i, i, d, d]), ("orc_gelu", d, [d]),
             ("orc_mlp_forward", d, [vp, i, vp]), ("orc_projection", i, [vp, vp]),
             ("orc_prologue_cell", None, [vp, vp, d, d, vp, vp, vp]), ("orc_step", i, [vp, vp, vp, i]),
+            ("orc_pasr_kappa", d, [vp, d, vp, vp, d]),
         ]:
             f = getattr(_lib, name)
             f.restype, f.argtypes = res, args
@@ -114,6 +115,11 @@ class Mech:
         lib().orc_transport_cell(self.ref, T, p, _p(Y), C.addressof(mu), C.addressof(lam), _p(D))
         return mu.value, lam.value, D
 
+    def pasr_kappa(self, rho, Y, wdot, tau_mix):
+        Y = np.ascontiguousarray(Y, dtype=np.float64)
+        w = np.ascontiguousarray(wdot, dtype=np.float64)
+        return lib().orc_pasr_kappa(self.ref, rho, _p(Y), _p(w), tau_mix)
+
     def projection(self):
         P = np.empty((self.ns, self.ns))
         if lib().orc_projection(self.ref, _p(P)) != 0:
@@ -151,7 +157,7 @@ class Mlp:
 
 
 def step(mech: Mech, mlp: "Mlp | None", T, p, Y, h=None, mode: str = "h", transport: bool = True,
-         chem: bool = True, nthreads: int = 0) -> dict:
+         chem: bool = True, nthreads: int = 0, tau_mix=None) -> dict:
     """Run oracle steps 1-10 + a6 on host arrays. T is the guess (h-mode) or value (T-mode).
 
     Returns dict with T, h, cp, rho, mu, lambda, D[ns][n], o[n_nets][n], wdot[ns][n], qdot, red, diag.
@@ -174,6 +180,8 @@ def step(mech: Mech, mlp: "Mlp | None", T, p, Y, h=None, mode: str = "h", transp
     c = _Cells(n, n, 0 if mode == "h" else 1, _p(out["h"]), _p(out["T"]), _p(p), _p(Y), _p(out["cp"]),
                _p(out["rho"]), _p(out.get("mu")), _p(out.get("lambda")), _p(out.get("D")), _p(out.get("o")),
                _p(out.get("wdot")), _p(out.get("qdot")))
+    tau = None if tau_mix is None else np.ascontiguousarray(tau_mix, dtype=np.float64)
+    c.tau_mix = _p(tau)
     rc = lib().orc_step(mech.ref, mlp.ref if do_chem else None, C.byref(c), nthreads)
     if rc != 0:
         raise RuntimeError(f"orc_step failed: {rc}")

@@ -305,6 +305,22 @@ int orc_projection(const orc_mech *m, double *P) {
 /* ------------------------------------------------------------------ */
 /* whole field                                                          */
 /* ------------------------------------------------------------------ */
+/* step 11, LES partially-stirred reactor (PAPER.md:112 names PaSR for the SGS turbulence-chemistry
+ * interaction; its equations are not in the paper, reading R19):
+ *   C+_k = rho max(Y_k, 0) / W_k,  1/tau_c = (1/2 sum_k |wdot_k| / W_k) / sum_k C+_k,
+ *   kappa = tau_c / (tau_c + tau_mix), and kappa = 1 if sum_k |wdot_k| = 0. */
+double orc_pasr_kappa(const orc_mech *m, double rho, const double *Y, const double *wdot, double tau_mix) {
+  double conc = 0.0, act = 0.0;
+  for (int k = 0; k < m->ns; ++k) {
+    double W = species_W(m, k);
+    conc += rho * (Y[k] > 0.0 ? Y[k] : 0.0) / W;
+    act += fabs(wdot[k]) / W;
+  }
+  if (act == 0.0) return 1.0;
+  double tau_c = conc / (0.5 * act);
+  return tau_c / (tau_c + tau_mix);
+}
+
 typedef struct {
   const orc_mech *m;
   const orc_mlp *n;
@@ -405,12 +421,18 @@ static void *run_cells(void *arg) {
       }
       J->diag[4] += negout;
       /* step 10: sources */
+      double w[64];
+      for (int k = 0; k < ns; ++k) w[k] = rho * dYp[k] / n->dt;
+      /* step 11 (LES): PaSR scaling of the laminar sources */
+      if (c->tau_mix) {
+        double kappa = orc_pasr_kappa(m, rho, Y, w, c->tau_mix[i]);
+        for (int k = 0; k < ns; ++k) w[k] = kappa * w[k];
+      }
       double q = 0.0;
       for (int k = 0; k < ns; ++k) {
-        double w = rho * dYp[k] / n->dt;
-        c->wdot[k * ld + i] = w;
-        q -= orc_species_h(m, k, T) * w;
-        bad |= !isfinite(w);
+        c->wdot[k * ld + i] = w[k];
+        q -= orc_species_h(m, k, T) * w[k];
+        bad |= !isfinite(w[k]);
       }
       if (c->qdot) c->qdot[i] = q;
       bad |= !isfinite(q);

@@ -70,6 +70,11 @@ int orc_projection(const orc_mech *m, double *P);
 void orc_prologue_cell(const orc_mech *m, const orc_mlp *n, double T, double p, const double *Y,
                        double *z, double *b);
 
+/* step 11 (LES only, reading R19): PaSR fraction kappa = tau_c / (tau_c + tau_mix) of a cell
+ * from its laminar sources wdot[ns], density and mass fractions, with the chemical time
+ * tau_c = sum_k rho max(Y_k,0)/W_k / (1/2 sum_k |wdot_k|/W_k); kappa = 1 when wdot = 0 */
+double orc_pasr_kappa(const orc_mech *m, double rho, const double *Y, const double *wdot, double tau_mix);
+
 /* ---- whole-field entry points (SoA, host arrays) ---- */
 typedef struct {
   int64_t n, ld;
@@ -82,6 +87,7 @@ typedef struct {
   double *qdot;        /* [ld] */
   double red[2];       /* out: max T, sum qdot (Neumaier) */
   int64_t diag[5];     /* out: newton_bisect, newton_maxit, nonfinite, negY_in, negY_out */
+  const double *tau_mix; /* [ld] LES PaSR subgrid mixing time (NULL = laminar), step 11 */
 } orc_cells;
 
 /* a1 (+cp, rho); a2 if mu/lambda/D non-NULL; a3-a5 if mlp != NULL and wdot != NULL; a6 reductions.

@@ -48,6 +48,7 @@ class CellState:
         self.o = torch.zeros(max(n_nets, 1), ld, dtype=torch.float32, device=device) if ("o" in outputs and n_nets) else None
         self.red = torch.zeros(2, **f64)
         self.diag = torch.zeros(5, dtype=torch.int64, device=device)
+        self.tau_mix = None  # LES PaSR mixing time [ld] (set_tau_mix); None = laminar
 
     def load(self, T, p, Y, h=None):
         """Copy host (numpy) inputs into the device buffers (first n columns)."""
@@ -60,12 +61,23 @@ class CellState:
             self.h[:n].copy_(torch.from_numpy(np.ascontiguousarray(h, dtype=np.float64)))
         return self
 
+    def set_tau_mix(self, tau):
+        """LES PaSR subgrid mixing time per cell (host array, s); None switches PaSR off."""
+        import torch
+        if tau is None:
+            self.tau_mix = None
+            return self
+        if self.tau_mix is None:
+            self.tau_mix = torch.zeros(self.ld, dtype=torch.float64, device=self.T.device)
+        self.tau_mix[:self.n].copy_(torch.from_numpy(np.ascontiguousarray(tau, dtype=np.float64)))
+        return self
+
     def cells(self, mode=RC_MODE_H, dt=0.0, chem=True, transport=True):
         return make_cells(self.n, self.ld, mode, self.T, self.p, self.Y, h=self.h, cp=self.cp, rho=self.rho,
                           mu=self.mu if transport else None, lam=self.lam if transport else None,
                           D=self.D if transport else None, wdot=self.wdot if chem else None,
                           qdot=self.qdot if chem else None, o=self.o if chem else None, dt=dt, red=self.red,
-                          diag=self.diag)
+                          diag=self.diag, tau_mix=self.tau_mix)
 
     def host(self):
         """dict of numpy copies of every buffer (first n columns)."""

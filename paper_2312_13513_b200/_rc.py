@@ -44,7 +44,8 @@ class rc_cells(C.Structure):
     _fields_ = [("n", C.c_int64), ("ld", C.c_int64), ("mode", C.c_int32), ("h", C.c_void_p), ("T", C.c_void_p),
                 ("p", C.c_void_p), ("Y", C.c_void_p), ("cp", C.c_void_p), ("rho", C.c_void_p), ("mu", C.c_void_p),
                 ("lam", C.c_void_p), ("D", C.c_void_p), ("wdot", C.c_void_p), ("qdot", C.c_void_p),
-                ("o", C.c_void_p), ("dt", C.c_double), ("red", C.c_void_p), ("diag", C.c_void_p)]
+                ("o", C.c_void_p), ("dt", C.c_double), ("red", C.c_void_p), ("diag", C.c_void_p),
+                ("tau_mix", C.c_void_p)]
 
 
 EXPORTS = {
@@ -159,10 +160,11 @@ class MLPBundle:
 
 
 def make_cells(n, ld, mode, T, p, Y, h=None, cp=None, rho=None, mu=None, lam=None, D=None, wdot=None, qdot=None,
-               o=None, dt=0.0, red=None, diag=None):
+               o=None, dt=0.0, red=None, diag=None, tau_mix=None):
     """rc_cells struct from torch device tensors (component-major, stride ld)."""
     return rc_cells(int(n), int(ld), int(mode), _ptr(h), _ptr(T), _ptr(p), _ptr(Y), _ptr(cp), _ptr(rho), _ptr(mu),
-                    _ptr(lam), _ptr(D), _ptr(wdot), _ptr(qdot), _ptr(o), float(dt), _ptr(red), _ptr(diag))
+                    _ptr(lam), _ptr(D), _ptr(wdot), _ptr(qdot), _ptr(o), float(dt), _ptr(red), _ptr(diag),
+                    _ptr(tau_mix))
 
 
 def _stream(stream):

@@ -332,13 +332,13 @@ static int check_cells(const rc_mech *m, const rc_cells *c, CellsDev &o) {
   if (c->mode != RC_MODE_H && c->mode != RC_MODE_T) return rc_fail(RC_EINVAL, "mode must be RC_MODE_H or RC_MODE_T");
   if (!c->T || !c->p || !c->Y) return rc_fail(RC_EINVAL, "T, p and Y are required");
   if (c->mode == RC_MODE_H && !c->h) return rc_fail(RC_EINVAL, "h-mode needs h");
-  const void *ptrs[] = {c->h, c->T, c->p, c->Y, c->cp, c->rho, c->mu, c->lambda, c->D, c->wdot, c->qdot, c->o};
+  const void *ptrs[] = {c->h, c->T, c->p, c->Y, c->cp, c->rho, c->mu, c->lambda, c->D, c->wdot, c->qdot, c->o, c->tau_mix};
   for (const void *p : ptrs)
     if (p && !aligned16(p)) return rc_fail(RC_EALIGN, "cell arrays must be 16-byte aligned");
   if (((uintptr_t)c->red & 7u) || ((uintptr_t)c->diag & 7u))  // 64-bit atomics only
     return rc_fail(RC_EALIGN, "red / diag must be 8-byte aligned");
   o = CellsDev{c->n, c->ld, c->mode, c->h, c->T, c->p, c->Y, c->cp, c->rho, c->mu, c->lambda, c->D, c->wdot,
-               c->qdot, c->o, c->red, c->diag};
+               c->qdot, c->o, c->red, c->diag, c->tau_mix};
   return RC_OK;
 }
 

@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, NS == 0 ? 1 : 2) chem_epi
   auto src4 = [&](int r) -> const float * { return a.opart + (size_t)r * a.cap; };
   rcx::mbar_wait(&bars[0], 0);
   const double *hlo = s_tab + ThermoSeg::hlo(ns), *hhi = s_tab + ThermoSeg::hhi(ns), *tmid = s_tab + ThermoSeg::tmid(ns);
+  const double *invW = s_tab + ThermoSeg::invW(ns);
   // the columns of P gathered by net and stored contiguously: Pn[net][k] = P[k][species[net]]
   // (the other columns multiply dY = 0), padded to an even length for 16-byte loads
   for (int e = threadIdx.x; e < nn * nse; e += blockDim.x) {
@@ -284,7 +285,22 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, NS == 0 ? 1 : 2) chem_epi
           if (k + 1 < ns) v[k + 1] = fma(pp.y, dy, v[k + 1]);
         }
     }
-    // sources
+    // sources; LES: PaSR factor kappa = tau_c / (tau_c + tau_mix) = 1 / (1 + tau_mix / tau_c) with
+    // 1 / tau_c = (1/2 sum_k |wdot_k| / W_k) / sum_k C+_k (rc.h tau_mix, R19)
+    double scale = rho * a.inv_dt;
+    if (c.tau_mix) {
+      double act = 0.0, conc = 0.0;
+#pragma unroll UR
+      for (int k = 0; k < CAP; ++k)
+        if (k < ns) {
+          const double y = S8[(2 + k) * EPI_TILE];
+          act = fma(fabs(v[k]), invW[k], act);
+          conc = fma(y > 0.0 ? y : 0.0, invW[k], conc);
+        }
+      // 1/tau_c = (rho/dt) (1/2) act / (rho conc); kappa = 1 when nothing reacts
+      const double r = act > 0.0 ? 0.5 * act * a.inv_dt / conc : 0.0;
+      scale *= rcx::rcp_f64(fma(c.tau_mix[i], r, 1.0));
+    }
     double q = 0.0;
     bool neg = false, bad = false;
 #pragma unroll UR
@@ -292,7 +308,7 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, NS == 0 ? 1 : 2) chem_epi
       if (k < ns) {
         const double y = S8[(2 + k) * EPI_TILE];
         neg |= ((y > 0.0 ? y : 0.0) + v[k]) < 0.0;
-        const double w = rho * v[k] * a.inv_dt;
+        const double w = scale * v[k];
         c.wdot[k * c.ld + i] = w;
         const double *h = (T <= tmid[k]) ? hlo + 6 * k : hhi + 6 * k;
         const double hk = fma(T, fma(T, fma(T, fma(T, fma(T, h[4], h[3]), h[2]), h[1]), h[0]), h[5]);

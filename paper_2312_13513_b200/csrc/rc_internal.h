@@ -122,6 +122,7 @@ struct CellsDev {
   float *o;
   double *red;
   int64_t *diag;
+  const double *tau_mix;  // PaSR mixing time (NULL = laminar)
 };
 
 int launch_thermo(const rc_mech *m, const CellsDev &c, cudaStream_t s);

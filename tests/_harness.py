@@ -44,12 +44,12 @@ def inputs(cfg, idx=None, begin=0, end=None):
     return c
 
 
-def run_oracle(cfg, c, chem=True, transport=True, nthreads=0, b=None):
+def run_oracle(cfg, c, chem=True, transport=True, nthreads=0, b=None, tau_mix=None):
     m = mech(CONFIGS[cfg].mech)
     om = oracle.Mech(m)
     ob = oracle.Mlp(b if b is not None else bundle(CONFIGS[cfg].mech, CONFIGS[cfg].hidden)) if chem else None
     return oracle.step(om, ob, c["T_guess"], c["p"], c["Y"], h=c["h"], transport=transport, chem=chem,
-                       nthreads=nthreads)
+                       nthreads=nthreads, tau_mix=tau_mix)
 
 
 class Gpu:
@@ -67,12 +67,13 @@ class Gpu:
         self.n_nets = b["n_nets"]
         self.dt = b["dt"]
 
-    def run(self, c, ld=None, chem=True, transport=True, ws=None):
+    def run(self, c, ld=None, chem=True, transport=True, ws=None, tau_mix=None):
         import torch
         rc = self.rc
         n = c["p"].shape[0]
         st = rc.CellState(n, self.ns, self.n_nets if chem else 0, ld=ld)
         st.load(c["T_guess"], c["p"], c["Y"], h=c["h"])
+        st.set_tau_mix(tau_mix)
         if ws is None:
             ws = rc.aligned_workspace(self.mlp, max(n, 1))
         rc.rc_step(self.mech, self.mlp if chem else None, st.cells(rc.RC_MODE_H, dt=self.dt, chem=chem,

@@ -208,6 +208,19 @@ def _ch4_swb(cfg, idx, X):
 MINOR = {"h2_9sp": [3, 4, 5, 6, 7], "ch4_20sp": [1, 2, 4, 6, 7, 8, 9, 13, 14, 15, 16, 17, 18]}
 
 
+def tau_mix_at(cfg, idx: np.ndarray) -> np.ndarray:
+    """LES subgrid mixing time per cell [s] for the PaSR option (rc_cells.tau_mix, R19):
+    log-uniform in [1e-6, 1e-3] s along a smooth field (tau_mix = C_mix sqrt(nu_sgs / eps) of an LES
+    with eps ~ 1e1..1e6 m^2/s^3), so kappa spans ~0.2..1 against the random-init nets' tau_c."""
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    idx = np.asarray(idx, dtype=np.int64)
+    X = coords(cfg, idx)
+    F = SmoothField(11, X.shape[1])(X)                   # ~N(0,1)-like smooth field
+    u = 0.5 * (1.0 + np.tanh(F))                        # (0, 1)
+    return 10.0 ** (-6.0 + 3.0 * u)
+
+
 def make_cells(cfg, begin: int = 0, end: int | None = None, chunk: int = 1 << 20) -> dict:
     """States of global cells [begin, end) of config `cfg` (name or Config).
 
