@@ -36,7 +36,7 @@ class _Mlp(C.Structure):
     _fields_ = [("n_nets", C.c_int32), ("d_in", C.c_int32), ("hidden", C.c_int32 * 3),
                 ("species_of_net", C.c_void_p), ("params", C.c_void_p), ("x_mean", C.c_void_p),
                 ("x_std", C.c_void_p), ("y_mean", C.c_void_p), ("y_std", C.c_void_p),
-                ("lambda_bc", C.c_double), ("dt", C.c_double)]
+                ("lambda_bc", C.c_double), ("dt", C.c_double), ("shared", C.c_int32)]
 
 
 class _Cells(C.Structure):
@@ -142,7 +142,7 @@ class Mlp:
         self.s = _Mlp(self.n_nets, self.d_in, (C.c_int32 * 3)(*b["hidden"]),
                       _p(self.keep["species_of_net"]), _p(self.keep["params"]), _p(self.keep["x_mean"]),
                       _p(self.keep["x_std"]), _p(self.keep["y_mean"]), _p(self.keep["y_std"]),
-                      float(b["lambda_bc"]), float(b["dt"]))
+                      float(b["lambda_bc"]), float(b["dt"]), int(bool(b.get("shared", False))))
         self.ref = C.byref(self.s)
 
     def forward(self, net: int, z):

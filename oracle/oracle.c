@@ -214,9 +214,21 @@ void orc_prologue_cell(const orc_mech *m, const orc_mlp *n, double T, double p, 
   for (int i = 0; i < n->d_in; ++i) z[i] = (x[i] - n->x_mean[i]) / n->x_std[i];
 }
 
+/* parameters of one net (one-net-per-species bundles) or of the single shared net */
 static int64_t net_param_count(const orc_mlp *n) {
   int64_t d = n->d_in, h1 = n->hidden[0], h2 = n->hidden[1], h3 = n->hidden[2];
-  return h1 * d + h1 + h2 * h1 + h2 + h3 * h2 + h3 + h3 + 1;
+  int64_t nout = n->shared ? n->n_nets : 1;
+  return h1 * d + h1 + h2 * h1 + h2 + h3 * h2 + h3 + nout * h3 + nout;
+}
+
+/* output layer of net `net`: row W4[net] and b4[net] of the shared net, or the net's own W4, b4 */
+static void output_layer(const orc_mlp *n, int net, const double **W4, const double **b4) {
+  int64_t d = n->d_in, h1 = n->hidden[0], h2 = n->hidden[1], h3 = n->hidden[2];
+  const double *P = n->params + (n->shared ? 0 : (int64_t)net * net_param_count(n));
+  const double *W4all = P + h1 * d + h1 + h2 * h1 + h2 + h3 * h2 + h3;
+  int64_t nout = n->shared ? n->n_nets : 1;
+  *W4 = W4all + (n->shared ? (int64_t)net * h3 : 0);
+  *b4 = W4all + nout * h3 + (n->shared ? net : 0);
 }
 
 /* out[j] = b[j] + sum_{k=0}^{in-1} W[j][k] x[k], sum in index order k = 0, 1, ... */
@@ -230,9 +242,10 @@ static void dense_ref(const double *W, const double *bias, int in, int out, cons
 
 double orc_mlp_forward(const orc_mlp *n, int net, const double *z) {
   int d = n->d_in, h1 = n->hidden[0], h2 = n->hidden[1], h3 = n->hidden[2];
-  const double *P = n->params + (int64_t)net * net_param_count(n);
+  const double *P = n->params + (n->shared ? 0 : (int64_t)net * net_param_count(n));
   const double *W1 = P, *b1 = W1 + (int64_t)h1 * d, *W2 = b1 + h1, *b2 = W2 + (int64_t)h2 * h1;
-  const double *W3 = b2 + h2, *b3 = W3 + (int64_t)h3 * h2, *W4 = b3 + h3, *b4 = W4 + h3;
+  const double *W3 = b2 + h2, *b3 = W3 + (int64_t)h3 * h2, *W4, *b4;
+  output_layer(n, net, &W4, &b4);
   double *a1 = malloc(sizeof(double) * (h1 + h2 + h3));
   double *a2 = a1 + h1, *a3 = a2 + h2, o;
   dense_ref(W1, b1, d, h1, z, a1);
@@ -388,18 +401,24 @@ static void *run_cells(void *arg) {
       orc_prologue_cell(m, n, T, p, Y, z, b);
       for (int k = 0; k < ns; ++k) dY[k] = 0.0;
       for (int net = 0; net < n->n_nets; ++net) {
-        const double *const *Wt = (const double *const *)&J->Wt[3 * net];
-        const double *Pn = n->params + (int64_t)net * net_param_count(n);
-        int d = n->d_in;
-        const double *b1 = Pn + (int64_t)h1 * d, *b2 = b1 + h1 + (int64_t)h2 * h1;
-        const double *b3 = b2 + h2 + (int64_t)h3 * h2, *W4 = b3 + h3, *b4 = W4 + h3;
+        /* hidden layers of this net (of the shared net: once per cell) */
+        int g = n->shared ? 0 : net;
         double *a1 = act, *a2 = act + h1, *a3 = a2 + h2, o;
-        dense_t(Wt[0], b1, d, h1, z, a1);
-        for (int j = 0; j < h1; ++j) a1[j] = orc_gelu(a1[j]);
-        dense_t(Wt[1], b2, h1, h2, a1, a2);
-        for (int j = 0; j < h2; ++j) a2[j] = orc_gelu(a2[j]);
-        dense_t(Wt[2], b3, h2, h3, a2, a3);
-        for (int j = 0; j < h3; ++j) a3[j] = orc_gelu(a3[j]);
+        if (!n->shared || net == 0) {
+          const double *const *Wt = (const double *const *)&J->Wt[3 * g];
+          const double *Pn = n->params + (int64_t)g * net_param_count(n);
+          int d = n->d_in;
+          const double *b1 = Pn + (int64_t)h1 * d, *b2 = b1 + h1 + (int64_t)h2 * h1;
+          const double *b3 = b2 + h2 + (int64_t)h3 * h2;
+          dense_t(Wt[0], b1, d, h1, z, a1);
+          for (int j = 0; j < h1; ++j) a1[j] = orc_gelu(a1[j]);
+          dense_t(Wt[1], b2, h1, h2, a1, a2);
+          for (int j = 0; j < h2; ++j) a2[j] = orc_gelu(a2[j]);
+          dense_t(Wt[2], b3, h2, h3, a2, a3);
+          for (int j = 0; j < h3; ++j) a3[j] = orc_gelu(a3[j]);
+        }
+        const double *W4, *b4;
+        output_layer(n, net, &W4, &b4);
         dense_ref(W4, b4, h3, 1, a3, &o);
         if (c->o) c->o[net * ld + i] = o;
         /* step 8: inverse Box-Cox */
@@ -453,7 +472,7 @@ int orc_step(const orc_mech *m, const orc_mlp *n, orc_cells *c, int nthreads) {
     /* transposed copies of W1..W3 for dense_t (layout only, no arithmetic) */
     Wt = calloc((size_t)3 * n->n_nets, sizeof(double *));
     int dims[4] = {n->d_in, n->hidden[0], n->hidden[1], n->hidden[2]};
-    for (int net = 0; net < n->n_nets; ++net) {
+    for (int net = 0; net < (n->shared ? 1 : n->n_nets); ++net) {
       const double *W = n->params + (int64_t)net * net_param_count(n);
       for (int l = 0; l < 3; ++l) {
         int in = dims[l], out = dims[l + 1];
@@ -483,7 +502,7 @@ int orc_step(const orc_mech *m, const orc_mlp *n, orc_cells *c, int nthreads) {
   free(jobs);
   free(th);
   if (Wt) {
-    for (int i = 0; i < 3 * n->n_nets; ++i) free(Wt[i]);
+    for (int i = 0; i < 3 * n->n_nets; ++i) free(Wt[i]); /* unused slots are NULL */
     free(Wt);
   }
   /* step a6: T_max and Neumaier-compensated sum of qdot (V_c = 1), cell order */

@@ -45,6 +45,9 @@ typedef struct {
   const double *x_mean, *x_std; /* [d_in] */
   const double *y_mean, *y_std; /* [n_nets] */
   double lambda_bc, dt;
+  int32_t shared;             /* 0: one net per species (reading R1);
+                                 1: ONE shared net d_in -> h1 -> h2 -> h3 -> n_nets (SURVEY §8(f) NEXT-2,
+                                 reading R20): params = W1 b1 W2 b2 W3 b3 W4[n_nets][h3] b4[n_nets] */
 } orc_mlp;
 
 /* ---- per-species / per-cell primitives (exposed for the pin tests) ---- */

@@ -150,9 +150,10 @@ def test_inverse_box_cox_single_net(orc, h2mech):
 
 
 def _torch_net(b, net):
-    """torch.nn float64 Sequential with net `net`'s weights (GELU MLP)."""
+    """torch.nn float64 Sequential with net `net`'s weights (GELU MLP); for a shared
+    bundle the one net with all n_nets outputs."""
     d, hid = b["d_in"], b["hidden"]
-    dims = [d, *hid, 1]
+    dims = [d, *hid, b["n_nets"] if b.get("shared") else 1]
     layers = []
     for l in range(4):
         layers.append(torch.nn.Linear(dims[l], dims[l + 1]))
@@ -208,3 +209,45 @@ def test_step_zscore_hand_computable(orc, h2mech):
             with torch.no_grad():
                 ref = _torch_net(bb, net)(torch.from_numpy(z0)[None]).item()
             assert r["o"][net, 0] == pytest.approx(ref, rel=1e-12, abs=1e-14)
+
+
+@pytest.mark.parametrize("hidden,cfg,n", [((64, 32, 16), "C1", 200), ((1600, 800, 400), "C2", 32)])
+def test_shared_net_field_path_matches_torch(orc, h2mech, hidden, cfg, n):
+    """NEXT-2 (reading R20): ONE net d_in -> h1 -> h2 -> h3 -> n_nets outputs.  orc_step's o[net]
+    equals output `net` of a torch float64 Sequential ending in Linear(h3, n_nets), on z from the
+    step-6 definition; orc_mlp_forward agrees; and wdot still conserves mass and elements."""
+    b = make_bundle("h2_9sp", hidden=hidden, shared=True)
+    assert b["params"].shape[0] == 1
+    om, mlp = orc.Mech(h2mech), orc.Mlp(b)
+    c = make_cells(cfg, 0, n) if cfg == "C1" else make_cells(cfg, 300_000, 300_000 + n)
+    r = orc.step(om, mlp, c["T_true"], c["p"], c["Y"], mode="T", transport=False)
+    lam = b["lambda_bc"]
+    x = np.vstack([c["T_true"][None], c["p"][None], (np.maximum(c["Y"], 0.0) ** lam - 1.0) / lam])
+    z = (x - b["x_mean"][:, None]) / b["x_std"][:, None]
+    with torch.no_grad():
+        ref = _torch_net(b, 0)(torch.from_numpy(np.ascontiguousarray(z.T))).numpy()   # [n][n_nets]
+    np.testing.assert_allclose(r["o"], ref.T, rtol=1e-12, atol=1e-13 * np.abs(ref).max())
+    for net in (0, b["n_nets"] - 1):
+        assert mlp.forward(net, z[:, 0]) == pytest.approx(ref[0, net], rel=1e-12, abs=1e-14)
+    tot = np.abs(r["wdot"]).sum(axis=0)
+    assert np.all(np.abs(r["wdot"].sum(axis=0)) <= 1e-12 * tot)
+    E = _mech_E(h2mech)
+    assert np.all(np.abs(E @ r["wdot"]) <= 1e-12 * tot[None, :])
+
+
+def test_shared_net_with_equal_output_rows_is_the_per_species_net(orc, h2mech):
+    """A shared net whose output rows all equal net 0's W4 (and b4) is n_nets copies of the
+    individual net 0: every o[net] equals the per-species bundle's o[0] bitwise (same summation
+    order).  Pins the shared output-layer indexing against the per-species path."""
+    bi = make_bundle("h2_9sp", hidden=(64, 32, 16))
+    bs = make_bundle("h2_9sp", hidden=(64, 32, 16), shared=True)
+    W = split_params(bi, 0)
+    P = np.concatenate([np.ravel(W[k]) for k in range(6)] + [np.tile(W[6][0], bs["n_nets"]),
+                                                             np.full(bs["n_nets"], W[7][0])])
+    bs["params"] = P[None, :]
+    c = make_cells("C1", 0, 64)
+    om = orc.Mech(h2mech)
+    ri = orc.step(om, orc.Mlp(bi), c["T_true"], c["p"], c["Y"], mode="T", transport=False)
+    rs = orc.step(om, orc.Mlp(bs), c["T_true"], c["p"], c["Y"], mode="T", transport=False)
+    for net in range(bs["n_nets"]):
+        assert np.array_equal(rs["o"][net], ri["o"][0])

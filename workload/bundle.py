@@ -23,20 +23,24 @@ SEED = 231213513
 STATS = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "data", "bundle_stats")
 
 
-def param_count(d_in: int, hidden) -> int:
+def param_count(d_in: int, hidden, n_out: int = 1) -> int:
     h1, h2, h3 = hidden
-    return h1 * d_in + h1 + h2 * h1 + h2 + h3 * h2 + h3 + h3 + 1
+    return h1 * d_in + h1 + h2 * h1 + h2 + h3 * h2 + h3 + n_out * h3 + n_out
 
 
 def make_bundle(mech_name: str, hidden=(1600, 800, 400), lambda_bc: float = 0.1, dt: float = 1e-6,
-                y_std: float = 0.02, stats: dict | None = None) -> dict:
+                y_std: float = 0.02, stats: dict | None = None, shared: bool = False) -> dict:
+    """shared=False: one net per non-inert species (PAPER.md:114, reading R1), params [n_nets][P];
+    shared=True: ONE net d_in -> hidden -> n_nets outputs (reading R20),
+    params [1][P] with the output layer W4 [n_nets][h3], b4 [n_nets]."""
     m = load_mech(mech_name)
     ns = m["ns"]
     d_in = ns + 2
     nets = [k for k in range(ns) if not m["inert"][k]]
-    dims = [d_in, *hidden, 1]
-    params = np.empty((len(nets), param_count(d_in, hidden)), dtype=np.float64)
-    for i in range(len(nets)):
+    n_out = len(nets) if shared else 1
+    dims = [d_in, *hidden, n_out]
+    params = np.empty((1 if shared else len(nets), param_count(d_in, hidden, n_out)), dtype=np.float64)
+    for i in range(params.shape[0]):
         g = torch.Generator().manual_seed(SEED + i)
         parts = []
         for l in range(4):
@@ -62,15 +66,18 @@ def make_bundle(mech_name: str, hidden=(1600, 800, 400), lambda_bc: float = 0.1,
         "y_std": np.full(len(nets), y_std),
         "lambda_bc": lambda_bc,
         "dt": dt,
+        "shared": bool(shared),
     }
 
 
 def split_params(bundle: dict, net: int):
-    """Views (W1, b1, W2, b2, W3, b3, W4, b4) of one net's flat fp64 parameters."""
+    """Views (W1, b1, W2, b2, W3, b3, W4, b4) of one net's flat fp64 parameters (of the shared
+    net for shared bundles: W4 [n_nets][h3], b4 [n_nets]; pass net = 0)."""
     d, (h1, h2, h3) = bundle["d_in"], bundle["hidden"]
+    n_out = bundle["n_nets"] if bundle.get("shared") else 1
     p = bundle["params"][net]
     out, o = [], 0
-    for fi, fo in ((d, h1), (h1, h2), (h2, h3), (h3, 1)):
+    for fi, fo in ((d, h1), (h1, h2), (h2, h3), (h3, n_out)):
         out.append(p[o:o + fi * fo].reshape(fo, fi)); o += fi * fo
         out.append(p[o:o + fo]); o += fo
     return out
