@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--strong", action="store_true", help="partition the config's cells (strong scaling)")
     ap.add_argument("--layerwise", action="store_true", help="rc_mlp_desc.flags = RC_MLP_LAYERWISE (comparison path)")
     ap.add_argument("--pasr", action="store_true", help="LES: PaSR scaling of wdot with per-cell tau_mix (NEXT-4)")
+    ap.add_argument("--shared", action="store_true", help="one shared net with n_nets outputs (NEXT-2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle baseline")
@@ -151,10 +152,11 @@ def algorithmic(cfg, bundle, ns, n, precision="bf16"):
     """Per-step algorithmic work: bytes for the HBM-bound stages (the
     minimum each must move), FLOPs for the MLP, FP64 flops for transport."""
     d, (h1, h2, h3) = bundle["d_in"], bundle["hidden"]
-    nets = bundle["n_nets"]
+    nout = bundle["n_nets"]
+    nets = 1 if bundle.get("shared") else nout              # hidden-layer nets (NEXT-2 shared net: one)
     eb = {"bf16": 2, "tf32": 4, "tf32x3": 8}[precision]  # MLP activation bytes (tf32x3: hi + lo)
     kz = 16 if d + 2 <= 16 else 32                          # layer-1 input row (d inputs, 2 bias columns)
-    flops_net = 2 * (d * h1 + h1 * h2 + h2 * h3 + h3)
+    flops_net = 2 * (d * h1 + h1 * h2 + h2 * h3 + h3 * nout // nets)
     npair = ns * (ns + 1) // 2
     return {
         "thermo_bytes": n * ((3 + ns) * 8 + 3 * 8),
@@ -165,11 +167,13 @@ def algorithmic(cfg, bundle, ns, n, precision="bf16"):
         "transport_fp64_flops": n * 2 * (3 * ns * ((ns + 1) // 2 * 2) + 8 * (npair - ns) + 32 * ns + 120),
         "L1_flops": n * nets * 2 * d * h1,
         "L2_flops": n * nets * 2 * h1 * h2,
-        "L3_flops": n * nets * 2 * (h2 * h3 + h3),
+        "L3_flops": n * nets * 2 * (h2 * h3 + (0 if bundle.get("shared") else h3)),
+        "L4_flops": n * 2 * h3 * nout if bundle.get("shared") else 0,
+        "L4_bytes": n * (h3 * eb + nout * 4) if bundle.get("shared") else 0,  # h3 read, o written
         "mlp_flops": n * nets * flops_net,
         "L1_bytes": n * nets * h1 * eb,               # h1 activations written
         # in: raw outputs o (fp32 per net), T, rho, Y; out: wdot, qdot
-        "epilogue_bytes": n * (nets * 4 + 2 * 8 + ns * 8 + ns * 8 + 8),
+        "epilogue_bytes": n * (nout * 4 + 2 * 8 + ns * 8 + ns * 8 + 8),
         # in: T, p, Y; out: the layer-1 input row
         "prologue_bytes": n * ((2 + ns) * 8 + kz * eb),
     }
@@ -191,7 +195,7 @@ def run_ours(a):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = CONFIGS[a.config]
     mech_d = load_mech(cfg.mech)
-    bundle = make_bundle(cfg.mech, hidden=cfg.hidden)
+    bundle = make_bundle(cfg.mech, hidden=cfg.hidden, shared=a.shared)
     mech = rc.Mechanism(mech_d)
     prec = {"bf16": rc.RC_BF16, "tf32": rc.RC_TF32, "tf32x3": rc.RC_TF32X3}[a.precision]
     mlp = rc.MLPBundle(mech, bundle, prec, flags=rc._rc.RC_MLP_LAYERWISE if a.layerwise else 0)
@@ -274,6 +278,7 @@ def run_ours(a):
             ("L2", alg["L2_flops"], "TFLOP/s", "tensor", tpeak),
             ("L12", alg["L1_flops"] + alg["L2_flops"], "TFLOP/s", "tensor", tpeak),  # fused layers 1+2
             ("L3", alg["L3_flops"], "TFLOP/s", "tensor", tpeak),
+            ("L4", alg["L4_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),  # shared net's output layer (CUDA cores)
             ("epilogue", alg["epilogue_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),
         ]:
             t_ms, cnt = per(st_name)
@@ -298,7 +303,7 @@ def run_ours(a):
                 traffic = tj.get("dominant_kernel_dram_bytes_per_launch", tj.get("L2_gemm_dram_bytes_per_launch"))
             except (OSError, ValueError):
                 traffic = None
-        mlp_ms = sum(per(s)[0] for s in ("L1", "L2", "L3", "L12"))
+        mlp_ms = sum(per(s)[0] for s in ("L1", "L2", "L3", "L12", "L4"))
         out = {
             "metric": "Mcells/s per thermo+transport+DNN-chem step",
             "value": round(value, 4),
@@ -316,7 +321,8 @@ def run_ours(a):
                        "mech": cfg.mech, "hidden": list(cfg.hidden), "nets": nets, "parallelism": f"cells dp{world}",
                        "l2": "working set > L2 (h2 of 262144-cell chunks x 8 nets 3.4 GB, z 32 MB; "
                              "cell state 0.2 GB) - no flush needed",
-                       "precision": a.precision, **({"les_pasr": True} if a.pasr else {})},
+                       "precision": a.precision, **({"les_pasr": True} if a.pasr else {}),
+                       **({"mlp": "one shared net, n_nets outputs (NEXT-2)"} if a.shared else {})},
             "roofline": {"kernel": ("fused L1+L2 (z -> h1 1600 on chip -> h2 800, tcgen05 bf16, 4-CTA clusters)"
                                     if fused else "L2 GEMM (h1 1600 -> h2 800, tcgen05)"), "bound": "tensor",
                          "achieved": l2.get("achieved"), "peak": tpeak, "unit": "TFLOP/s",

@@ -53,7 +53,7 @@ enum {
 
 enum { RC_MODE_H = 0, RC_MODE_T = 1 };               /* rc_cells.mode */
 enum { RC_BF16 = 0, RC_TF32 = 1, RC_TF32X3 = 2 };     /* rc_mlp_desc.precision */
-enum { RC_MLP_LAYERWISE = 1 };                        /* rc_mlp_desc.flags */
+enum { RC_MLP_LAYERWISE = 1, RC_MLP_SHARED = 2 };     /* rc_mlp_desc.flags */
 
 /* Diagnostic counters in rc_cells.diag[] (int64, accumulated with atomics). */
 enum {
@@ -119,9 +119,15 @@ typedef struct {
                                      RC_TF32X3: fp32-accurate GEMMs as three tf32 MMAs per product
                                      (a_hi b_hi + a_lo b_hi + a_hi b_lo), activations kept as tf32
                                      hi/lo pairs, exact-erf GELU (gate 1e-3 on o and wdot) */
-  int32_t flags;                  /* 0, or RC_MLP_LAYERWISE: run layers 1 and 2 as separate kernels
-                                     (h1 through the workspace) even where the fused layer-1/2 kernel
-                                     applies -- the comparison path; results agree to rounding */
+  int32_t flags;                  /* bitwise OR of
+                                     RC_MLP_LAYERWISE: run layers 1 and 2 as separate kernels (h1
+                                     through the workspace) even where the fused layer-1/2 kernel
+                                     applies -- the comparison path; results agree to rounding;
+                                     RC_MLP_SHARED: ONE shared net with n_nets outputs instead of one
+                                     net per species (reading R20:
+                                     the Table-1-consistent reading of PAPER.md:114/210); params is
+                                     then one block W1 b1 W2 b2 W3 b3 W4[n_nets][h3] b4[n_nets] and
+                                     output i predicts species_of_net[i].  RC_BF16 or RC_TF32 only. */
 } rc_mlp_desc;
 
 int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *desc, rc_mlp **out);
@@ -215,7 +221,8 @@ enum {
   RC_STAGE_THERMO = 0, RC_STAGE_TRANSPORT = 1, RC_STAGE_PROLOGUE = 2, RC_STAGE_L1 = 3, RC_STAGE_L2 = 4,
   RC_STAGE_L3 = 5, RC_STAGE_EPILOGUE = 6, RC_STAGE_FINALIZE = 7,
   RC_STAGE_L12 = 8,  /* fused layers 1+2 (bf16 at the paper widths; replaces L1 and L2) */
-  RC_STAGE_COUNT = 9
+  RC_STAGE_L4 = 9,   /* layer 4 of the shared net (RC_MLP_SHARED) */
+  RC_STAGE_COUNT = 10
 };
 int rc_profile_enable(int on);
 int rc_profile_read(double *ms /* [RC_STAGE_COUNT] */, int64_t *launches /* [RC_STAGE_COUNT] */, int reset);

@@ -16,7 +16,7 @@ SO = os.environ.get("RC_LIB") or os.path.join(HERE, "librc_b200.so")  # RC_LIB: 
 RC_OK, RC_EINVAL, RC_ENOMEM, RC_ECUDA, RC_EALIGN, RC_EUNSUPPORTED, RC_EDTMISMATCH = 0, -1, -2, -3, -4, -5, -6
 RC_MODE_H, RC_MODE_T = 0, 1
 RC_BF16, RC_TF32, RC_TF32X3 = 0, 1, 2
-RC_MLP_LAYERWISE = 1
+RC_MLP_LAYERWISE, RC_MLP_SHARED = 1, 2
 DIAG_NAMES = ["newton_bisect", "newton_maxit", "nonfinite", "negY_in", "negY_out"]
 
 
@@ -142,6 +142,8 @@ class MLPBundle:
                         self.keep["params"].ctypes.data, self.keep["x_mean"].ctypes.data,
                         self.keep["x_std"].ctypes.data, self.keep["y_mean"].ctypes.data,
                         self.keep["y_std"].ctypes.data, float(b["lambda_bc"]), float(b["dt"]), int(precision), int(flags))
+        if b.get("shared"):
+            d.flags |= RC_MLP_SHARED  # one shared net with n_nets outputs (NEXT-2)
         h = C.c_void_p()
         check(lib().rc_mlp_create(mech.h, C.byref(d), C.byref(h)))
         self.h = h
@@ -203,7 +205,7 @@ def rc_last_launch_count():
     return int(lib().rc_last_launch_count())
 
 
-STAGES = ["thermo", "transport", "prologue", "L1", "L2", "L3", "epilogue", "finalize", "L12"]
+STAGES = ["thermo", "transport", "prologue", "L1", "L2", "L3", "epilogue", "finalize", "L12", "L4"]
 
 
 def rc_profile_enable(on=True):

@@ -278,7 +278,9 @@ extern "C" int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *d, rc_mlp **ou
     return rc_fail(RC_EUNSUPPORTED, "rc_mlp_create: hidden (%d,%d,%d) must be multiples of (64,16,16)", h1, h2, h3);
   if (d->precision != RC_BF16 && d->precision != RC_TF32 && d->precision != RC_TF32X3)
     return rc_fail(RC_EINVAL, "rc_mlp_create: unknown precision %d", d->precision);
-  if (d->flags & ~RC_MLP_LAYERWISE) return rc_fail(RC_EINVAL, "rc_mlp_create: unknown flags 0x%x", d->flags);
+  if (d->flags & ~(RC_MLP_LAYERWISE | RC_MLP_SHARED)) return rc_fail(RC_EINVAL, "rc_mlp_create: unknown flags 0x%x", d->flags);
+  if ((d->flags & RC_MLP_SHARED) && d->precision == RC_TF32X3)
+    return rc_fail(RC_EUNSUPPORTED, "rc_mlp_create: RC_MLP_SHARED runs in RC_BF16 or RC_TF32");
   if (!(d->lambda_bc > 0.0) || !(d->dt > 0.0)) return rc_fail(RC_EINVAL, "rc_mlp_create: lambda and dt must be > 0");
   double inv = 1.0 / d->lambda_bc;
   int invi = (int)std::lround(inv);
@@ -295,6 +297,7 @@ extern "C" int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *d, rc_mlp **ou
   }
   rc_mlp *n = new rc_mlp();
   n->n_nets = d->n_nets;
+  n->gnets = (d->flags & RC_MLP_SHARED) ? 1 : d->n_nets;
   n->d_in = d_in;
   n->h1 = h1; n->h2 = h2; n->h3 = h3;
   n->precision = d->precision;

@@ -26,6 +26,7 @@ struct L2Args {
   float *opart;            // layer-3 mode: [nets][passes][cap] dots (column quarters summed in-kernel)
   int cap;
   int ktail;               // MMA K atoms in the last K chunk when K is not a multiple of it (0: full chunk)
+  int prof_stage = -1;     // rc_profile stage (-1: L3 with w4, else L2)
 };
 // fused layers 1+2 (mlp_l12_sm100.cu, bf16, h2 = 800): clusters of two CTA pairs share h1 chunks
 // maps: {z (KZ x 128 rows), W1 (KZ x 16 rows), W2 piece 1 (32 x 128 rows), W2 piece 2 (32 x 72 rows),

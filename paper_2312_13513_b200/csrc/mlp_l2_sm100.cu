@@ -577,7 +577,7 @@ int l2_pass_width(int h) {
 }
 
 int launch_l2_pair(int NP, int prec, const CUtensorMap *maps, const L2Args &a, cudaStream_t s) {
-  ProfScope prof(a.w4 ? RC_STAGE_L3 : RC_STAGE_L2, s);
+  ProfScope prof(a.prof_stage >= 0 ? a.prof_stage : a.w4 ? RC_STAGE_L3 : RC_STAGE_L2, s);
 #define RC_L2P_PREC(np, dot)                                                                                \
   return prec == 0 ? launch_l2_pair_t<np, dot, 0>(maps, a, s)                                               \
                    : prec == 1 ? launch_l2_pair_t<np, dot, 1>(maps, a, s) : launch_l2_pair_t<np, dot, 2>(maps, a, s);

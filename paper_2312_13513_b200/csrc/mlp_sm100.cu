@@ -135,6 +135,132 @@ __global__ void __launch_bounds__(PRO_THREADS) prologue_kernel(ProArgs a, CellsD
     store_z_row(a, r, x0);
 }
 
+// ------------------------------------------------------------------ layer 4 of the shared net (NEXT-2)
+// RC_MLP_SHARED (R20): o[out][r] = h3[r] . W4[out] for the n_out outputs of the one shared
+// net (b4 is added by the epilogue, as for the per-species nets).  h3 = GELU(h2 W3^T + b3) was
+// stored by the layer-3 GEMM ([cap][h3], bf16 or tf32-rounded fp32).  CUDA cores (2 h3 n_out FLOP
+// per cell is ~1% of the shared net's GEMM work), HBM-bound on the h3 read: one warp per row, lane
+// l owning the 8-column chunks l and l + 32 of the row (coalesced 16-byte loads of the contiguous
+// row), with its W4 slice (8 outputs x 16 columns) held in registers for all the warp's rows; the
+// 8 per-lane partial dots are combined by a 9-shuffle reduce-scatter (lane 4o holds output o).
+// Outputs beyond 8 run as further passes of 8.
+constexpr int L4_ROWS = 16;     // rows per stage: one bulk copy of 16 contiguous h3 rows
+constexpr int L4_STAGES = 4;
+constexpr int L4_THREADS = 32 + 32 * (L4_ROWS / 2);  // producer warp + one consumer warp per 2 rows
+
+template <bool TF32>
+__global__ void __launch_bounds__(L4_THREADS, 1) l4_kernel(const void *__restrict__ h3, const float *__restrict__ w4,
+                                                           float *__restrict__ o, int rows, int h3n, int nout, int cap,
+                                                           int o0) {
+  constexpr int CJ = 2;  // 8-column chunks per lane (h3 <= 512)
+  constexpr int EB = TF32 ? 4 : 2;
+  extern __shared__ __align__(128) uint8_t l4s[];
+  __shared__ __align__(8) uint64_t full[L4_STAGES], empty[L4_STAGES];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t row_bytes = (uint32_t)h3n * EB, stage_bytes = L4_ROWS * row_bytes;
+  const int ntiles = (rows + L4_ROWS - 1) / L4_ROWS;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < L4_STAGES; ++s) {
+      rcx::mbar_init(&full[s], 1);
+      rcx::mbar_init(&empty[s], L4_ROWS / 2);
+    }
+    rcx::fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 0) {  // producer: one bulk copy per 16-row tile
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int s = it % L4_STAGES;
+        if (it >= L4_STAGES) rcx::mbar_wait_sleep(&empty[s], (uint32_t)(it / L4_STAGES - 1) & 1u);
+        const int nr = rows - t * L4_ROWS < L4_ROWS ? rows - t * L4_ROWS : L4_ROWS;
+        rcx::mbar_arrive_expect_tx(&full[s], nr * row_bytes);
+        rcx::bulk_g2s(l4s + s * stage_bytes, static_cast<const uint8_t *>(h3) + (size_t)t * stage_bytes, nr * row_bytes,
+                      &full[s]);
+      }
+    }
+    return;
+  }
+  const int nch = h3n / 8;
+  float w[CJ][8][8];
+#pragma unroll
+  for (int j = 0; j < CJ; ++j)
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int c = lane + 32 * j, k = 8 * c + i, out = o0 + q;
+        w[j][i][q] = (c < nch && out < nout) ? w4[(size_t)out * h3n + k] : 0.f;
+      }
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  const int q = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
+  const int cw = warp - 1;  // consumer warp: rows 2 cw, 2 cw + 1 of each tile
+  int it = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int s = it % L4_STAGES;
+    rcx::mbar_wait(&full[s], (uint32_t)(it / L4_STAGES) & 1u);
+    const uint8_t *st = l4s + s * stage_bytes;
+    float x[2][CJ][8];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+      for (int j = 0; j < CJ; ++j) {
+        const int c = lane + 32 * j;
+        const uint8_t *src = st + (2 * cw + rr) * row_bytes + c * 8 * EB;
+        if (c < nch) {
+          if constexpr (TF32) {
+            const float4 a = *reinterpret_cast<const float4 *>(src), b = *reinterpret_cast<const float4 *>(src + 16);
+            x[rr][j][0] = a.x; x[rr][j][1] = a.y; x[rr][j][2] = a.z; x[rr][j][3] = a.w;
+            x[rr][j][4] = b.x; x[rr][j][5] = b.y; x[rr][j][6] = b.z; x[rr][j][7] = b.w;
+          } else {
+            const uint4 v = *reinterpret_cast<const uint4 *>(src);
+            const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              x[rr][j][2 * i] = __uint_as_float(u[i] << 16);
+              x[rr][j][2 * i + 1] = __uint_as_float(u[i] & 0xffff0000u);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) x[rr][j][i] = 0.f;
+        }
+      }
+    __syncwarp();
+    if (lane == 0) rcx::mbar_arrive(&empty[s]);  // stage rows read into registers
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int r = t * L4_ROWS + 2 * cw + rr;
+      float acc[8];
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) acc[qq] = 0.f;
+#pragma unroll
+      for (int j = 0; j < CJ; ++j)
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int qq = 0; qq < 8; ++qq) acc[qq] = fmaf(x[rr][j][i], w[j][i][qq], acc[qq]);
+      // reduce-scatter over the warp: xor 16 halves the outputs a lane holds (8 -> 4), xor 8
+      // (4 -> 2), xor 4 (2 -> 1), then xor 2 and xor 1 sum the last one
+      float u[4], tt[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float send = b4 ? acc[i] : acc[i + 4], keep = b4 ? acc[i + 4] : acc[i];
+        u[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const float send = b3 ? u[i] : u[i + 2], keep = b3 ? u[i + 2] : u[i];
+        tt[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
+      float v = (b2 ? tt[1] : tt[0]) + __shfl_xor_sync(0xffffffffu, b2 ? tt[0] : tt[1], 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      if ((lane & 3) == 0 && o0 + q < nout && r < rows) o[(size_t)(o0 + q) * cap + r] = v;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ epilogue (a5)
 struct EpiArgs {
   int64_t c0;
@@ -447,7 +573,7 @@ int mlp_num_sms() { return rc_sm_count(); }
 namespace {
 
 struct WsLayout {
-  size_t z, h1, h2, opart, qpart, total;
+  size_t z, h1, h2, h3, opart, qpart, total;
   int cap;
 };
 
@@ -468,9 +594,11 @@ WsLayout ws_layout(const rc_mlp *n, int cap, int64_t ncells) {
   const size_t eb = n->precision == RC_BF16 ? 2 : 4, nc = n->precision == RC_TF32X3 ? 2 : 1;
   const size_t zrows = (size_t)((ncells + 255) / 256 * 256);
   L.z = o; o = al(o + nc * zrows * n->kpad1 * eb);
-  L.h1 = o; o = al(o + (fused_path(n) ? 0 : nc * (size_t)n->n_nets * cap * n->h1 * eb));
-  L.h2 = o; o = al(o + nc * (size_t)n->n_nets * cap * n->h2 * eb);
-  const int np3 = n->h3 / l2_pass_width(n->h3);  // raw outputs per row: one per layer-3 pass
+  L.h1 = o; o = al(o + (fused_path(n) ? 0 : nc * (size_t)n->gnets * cap * n->h1 * eb));
+  L.h2 = o; o = al(o + nc * (size_t)n->gnets * cap * n->h2 * eb);
+  const bool shared = (n->flags & RC_MLP_SHARED) != 0;
+  L.h3 = o; o = al(o + (shared ? (size_t)cap * n->h3 * eb : 0));  // shared net: h3 for the layer-4 kernel
+  const int np3 = shared ? 1 : n->h3 / l2_pass_width(n->h3);  // raw outputs per row: one per layer-3 pass
   L.opart = o; o = al(o + (size_t)n->n_nets * np3 * cap * 4);
   L.total = o;
   return L;
@@ -517,8 +645,10 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
   if (n->h1 % 64 || !l2_pass_width(n->h2) || !l2_pass_width(n->h3))
     return rc_fail(RC_EUNSUPPORTED, "hidden widths (%d,%d,%d) not supported by the MLP kernels", n->h1, n->h2, n->h3);
   const bool tf32 = n->precision != RC_BF16, x3 = n->precision == RC_TF32X3;
-  const int nets = n->n_nets, din = n->d_in, h1 = n->h1, h2 = n->h2, h3 = n->h3, kp = n->kpad1;
-  const size_t P = (size_t)h1 * din + h1 + (size_t)h2 * h1 + h2 + (size_t)h3 * h2 + h3 + h3 + 1;
+  // hidden layers: one block per GEMM net (shared: one); output layer: one row per output
+  const int nets = n->gnets, nout = n->n_nets, din = n->d_in, h1 = n->h1, h2 = n->h2, h3 = n->h3, kp = n->kpad1;
+  const bool shared = (n->flags & RC_MLP_SHARED) != 0;
+  const size_t P = (size_t)h1 * din + h1 + (size_t)h2 * h1 + h2 + (size_t)h3 * h2 + h3 + (shared ? (size_t)nout : 1) * (h3 + 1);
   // weights, K-major [net][out][in]: bf16 (RNE) or tf32-rounded fp32
   // W1 gets 64 zero rows after the last net: the fused layer-1/2 kernel's W1 box of the last
   // chunk pair can reach past the last net when h1 / 64 is odd
@@ -551,7 +681,7 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
     row[0] = hi;
     row[1] = f2bf((float)(b - (double)hf));
   };
-  std::vector<float> b1((size_t)nets * h1), b2((size_t)nets * h2), b3((size_t)nets * h3), w4((size_t)nets * h3), b4(nets);
+  std::vector<float> b1((size_t)nets * h1), b2((size_t)nets * h2), b3((size_t)nets * h3), w4((size_t)nout * h3), b4(nout);
   for (int i = 0; i < nets; ++i) {
     const double *p = d->params + i * P;
     const double *pb1 = p + (size_t)h1 * din;
@@ -598,9 +728,13 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
       if (!tf32) bias_operand(p[r], &B3k[((size_t)i * h3 + r) * 16]);
     }
     p += h3;
-    for (int r = 0; r < h3; ++r) w4[(size_t)i * h3 + r] = (float)p[r];
-    p += h3;
-    b4[i] = (float)p[0];
+    if (shared) {  // W4 [nout][h3], b4 [nout] of the one shared net
+      for (size_t e = 0; e < (size_t)nout * h3; ++e) w4[e] = (float)p[e];
+      for (int o = 0; o < nout; ++o) b4[o] = (float)p[(size_t)nout * h3 + o];
+    } else {
+      for (int r = 0; r < h3; ++r) w4[(size_t)i * h3 + r] = (float)p[r];
+      b4[i] = (float)p[h3];
+    }
   }
   std::vector<float> xm(din), xi(din);
   for (int k = 0; k < din; ++k) {
@@ -618,8 +752,8 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
             up((void **)&n->d_b2, b2.data(), b2.size() * 4) && up((void **)&n->d_b3, b3.data(), b3.size() * 4) &&
             up((void **)&n->d_w4, w4.data(), w4.size() * 4) && up((void **)&n->d_b4, b4.data(), b4.size() * 4) &&
             up((void **)&n->d_xmean, xm.data(), xm.size() * 4) && up((void **)&n->d_xinvstd, xi.data(), xi.size() * 4) &&
-            up((void **)&n->d_ymean, d->y_mean, nets * 8) && up((void **)&n->d_ystd, d->y_std, nets * 8) &&
-            up((void **)&n->d_species, d->species_of_net, nets * 4);
+            up((void **)&n->d_ymean, d->y_mean, nout * 8) && up((void **)&n->d_ystd, d->y_std, nout * 8) &&
+            up((void **)&n->d_species, d->species_of_net, nout * 4);
   if (ok && !tf32) ok = up(&n->d_b2k, B2k.data(), B2k.size() * 2) && up(&n->d_b3k, B3k.data(), B3k.size() * 2);
   if (ok && x3)
     ok = up(&n->d_W1lo, L1v.data(), L1v.size() * 4) && up(&n->d_W2lo, L2v.data(), L2v.size() * 4) &&
@@ -652,6 +786,22 @@ int launch_epilogue_t(const rc_mech *m, const EpiArgs &ea, const CellsDev &c, cu
   return RC_OK;
 }
 
+int launch_l4(const rc_mlp *n, const void *h3, float *o, int rows, int cap, bool tf32, cudaStream_t s) {
+  if (n->h3 > 512 || n->h3 % 8) return rc_fail(RC_EUNSUPPORTED, "shared net: layer-4 kernel needs h3 <= 512");
+  ProfScope prof(RC_STAGE_L4, s);
+  const size_t smem = (size_t)L4_STAGES * L4_ROWS * n->h3 * (tf32 ? 4 : 2);
+  const void *k = tf32 ? (const void *)l4_kernel<true> : (const void *)l4_kernel<false>;
+  int64_t grid = rc_resident_blocks(k, L4_THREADS, smem);
+  const int64_t ntiles = (rows + L4_ROWS - 1) / L4_ROWS;
+  if (grid > ntiles) grid = ntiles;
+  for (int o0 = 0; o0 < n->n_nets; o0 += 8) {
+    if (tf32) l4_kernel<true><<<(unsigned)grid, L4_THREADS, smem, s>>>(h3, n->d_w4, o, rows, n->h3, n->n_nets, cap, o0);
+    else l4_kernel<false><<<(unsigned)grid, L4_THREADS, smem, s>>>(h3, n->d_w4, o, rows, n->h3, n->n_nets, cap, o0);
+    RC_LAUNCH_CHECK();
+  }
+  return RC_OK;
+}
+
 int launch_epilogue(const rc_mech *m, const EpiArgs &ea, const CellsDev &c, cudaStream_t s) {
   if (m->ns == 9) return launch_epilogue_t<9>(m, ea, c, s);
   if (m->ns == 20) return launch_epilogue_t<20>(m, ea, c, s);
@@ -672,7 +822,8 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   const int EB = tf32 ? 4 : 2;
   const int RB = x3 ? 64 : 128, KC = RB / EB;  // element bytes; K elements per swizzled operand row
   const int KATOM = tf32 ? 8 : 16;  // K elements per MMA (32 bytes)
-  const int nets = n->n_nets;
+  const int nets = n->gnets, nout = n->n_nets;  // GEMM nets (shared: 1), raw outputs per cell
+  const bool shared = (n->flags & RC_MLP_SHARED) != 0;
   // activations: hi copy at the start of each region, X3's lo copy right after it
   uint8_t *z = w + L.z, *h1 = w + L.h1, *h2 = w + L.h2;
   const int64_t zrows = (c.n + 255) / 256 * 256;  // z holds every cell of the call
@@ -703,7 +854,11 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
         (rc = make_map(&a3[1], W3, n->h2, n->h3, nets, Q1 / 2, KC, EB)) ||
         (rc = make_map(&a3[2], W3, n->h2, n->h3, nets, Q2 > 0 ? Q2 / 2 : Q1 / 2, KC, EB)))
       return rc;
-    a3[3] = a2[3];  // unused by the dot epilogue
+    if (shared) {  // layer 3 stores h3 = GELU(h2 W3^T + b3) for the layer-4 kernel
+      if ((rc = make_map(&a3[3], w + L.h3, n->h3, cap, 1, 32, 16, EB))) return rc;
+    } else {
+      a3[3] = a2[3];  // unused by the dot epilogue
+    }
   }
   // fused layers 1+2 (bf16, paper widths); RC_MLP_LAYERWISE forces the layer-wise path (comparisons)
   const bool fused = fused_path(n);
@@ -771,9 +926,17 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
       if ((rc = launch_l2_pair(NP, prec, m2, la, s))) return rc;
     }
     // layer 3 + folded layer 4: the same CTA-pair GEMM with the dot epilogue (K = h2, zero-filled to KC)
-    L2Args l3{mt, n->h3 / NP3, nets, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, n->d_w4, opart, cap, (n->h2 % KC) / KATOM};
-    if ((rc = launch_l2_pair(NP3, prec, m3, l3, s))) return rc;
-    EpiArgs ea{c0, rows, cap, nets, n->h3 / NP3, n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt, opart,
+    if (!shared) {
+      L2Args l3{mt, n->h3 / NP3, nets, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, n->d_w4, opart, cap, (n->h2 % KC) / KATOM};
+      if ((rc = launch_l2_pair(NP3, prec, m3, l3, s))) return rc;
+    } else {
+      // shared net (NEXT-2): layer 3 as a plain GELU layer into h3, then the n_out-wide layer 4
+      L2Args l3{mt, n->h3 / NP3, 1, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, nullptr, nullptr, cap, (n->h2 % KC) / KATOM};
+      l3.prof_stage = RC_STAGE_L3;
+      if ((rc = launch_l2_pair(NP3, prec, m3, l3, s))) return rc;
+      if ((rc = launch_l4(n, w + L.h3, opart, rows, cap, tf32, s))) return rc;
+    }
+    EpiArgs ea{c0, rows, cap, nout, shared ? 1 : n->h3 / NP3, n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt, opart,
                n->d_b4, n->d_ymean, n->d_ystd, m->d_P, m->d_thermo, n->d_species, qpart, {}};
     for (int q = 0; q <= 16; ++q) ea.binom[q] = q <= n->inv_lambda ? binom(n->inv_lambda, q) : 0.0;
     if ((rc = launch_epilogue(m, ea, c, s))) return rc;

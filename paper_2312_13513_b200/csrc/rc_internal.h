@@ -62,6 +62,7 @@ struct rc_mech {
 
 struct rc_mlp {
   int n_nets, d_in, h1, h2, h3, precision, ns, device;
+  int gnets;                      // nets the hidden-layer GEMMs run: n_nets, or 1 (RC_MLP_SHARED)
   int flags;                      // rc_mlp_desc.flags (RC_MLP_LAYERWISE)
   int kpad1;                      // padded K of layer 1 (64 bf16 / 32 fp32)
   double lambda_bc, dt;
@@ -72,7 +73,7 @@ struct rc_mlp {
   void *d_W1lo = nullptr, *d_W2lo = nullptr, *d_W3lo = nullptr;  // RC_TF32X3: tf32(W - W_hi)
   float *d_b1 = nullptr, *d_b2 = nullptr, *d_b3 = nullptr;  // [nets][N]
   void *d_b2k = nullptr, *d_b3k = nullptr;  // bf16: b2, b3 as K = 16 MMA operands [nets][N][16] = (hi, lo, 0...)
-  float *d_w4 = nullptr;                                    // [nets][h3]
+  float *d_w4 = nullptr;                                    // [n_nets][h3] (shared: the output layer)
   float *d_b4 = nullptr;                                    // [nets]
   float *d_xmean = nullptr, *d_xinvstd = nullptr;           // [d_in]
   double *d_ymean = nullptr, *d_ystd = nullptr;             // [nets]
