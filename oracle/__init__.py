@@ -64,6 +64,8 @@ def lib():
             ("orc_mlp_forward", d, [vp, i, vp]), ("orc_projection", i, [vp, vp]),
             ("orc_prologue_cell", None, [vp, vp, d, d, vp, vp, vp]), ("orc_step", i, [vp, vp, vp, i]),
             ("orc_pasr_kappa", d, [vp, d, vp, vp, d]),
+            ("orc_species_g", d, [vp, i, d]), ("orc_rate_constant", d, [vp, i, d, d]),
+            ("orc_kinetics_cell", None, [vp, vp, d, d, vp, vp, vp, vp]), ("orc_kinetics", i, [vp, vp, vp, vp, i]),
         ]:
             f = getattr(_lib, name)
             f.restype, f.argtypes = res, args
@@ -119,6 +121,8 @@ class Mech:
         Y = np.ascontiguousarray(Y, dtype=np.float64)
         w = np.ascontiguousarray(wdot, dtype=np.float64)
         return lib().orc_pasr_kappa(self.ref, rho, _p(Y), _p(w), tau_mix)
+
+    def g_k(self, k, T): return lib().orc_species_g(self.ref, k, T)
 
     def projection(self):
         P = np.empty((self.ns, self.ns))
@@ -185,6 +189,56 @@ def step(mech: Mech, mlp: "Mlp | None", T, p, Y, h=None, mode: str = "h", transp
     rc = lib().orc_step(mech.ref, mlp.ref if do_chem else None, C.byref(c), nthreads)
     if rc != 0:
         raise RuntimeError(f"orc_step failed: {rc}")
+    out["red"] = np.array(c.red[:])
+    out["diag"] = np.array(c.diag[:], dtype=np.int64)
+    return out
+
+
+class _Kin(C.Structure):
+    _fields_ = [("nr", C.c_int32), ("nu_f", C.c_void_p), ("nu_r", C.c_void_p), ("type", C.c_void_p),
+                ("reversible", C.c_void_p), ("A", C.c_void_p), ("b", C.c_void_p), ("Ea", C.c_void_p),
+                ("eff", C.c_void_p), ("A0", C.c_void_p), ("b0", C.c_void_p), ("Ea0", C.c_void_p), ("troe", C.c_void_p)]
+
+
+KIN_KEYS = [("nu_f", np.int32), ("nu_r", np.int32), ("type", np.int32), ("reversible", np.int32), ("A", np.float64),
+            ("b", np.float64), ("Ea", np.float64), ("eff", np.float64), ("A0", np.float64), ("b0", np.float64),
+            ("Ea0", np.float64), ("troe", np.float64)]
+
+
+class Kin:
+    """Oracle view of a workload.load_kinetics() dict (detailed kinetics, NEXT-3)."""
+
+    def __init__(self, k: dict):
+        self.keep = {key: np.ascontiguousarray(k[key], dtype=dt) for key, dt in KIN_KEYS}
+        self.nr = int(k["nr"])
+        self.s = _Kin(self.nr, *[_p(self.keep[key]) for key, _ in KIN_KEYS])
+        self.ref = C.byref(self.s)
+
+    def rate_constant(self, r, T, M):
+        return lib().orc_rate_constant(self.ref, r, T, M)
+
+    def cell(self, mech: Mech, T, p, Y):
+        """(wdot[ns], q_net[nr], gross-rate scale[ns]) of one cell."""
+        Y = np.ascontiguousarray(Y, dtype=np.float64)
+        w, q, sc = np.empty(mech.ns), np.empty(self.nr), np.empty(mech.ns)
+        lib().orc_kinetics_cell(mech.ref, self.ref, T, p, _p(Y), _p(w), _p(q), _p(sc))
+        return w, q, sc
+
+
+def kinetics(mech: Mech, kin: Kin, T, p, Y, tau_mix=None, nthreads: int = 0) -> dict:
+    """Detailed-kinetics sources of a field (T given): wdot[ns][n], qdot, wscale[ns][n], red, diag."""
+    n = int(np.asarray(T).shape[0])
+    ns = mech.ns
+    T = np.ascontiguousarray(T, dtype=np.float64)
+    p = np.ascontiguousarray(p, dtype=np.float64)
+    Y = np.ascontiguousarray(Y, dtype=np.float64)
+    out = {"wdot": np.empty((ns, n)), "qdot": np.empty(n), "wscale": np.empty((ns, n))}
+    c = _Cells(n, n, 1, None, _p(T), _p(p), _p(Y), None, None, None, None, None, None, _p(out["wdot"]),
+               _p(out["qdot"]))
+    tau = None if tau_mix is None else np.ascontiguousarray(tau_mix, dtype=np.float64)
+    c.tau_mix = _p(tau)
+    if lib().orc_kinetics(mech.ref, kin.ref, C.byref(c), _p(out["wscale"]), nthreads) != 0:
+        raise RuntimeError("orc_kinetics failed")
     out["red"] = np.array(c.red[:])
     out["diag"] = np.array(c.diag[:], dtype=np.int64)
     return out

@@ -519,3 +519,165 @@ int orc_step(const orc_mech *m, const orc_mlp *n, orc_cells *c, int nthreads) {
   c->red[1] = s + comp;
   return 0;
 }
+
+
+/* ====================================================================== detailed kinetics (NEXT-3)
+ * Mass-action law (textbook; the CVODE path's right-hand side), R21:
+ *   C_k = rho Y_k / W_k                                   [kmol/m^3]
+ *   k_f = A T^b exp(-Ea / (R_u T))
+ *   three-body: q *= [M],  [M] = sum_k eff_k C_k
+ *   falloff: Pr = k0 [M] / k_inf, k_f = k_inf Pr / (1 + Pr) F, F = 1 (Lindemann) or Troe:
+ *     Fcent = (1 - a) exp(-T/T3) + a exp(-T/T1) + exp(-T2/T)   (T3, T1, T2 = Troe's T***, T*, T**)
+ *     c = -0.4 - 0.67 log10 Fcent, n = 0.75 - 1.27 log10 Fcent, d = 0.14
+ *     log10 F = log10 Fcent / (1 + ((log10 Pr + c) / (n - d (log10 Pr + c)))^2)
+ *   K_c = exp(-sum_k nu_k g_k) (p0 / (R_u T))^(sum_k nu_k),  nu = nu_r - nu_f, p0 = 101325 Pa
+ *   q = k_f (prod_k C_k^nu_f - prod_k C_k^nu_r / K_c)
+ *   wdot_k = W_k sum_r nu_rk q_r,   qdot = -sum_k h_k wdot_k  */
+#define ORC_P0 101325.0
+
+double orc_species_g(const orc_mech *m, int k, double T) {
+  const double *a = nasa_coeffs(m, k, T);
+  /* h/RT = a1 + a2 T/2 + a3 T^2/3 + a4 T^3/4 + a5 T^4/5 + a6/T
+   * s/R  = a1 ln T + a2 T + a3 T^2/2 + a4 T^3/3 + a5 T^4/4 + a7 */
+  double hRT = a[0] + a[1] * T / 2.0 + a[2] * T * T / 3.0 + a[3] * T * T * T / 4.0 + a[4] * T * T * T * T / 5.0 + a[5] / T;
+  double sR = a[0] * log(T) + a[1] * T + a[2] * T * T / 2.0 + a[3] * T * T * T / 3.0 + a[4] * T * T * T * T / 4.0 + a[6];
+  return hRT - sR;
+}
+
+double orc_rate_constant(const orc_kin *kin, int r, double T, double M) {
+  double kinf = kin->A[r] * pow(T, kin->b[r]) * exp(-kin->Ea[r] / (ORC_RU * T));
+  if (kin->type[r] != 2) return kinf;
+  double k0 = kin->A0[r] * pow(T, kin->b0[r]) * exp(-kin->Ea0[r] / (ORC_RU * T));
+  double Pr = k0 * M / kinf;
+  double F = 1.0;
+  const double *tr = kin->troe + 4 * r;
+  if (tr[0] >= 0.0) {
+    double Fcent = (1.0 - tr[0]) * exp(-T / tr[1]) + tr[0] * exp(-T / tr[2]) + exp(-tr[3] / T);
+    double lF = log10(Fcent);
+    double c = -0.4 - 0.67 * lF, n = 0.75 - 1.27 * lF, d = 0.14;
+    double x = (log10(Pr) + c) / (n - d * (log10(Pr) + c));
+    F = pow(10.0, lF / (1.0 + x * x));
+  }
+  return kinf * (Pr / (1.0 + Pr)) * F;
+}
+
+void orc_kinetics_cell(const orc_mech *m, const orc_kin *kin, double T, double p, const double *Y, double *wdot,
+                       double *qnet, double *scale) {
+  int ns = m->ns;
+  double C[64], g[64];
+  double rho = p * orc_mix_W(m, Y) / (ORC_RU * T);
+  for (int k = 0; k < ns; ++k) {
+    C[k] = rho * Y[k] / species_W(m, k);
+    g[k] = orc_species_g(m, k, T);
+    wdot[k] = 0.0;
+    if (scale) scale[k] = 0.0;
+  }
+  for (int r = 0; r < kin->nr; ++r) {
+    const int32_t *nf = kin->nu_f + (int64_t)r * ns, *nr = kin->nu_r + (int64_t)r * ns;
+    double M = 0.0;
+    for (int k = 0; k < ns; ++k) M += kin->eff[(int64_t)r * ns + k] * C[k];
+    double kf = orc_rate_constant(kin, r, T, M);
+    double fwd = kf, rev = 0.0;
+    for (int k = 0; k < ns; ++k)
+      for (int j = 0; j < nf[k]; ++j) fwd *= C[k];
+    if (kin->reversible[r]) {
+      double sg = 0.0;
+      int dnu = 0;
+      for (int k = 0; k < ns; ++k) {
+        sg += (nr[k] - nf[k]) * g[k];
+        dnu += nr[k] - nf[k];
+      }
+      double Kc = exp(-sg) * pow(ORC_P0 / (ORC_RU * T), dnu);
+      rev = kf / Kc;
+      for (int k = 0; k < ns; ++k)
+        for (int j = 0; j < nr[k]; ++j) rev *= C[k];
+    }
+    if (kin->type[r] == 1) {
+      fwd *= M;
+      rev *= M;
+    }
+    double q = fwd - rev;
+    if (qnet) qnet[r] = q;
+    for (int k = 0; k < ns; ++k) {
+      int nu = nr[k] - nf[k];
+      if (nu) wdot[k] += nu * q;
+      if (scale && (nf[k] || nr[k])) scale[k] += (nf[k] + nr[k]) * (fabs(fwd) + fabs(rev));
+    }
+  }
+  for (int k = 0; k < ns; ++k) {
+    wdot[k] *= species_W(m, k);
+    if (scale) scale[k] *= species_W(m, k);
+  }
+}
+
+typedef struct {
+  const orc_mech *m;
+  const orc_kin *kin;
+  orc_cells *c;
+  double *wscale;
+  int64_t c0, c1;
+  int64_t bad;
+} kjob_t;
+
+static void *run_kin(void *arg) {
+  kjob_t *J = (kjob_t *)arg;
+  const orc_mech *m = J->m;
+  orc_cells *c = J->c;
+  int ns = m->ns;
+  int64_t ld = c->ld;
+  double Y[64], w[64], sc[64];
+  for (int64_t i = J->c0; i < J->c1; ++i) {
+    for (int k = 0; k < ns; ++k) Y[k] = c->Y[k * ld + i];
+    double T = c->T[i], p = c->p[i];
+    orc_kinetics_cell(m, J->kin, T, p, Y, w, NULL, sc);
+    if (c->tau_mix) {
+      double rho = p * orc_mix_W(m, Y) / (ORC_RU * T);
+      double kappa = orc_pasr_kappa(m, rho, Y, w, c->tau_mix[i]);
+      for (int k = 0; k < ns; ++k) w[k] = kappa * w[k];
+    }
+    double q = 0.0;
+    int bad = 0;
+    for (int k = 0; k < ns; ++k) {
+      c->wdot[k * ld + i] = w[k];
+      if (J->wscale) J->wscale[k * ld + i] = sc[k];
+      q -= orc_species_h(m, k, T) * w[k];
+      bad |= !isfinite(w[k]);
+    }
+    if (c->qdot) c->qdot[i] = q;
+    J->bad += bad | !isfinite(q);
+  }
+  return NULL;
+}
+
+int orc_kinetics(const orc_mech *m, const orc_kin *kin, orc_cells *c, double *wscale, int nthreads) {
+  if (!m || !kin || !c || !c->wdot || m->ns <= 0 || m->ns > 64 || c->n < 0 || c->ld < c->n) return -1;
+  int nt = nthreads > 0 ? nthreads : ncpu();
+  if (nt > c->n) nt = c->n > 0 ? (int)c->n : 1;
+  kjob_t *jobs = calloc((size_t)nt, sizeof(kjob_t));
+  pthread_t *th = calloc((size_t)nt, sizeof(pthread_t));
+  for (int t = 0; t < nt; ++t) {
+    jobs[t].m = m; jobs[t].kin = kin; jobs[t].c = c; jobs[t].wscale = wscale;
+    jobs[t].c0 = c->n * t / nt;
+    jobs[t].c1 = c->n * (t + 1) / nt;
+    pthread_create(&th[t], NULL, run_kin, &jobs[t]);
+  }
+  for (int k = 0; k < 5; ++k) c->diag[k] = 0;
+  for (int t = 0; t < nt; ++t) {
+    pthread_join(th[t], NULL);
+    c->diag[2] += jobs[t].bad;
+  }
+  free(jobs);
+  free(th);
+  double Tmax = -INFINITY, s = 0.0, comp = 0.0;
+  for (int64_t i = 0; i < c->n; ++i) {
+    if (c->T[i] > Tmax) Tmax = c->T[i];
+    if (c->qdot) {
+      double v = c->qdot[i], t = s + v;
+      comp += (fabs(s) >= fabs(v)) ? (s - t) + v : (v - t) + s;
+      s = t;
+    }
+  }
+  c->red[0] = Tmax;
+  c->red[1] = s + comp;
+  return 0;
+}

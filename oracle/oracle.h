@@ -78,6 +78,29 @@ void orc_prologue_cell(const orc_mech *m, const orc_mlp *n, double T, double p, 
  * tau_c = sum_k rho max(Y_k,0)/W_k / (1/2 sum_k |wdot_k|/W_k); kappa = 1 when wdot = 0 */
 double orc_pasr_kappa(const orc_mech *m, double rho, const double *Y, const double *wdot, double tau_mix);
 
+/* ---- detailed kinetics (reading R21): the CVODE path's right-hand
+ * side ("CVODE on CPU"), mass-action law with Arrhenius rates, reverse rates from the
+ * equilibrium constant of the NASA-7 tables, third-body and Lindemann/Troe falloff forms ---- */
+typedef struct {
+  int32_t nr;
+  const int32_t *nu_f, *nu_r;   /* [nr][ns] reactant / product stoichiometric coefficients */
+  const int32_t *type;          /* [nr] 0 elementary, 1 three-body (+M), 2 falloff (+M) */
+  const int32_t *reversible;    /* [nr] */
+  const double *A, *b, *Ea;     /* [nr] k = A T^b exp(-Ea / (R_u T)); SI (kmol, m^3, s, J/kmol) */
+  const double *eff;            /* [nr][ns] third-body efficiencies */
+  const double *A0, *b0, *Ea0;  /* [nr] falloff low-pressure limit k0 */
+  const double *troe;           /* [nr][4] a, T3, T1, T2 (Troe's T***, T*, T**); a < 0: Lindemann (F = 1) */
+} orc_kin;
+
+/* g_k = h_k/(R_u T) - s_k/R_u (molar, dimensionless) of species k at T (NASA-7) */
+double orc_species_g(const orc_mech *m, int k, double T);
+/* forward rate constant of reaction r at T with third-body concentration M (falloff blending) */
+double orc_rate_constant(const orc_kin *kin, int r, double T, double M);
+/* one cell: wdot[ns] (kg/m^3/s); qnet[nr] rates of progress (kmol/m^3/s, may be NULL);
+ * scale[ns] = W_k sum_r |nu_rk| (|q_f,r| + |q_r,r|), the gross rates (may be NULL) */
+void orc_kinetics_cell(const orc_mech *m, const orc_kin *kin, double T, double p, const double *Y, double *wdot,
+                       double *qnet, double *scale);
+
 /* ---- whole-field entry points (SoA, host arrays) ---- */
 typedef struct {
   int64_t n, ld;
@@ -96,6 +119,11 @@ typedef struct {
 /* a1 (+cp, rho); a2 if mu/lambda/D non-NULL; a3-a5 if mlp != NULL and wdot != NULL; a6 reductions.
  * nthreads <= 0 -> all online cores.  Returns 0 on success, <0 on bad arguments. */
 int orc_step(const orc_mech *m, const orc_mlp *n, orc_cells *c, int nthreads);
+
+/* detailed-kinetics sources of every cell at the given T (T-mode values), p, Y: wdot, qdot (PaSR
+ * scaled if c->tau_mix), red = {max T, sum qdot}; wscale [ns][ld] (may be NULL) = the gross rates
+ * W_k sum_r |nu_rk| (|q_f| + |q_r|) of each cell (the parity scale of wdot).  Returns 0 ok. */
+int orc_kinetics(const orc_mech *m, const orc_kin *kin, orc_cells *c, double *wscale, int nthreads);
 
 #ifdef __cplusplus
 }

@@ -8,9 +8,9 @@ MLP or projection math); it only reads tables, draws random numbers and shapes
 profiles.  Every value is a pure function of (SEED, field, global cell index),
 so a shard of cells generated on its own equals the same cells of the whole.
 """
-from .mech import load_mech
+from .mech import load_kinetics, load_mech
 from .cells import CONFIGS, make_cells, make_cells_at, tau_mix_at, Config
 from .bundle import make_bundle
 
 SEED = 231213513
-__all__ = ["load_mech", "make_cells", "make_cells_at", "tau_mix_at", "make_bundle", "CONFIGS", "Config", "SEED"]
+__all__ = ["load_mech", "load_kinetics", "make_cells", "make_cells_at", "tau_mix_at", "make_bundle", "CONFIGS", "Config", "SEED"]

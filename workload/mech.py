@@ -33,3 +33,19 @@ def load_mech(name: str) -> dict:
     for k in ("atoms", "nasa_lo", "nasa_hi", "visc", "cond", "diff"):
         m[k] = np.ascontiguousarray(m[k])
     return m
+
+
+def load_kinetics(name: str) -> dict:
+    """Detailed-kinetics table data/mech/<name>_kin.json (SI) -> numpy arrays:
+    nu_f, nu_r [nr][ns] int32; type [nr] (0 elementary, 1 three-body, 2 falloff); reversible [nr];
+    A, b, Ea [nr] (k = A T^b exp(-Ea / (R_u T))); eff [nr][ns] third-body efficiencies; A0, b0, Ea0
+    [nr] low-pressure limit (falloff); troe [nr][4] = (a, T***, T*, T**), a < 0: Lindemann."""
+    with open(os.path.join(DATA, name + "_kin.json")) as f:
+        j = json.load(f)
+    R = j["reactions"]
+    k = {"name": j["name"], "species": list(j["species"]), "nr": len(R)}
+    for key, dt in (("nu_f", np.int32), ("nu_r", np.int32), ("type", np.int32), ("reversible", np.int32),
+                    ("A", np.float64), ("b", np.float64), ("Ea", np.float64), ("eff", np.float64),
+                    ("A0", np.float64), ("b0", np.float64), ("Ea0", np.float64), ("troe", np.float64)):
+        k[key] = np.ascontiguousarray(np.array([r[key] for r in R], dtype=dt))
+    return k
