@@ -30,6 +30,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 SUSTAINED = "bf16_tflops_sustained"
+# executed FP64-pipe instructions per cell of kinetics_kernel (ncu, profiles/ncu_kinetics_r02.json)
+KIN_FP64_INSTR_PER_CELL = {"h2_9sp": 1180}
 
 
 def parse():
@@ -44,6 +46,8 @@ def parse():
     ap.add_argument("--layerwise", action="store_true", help="rc_mlp_desc.flags = RC_MLP_LAYERWISE (comparison path)")
     ap.add_argument("--pasr", action="store_true", help="LES: PaSR scaling of wdot with per-cell tau_mix (NEXT-4)")
     ap.add_argument("--shared", action="store_true", help="one shared net with n_nets outputs (NEXT-2)")
+    ap.add_argument("--chem", default="dnn", choices=["dnn", "kinetics"],
+                    help="source term: the DNN (the paper's GPU path) or detailed kinetics (NEXT-3, the CVODE RHS)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle baseline")
@@ -170,6 +174,9 @@ def algorithmic(cfg, bundle, ns, n, precision="bf16"):
         "L3_flops": n * nets * 2 * (h2 * h3 + (0 if bundle.get("shared") else h3)),
         "L4_flops": n * 2 * h3 * nout if bundle.get("shared") else 0,
         "L4_bytes": n * (h3 * eb + nout * 4) if bundle.get("shared") else 0,  # h3 read, o written
+        # detailed kinetics: FP64-pipe instructions per cell executed by the kernel (ncu
+        # sm__inst_executed_pipe_fp64 per cell, profiles/ncu_kinetics_r02.json), x 2 flop per DFMA slot
+        "kinetics_fp64_flops": n * 2 * KIN_FP64_INSTR_PER_CELL.get(cfg.mech, 0),
         "mlp_flops": n * nets * flops_net,
         "L1_bytes": n * nets * h1 * eb,               # h1 activations written
         # in: raw outputs o (fp32 per net), T, rho, Y; out: wdot, qdot
@@ -215,10 +222,20 @@ def run_ours(a):
     ws = rc.aligned_workspace(mlp, n)
     reduce_a6 = GlobalReductions("cuda")
     cells = st.cells(rc.RC_MODE_H, dt=bundle["dt"])
+    if a.chem == "kinetics":
+        from workload import load_kinetics
+        kin = rc.Kinetics(mech, load_kinetics(cfg.mech))
 
     def step():
         st.T[:n].copy_(T_guess)                       # each step restarts Newton from the same guess
-        rc.rc_step(mech, mlp, cells, ws, stream)
+        if a.chem == "kinetics":                       # a1 + a2 + detailed kinetics instead of a3-a5
+            st.red.zero_()
+            st.diag.zero_()
+            rc.rc_thermo(mech, cells, stream)
+            rc.rc_transport(mech, cells, stream)
+            rc.rc_kinetics(mech, kin, cells, stream)
+        else:
+            rc.rc_step(mech, mlp, cells, ws, stream)
         reduce_a6(st.red, st.diag)                     # a6: global max T and sums (NCCL over NVLink; no-op at N=1)
 
     for _ in range(a.warmup):
@@ -251,7 +268,7 @@ def run_ours(a):
 
     # ---- end to end through the C ABI from pinned HOST buffers (H2D in, D2H out, every step)
     e2e = None
-    if not a.no_e2e:
+    if not a.no_e2e and a.chem == "dnn":
         e2e = run_e2e(a, rc, mech, mlp, bundle, host, st, ws, n, ns, world, stream)
 
     out = None
@@ -279,6 +296,7 @@ def run_ours(a):
             ("L12", alg["L1_flops"] + alg["L2_flops"], "TFLOP/s", "tensor", tpeak),  # fused layers 1+2
             ("L3", alg["L3_flops"], "TFLOP/s", "tensor", tpeak),
             ("L4", alg["L4_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),  # shared net's output layer (CUDA cores)
+            ("kinetics", alg["kinetics_fp64_flops"], "TFLOP/s", "fp64", f64),  # detailed kinetics (NEXT-3)
             ("epilogue", alg["epilogue_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),
         ]:
             t_ms, cnt = per(st_name)
@@ -322,7 +340,8 @@ def run_ours(a):
                        "l2": "working set > L2 (h2 of 262144-cell chunks x 8 nets 3.4 GB, z 32 MB; "
                              "cell state 0.2 GB) - no flush needed",
                        "precision": a.precision, **({"les_pasr": True} if a.pasr else {}),
-                       **({"mlp": "one shared net, n_nets outputs (NEXT-2)"} if a.shared else {})},
+                       **({"mlp": "one shared net, n_nets outputs (NEXT-2)"} if a.shared else {}),
+                       **({"chem": "detailed kinetics, 12 reactions (NEXT-3)"} if a.chem == "kinetics" else {})},
             "roofline": {"kernel": ("fused L1+L2 (z -> h1 1600 on chip -> h2 800, tcgen05 bf16, 4-CTA clusters)"
                                     if fused else "L2 GEMM (h1 1600 -> h2 800, tcgen05)"), "bound": "tensor",
                          "achieved": l2.get("achieved"), "peak": tpeak, "unit": "TFLOP/s",
@@ -342,7 +361,7 @@ def run_ours(a):
         dist.barrier()
     # ---- CPU oracle baseline, rank 0 at N = 1 only
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(cfg, bundle, mech_d, a.cpu_seconds)
+        out["cpu_baseline"] = cpu_baseline(cfg, bundle, mech_d, a.cpu_seconds, a.chem)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -440,18 +459,23 @@ def run_e2e(a, rc, mech, mlp, bundle, host, st, ws, n, ns, world, stream):
                    f"rc_combine_reductions + NCCL for a6"}
 
 
-def oracle_time(cfg, bundle, mech_d, idx):
+def oracle_time(cfg, bundle, mech_d, idx, chem="dnn"):
     import oracle
-    from workload import make_cells_at
+    from workload import load_kinetics, make_cells_at
     c = make_cells_at(cfg, idx)
     om, ob = oracle.Mech(mech_d), oracle.Mlp(bundle)
     h = oracle.step(om, None, c["T_true"], c["p"], c["Y"], mode="T", transport=False, chem=False)["h"]
+    kin = oracle.Kin(load_kinetics(cfg.mech)) if chem == "kinetics" else None
     t0 = time.perf_counter()
-    oracle.step(om, ob, c["T_guess"], c["p"], c["Y"], h=h)
+    if kin is None:
+        oracle.step(om, ob, c["T_guess"], c["p"], c["Y"], h=h)
+    else:  # a1 + a2, then the detailed-kinetics sources at the converged T
+        r = oracle.step(om, None, c["T_guess"], c["p"], c["Y"], h=h, chem=False)
+        oracle.kinetics(om, kin, r["T"], c["p"], c["Y"])
     return time.perf_counter() - t0
 
 
-def cpu_baseline(cfg, bundle, mech_d, seconds):
+def cpu_baseline(cfg, bundle, mech_d, seconds, chem="dnn"):
     """The fp64 oracle as it stands, on the box's host cores, on a bounded hashed sample."""
     import oracle
     from workload.cells import uniform
@@ -460,13 +484,14 @@ def cpu_baseline(cfg, bundle, mech_d, seconds):
     n_all = cfg.n_cells
     # probe with several cells per core (a 1-cell-per-thread probe overstates the per-cell cost)
     probe = np.unique((uniform(777, np.arange(max(64, 8 * cores))) * n_all).astype(np.int64))
-    t_probe = oracle_time(cfg, bundle, mech_d, probe)
+    t_probe = oracle_time(cfg, bundle, mech_d, probe, chem)
     per_cell = t_probe / probe.size
     m = int(min(n_all, max(probe.size, seconds / max(per_cell, 1e-9))))
     idx = np.unique((uniform(778, np.arange(m)) * n_all).astype(np.int64))
-    t = oracle_time(cfg, bundle, mech_d, idx)
+    t = oracle_time(cfg, bundle, mech_d, idx, chem)
+    what = "full step a1-a5" if chem == "dnn" else "a1 + a2 + detailed kinetics"
     return {"value": round(idx.size / t / 1e6, 8), "unit": "Mcells/s", "cores": cores, "kind": "oracle",
-            "sample": f"{idx.size} hashed-random cells of {cfg.name} (full step a1-a5, fp64, {t:.1f} s)"}
+            "sample": f"{idx.size} hashed-random cells of {cfg.name} ({what}, fp64, {t:.1f} s)"}
 
 
 def run_reference(a):

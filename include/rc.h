@@ -195,6 +195,39 @@ int rc_chem(const rc_mech *m, const rc_mlp *n, const rc_cells *c, void *ws, size
 /* a1 + a2 + a3-a5 in order on one stream; zeroes red and diag first. */
 int rc_step(const rc_mech *m, const rc_mlp *n, const rc_cells *c, void *ws, size_t ws_bytes, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Detailed kinetics (reading R21): the right-hand side the paper's
+ * CVODE option integrates ("CVODE ... on CPU or DNN on GPU"; the 9-species /
+ * 12-reaction H2 mechanism of PAPER.md:231) -- an alternative source term to the DNN, per cell:
+ *   C_k = rho Y_k / W_k with rho = p W / (R_u T);  k = A T^b exp(-Ea / (R_u T))
+ *   three-body: q *= [M], [M] = sum_k eff_k C_k;  falloff: k = k_inf Pr / (1 + Pr) F,
+ *   Pr = k0 [M] / k_inf, F = 1 (Lindemann, troe[0] < 0) or Troe with
+ *   Fcent = (1 - a) exp(-T/T3) + a exp(-T/T1) + exp(-T2/T), troe = {a, T3, T1, T2}
+ *   K_c = exp(-sum_k nu_k g_k) (p0 / (R_u T))^(sum_k nu_k), g_k = h_k/(R_u T) - s_k/R_u (NASA-7 a1..a7),
+ *   p0 = 101325 Pa, nu = nu_r - nu_f;  q = k (prod C^nu_f - prod C^nu_r / K_c) (reverse term only if
+ *   reversible);  wdot_k = W_k sum_r nu_rk q_r;  qdot = -sum_k h_k(T) wdot_k.
+ * HOST pointers, SI units (kmol, m^3, s, J/kmol), copied at create.  At most 3 reactant and 3 product
+ * molecules per reaction (RC_EUNSUPPORTED otherwise).
+ * ------------------------------------------------------------------------- */
+typedef struct rc_kin rc_kin;
+enum { RC_RX_ELEMENTARY = 0, RC_RX_THREE_BODY = 1, RC_RX_FALLOFF = 2 };
+typedef struct {
+  int32_t nr;                     /* reactions */
+  const int32_t *nu_f, *nu_r;     /* [nr][ns] stoichiometric coefficients of reactants / products */
+  const int32_t *type;            /* [nr] RC_RX_* */
+  const int32_t *reversible;      /* [nr] 0 / 1 */
+  const double *A, *b, *Ea;       /* [nr] (high-pressure limit for falloff) */
+  const double *eff;              /* [nr][ns] third-body efficiencies (three-body and falloff) */
+  const double *A0, *b0, *Ea0;    /* [nr] low-pressure limit (falloff) */
+  const double *troe;             /* [nr][4] a, T3, T1, T2 (falloff); a < 0: Lindemann */
+} rc_kin_desc;
+int rc_kin_create(const rc_mech *m, const rc_kin_desc *desc, rc_kin **out);
+void rc_kin_destroy(rc_kin *k);
+/* wdot, qdot of every cell from T (as stored: run after rc_thermo), p, Y; PaSR-scaled if tau_mix;
+ * red[1] = sum qdot (deterministic; one rc_kinetics in flight per handle), diag nonfinite counted.
+ * Errors: RC_EINVAL (NULL wdot), RC_EALIGN, RC_ECUDA. */
+int rc_kinetics(const rc_mech *m, const rc_kin *k, const rc_cells *c, void *stream);
+
 /* Step a6 on one device for a step run as k sub-batches (e.g. to overlap the host
  * copies of one batch with the compute of another, each rc_step writing its own
  * red/diag): red = {max_i red_parts[i][0], sum_i red_parts[i][1]} (sum in index
@@ -222,7 +255,8 @@ enum {
   RC_STAGE_L3 = 5, RC_STAGE_EPILOGUE = 6, RC_STAGE_FINALIZE = 7,
   RC_STAGE_L12 = 8,  /* fused layers 1+2 (bf16 at the paper widths; replaces L1 and L2) */
   RC_STAGE_L4 = 9,   /* layer 4 of the shared net (RC_MLP_SHARED) */
-  RC_STAGE_COUNT = 10
+  RC_STAGE_KINETICS = 10, /* detailed kinetics (rc_kinetics) */
+  RC_STAGE_COUNT = 11
 };
 int rc_profile_enable(int on);
 int rc_profile_read(double *ms /* [RC_STAGE_COUNT] */, int64_t *launches /* [RC_STAGE_COUNT] */, int reset);

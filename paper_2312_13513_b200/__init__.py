@@ -11,11 +11,11 @@ PyTorch is used only for device memory, streams and torch.distributed.
 import numpy as np
 
 from . import _rc
-from ._rc import (RC_BF16, RC_TF32, RC_TF32X3, RC_MODE_H, RC_MODE_T, DIAG_NAMES, Mechanism, MLPBundle, RcError, lib,
-                  make_cells, rc_chem, rc_combine_reductions, rc_last_launch_count, rc_partition, rc_profile_enable, rc_profile_read, rc_step,
+from ._rc import (RC_BF16, RC_TF32, RC_TF32X3, RC_MODE_H, RC_MODE_T, DIAG_NAMES, Kinetics, Mechanism, MLPBundle, RcError,
+                  lib, make_cells, rc_chem, rc_kinetics, rc_combine_reductions, rc_last_launch_count, rc_partition, rc_profile_enable, rc_profile_read, rc_step,
                   rc_thermo, rc_transport, STAGES)
 
-__all__ = ["Mechanism", "MLPBundle", "CellState", "RcError", "RC_BF16", "RC_TF32", "RC_TF32X3", "RC_MODE_H", "RC_MODE_T",
+__all__ = ["Mechanism", "MLPBundle", "Kinetics", "rc_kinetics", "CellState", "RcError", "RC_BF16", "RC_TF32", "RC_TF32X3", "RC_MODE_H", "RC_MODE_T",
            "rc_step", "rc_thermo", "rc_transport", "rc_chem", "rc_partition", "rc_combine_reductions",
            "rc_last_launch_count", "lib",
            "DIAG_NAMES", "make_cells", "rc_profile_enable", "rc_profile_read", "STAGES", "aligned_workspace"]
@@ -28,7 +28,9 @@ class CellState:
     qdot, o[n_nets][ld], red[2], diag[5].
     """
 
-    def __init__(self, n, ns, n_nets=0, device="cuda", ld=None, outputs=("cp", "rho", "mu", "lam", "D", "wdot", "qdot", "o")):
+    def __init__(self, n, ns, n_nets=0, device="cuda", ld=None, outputs=("cp", "rho", "mu", "lam", "D", "wdot", "qdot", "o"),
+                 sources=False):
+        """sources=True allocates wdot / qdot without an MLP (detailed kinetics, rc_kinetics)."""
         import torch
         self.n, self.ns, self.n_nets = int(n), int(ns), int(n_nets)
         self.ld = int(ld) if ld is not None else max(2, (self.n + 31) // 32 * 32)
@@ -43,8 +45,8 @@ class CellState:
         self.mu = torch.zeros(ld, **f64) if "mu" in outputs else None
         self.lam = torch.zeros(ld, **f64) if "lam" in outputs else None
         self.D = torch.zeros(ns, ld, **f64) if "D" in outputs else None
-        self.wdot = torch.zeros(ns, ld, **f64) if ("wdot" in outputs and n_nets) else None
-        self.qdot = torch.zeros(ld, **f64) if ("qdot" in outputs and n_nets) else None
+        self.wdot = torch.zeros(ns, ld, **f64) if ("wdot" in outputs and (n_nets or sources)) else None
+        self.qdot = torch.zeros(ld, **f64) if ("qdot" in outputs and (n_nets or sources)) else None
         self.o = torch.zeros(max(n_nets, 1), ld, dtype=torch.float32, device=device) if ("o" in outputs and n_nets) else None
         self.red = torch.zeros(2, **f64)
         self.diag = torch.zeros(5, dtype=torch.int64, device=device)

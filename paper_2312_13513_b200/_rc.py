@@ -48,6 +48,12 @@ class rc_cells(C.Structure):
                 ("tau_mix", C.c_void_p)]
 
 
+class rc_kin_desc(C.Structure):
+    _fields_ = [("nr", C.c_int32), ("nu_f", C.c_void_p), ("nu_r", C.c_void_p), ("type", C.c_void_p),
+                ("reversible", C.c_void_p), ("A", C.c_void_p), ("b", C.c_void_p), ("Ea", C.c_void_p),
+                ("eff", C.c_void_p), ("A0", C.c_void_p), ("b0", C.c_void_p), ("Ea0", C.c_void_p), ("troe", C.c_void_p)]
+
+
 EXPORTS = {
     # name: (restype, argtypes)
     "rc_mech_create": (C.c_int, [C.POINTER(rc_mech_desc), C.POINTER(C.c_void_p)]),
@@ -62,6 +68,9 @@ EXPORTS = {
     "rc_step": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(rc_cells), C.c_void_p, C.c_size_t, C.c_void_p]),
     "rc_partition": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "rc_combine_reductions": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rc_kin_create": (C.c_int, [C.c_void_p, C.POINTER(rc_kin_desc), C.POINTER(C.c_void_p)]),
+    "rc_kin_destroy": (None, [C.c_void_p]),
+    "rc_kinetics": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(rc_cells), C.c_void_p]),
     "rc_last_launch_count": (C.c_int64, []),
     "rc_profile_enable": (C.c_int, [C.c_int]),
     "rc_profile_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
@@ -161,6 +170,31 @@ class MLPBundle:
             self.h = None
 
 
+class Kinetics:
+    """rc_kin handle (detailed kinetics, NEXT-3) from a workload.load_kinetics() dict (SI)."""
+
+    KEYS = [("nu_f", np.int32), ("nu_r", np.int32), ("type", np.int32), ("reversible", np.int32),
+            ("A", np.float64), ("b", np.float64), ("Ea", np.float64), ("eff", np.float64), ("A0", np.float64),
+            ("b0", np.float64), ("Ea0", np.float64), ("troe", np.float64)]
+
+    def __init__(self, mech: Mechanism, k: dict):
+        keep = {key: _np(k[key], dt) for key, dt in self.KEYS}
+        d = rc_kin_desc(int(k["nr"]), *[keep[key].ctypes.data for key, _ in self.KEYS])
+        h = C.c_void_p()
+        check(lib().rc_kin_create(mech.h, C.byref(d), C.byref(h)))
+        self.h = h
+        self.nr = int(k["nr"])
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.rc_kin_destroy(self.h)
+            self.h = None
+
+
+def rc_kinetics(mech, kin, cells, stream=None):
+    return check(lib().rc_kinetics(mech.h, kin.h, C.byref(cells), _stream(stream)))
+
+
 def make_cells(n, ld, mode, T, p, Y, h=None, cp=None, rho=None, mu=None, lam=None, D=None, wdot=None, qdot=None,
                o=None, dt=0.0, red=None, diag=None, tau_mix=None):
     """rc_cells struct from torch device tensors (component-major, stride ld)."""
@@ -205,7 +239,7 @@ def rc_last_launch_count():
     return int(lib().rc_last_launch_count())
 
 
-STAGES = ["thermo", "transport", "prologue", "L1", "L2", "L3", "epilogue", "finalize", "L12", "L4"]
+STAGES = ["thermo", "transport", "prologue", "L1", "L2", "L3", "epilogue", "finalize", "L12", "L4", "kinetics"]
 
 
 def rc_profile_enable(on=True):

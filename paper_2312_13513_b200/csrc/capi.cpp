@@ -177,6 +177,9 @@ extern "C" int rc_mech_create(const rc_mech_desc *d, rc_mech **out) {
     }
   }
   m->inert.assign(d->inert, d->inert + ns);
+  m->nasa_lo.assign(d->nasa_lo, d->nasa_lo + 7 * ns);
+  m->nasa_hi.assign(d->nasa_hi, d->nasa_hi + 7 * ns);
+  m->T_mid.assign(d->T_mid, d->T_mid + ns);
   m->Tmin = d->T_lo[0];
   m->Tmax = d->T_hi[0];
   m->uniform_tmid = true;
@@ -435,4 +438,42 @@ extern "C" int rc_partition(int64_t n_global, int rank, int world, int64_t *begi
   *begin = bound(rank);
   *end = bound(rank + 1);
   return RC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// detailed kinetics (NEXT-3): table building lives in kinetics.cu (kin_build)
+// ---------------------------------------------------------------------------
+int kin_build(const rc_mech *m, const rc_kin_desc *d, rc_kin *k);
+
+extern "C" int rc_kin_create(const rc_mech *m, const rc_kin_desc *d, rc_kin **out) {
+  rc_reset_launches();
+  if (!m || !d || !out) return rc_fail(RC_EINVAL, "rc_kin_create: NULL argument");
+  *out = nullptr;
+  if (d->nr < 1 || d->nr > 256) return rc_fail(RC_EINVAL, "rc_kin_create: nr=%d out of range", d->nr);
+  if (!d->nu_f || !d->nu_r || !d->type || !d->reversible || !d->A || !d->b || !d->Ea || !d->eff || !d->A0 ||
+      !d->b0 || !d->Ea0 || !d->troe)
+    return rc_fail(RC_EINVAL, "rc_kin_create: NULL array");
+  rc_kin *k = new rc_kin();
+  int rc = kin_build(m, d, k);
+  if (rc != RC_OK) { rc_kin_destroy(k); return rc; }
+  *out = k;
+  return RC_OK;
+}
+
+extern "C" void rc_kin_destroy(rc_kin *k) {
+  if (!k) return;
+  cudaFree(k->d_tab);
+  cudaFree(k->d_qpart);
+  delete k;
+}
+
+extern "C" int rc_kinetics(const rc_mech *m, const rc_kin *k, const rc_cells *c, void *stream) {
+  rc_reset_launches();
+  CellsDev d;
+  int rc = check_cells(m, c, d);
+  if (rc) return rc;
+  if (!k) return rc_fail(RC_EINVAL, "NULL kinetics handle");
+  if (k->ns != m->ns) return rc_fail(RC_EINVAL, "kinetics built for ns=%d, mech has ns=%d", k->ns, m->ns);
+  if (!c->wdot) return rc_fail(RC_EINVAL, "rc_kinetics needs wdot");
+  return launch_kinetics(m, k, d, (cudaStream_t)stream);
 }

@@ -623,6 +623,13 @@ uint16_t f2bf(float f) {  // round-to-nearest-even float -> bf16 bits
 
 }  // namespace
 
+int launch_qdot_finalize(const double *qpart, int n, double *red, cudaStream_t s) {
+  ProfScope prof(RC_STAGE_FINALIZE, s);
+  qdot_finalize_kernel<<<1, 32, 0, s>>>(qpart, n, red);
+  RC_LAUNCH_CHECK();
+  return RC_OK;
+}
+
 int launch_combine_reductions(const double *rp, const int64_t *dp, int k, double *red, int64_t *diag, cudaStream_t s) {
   ProfScope prof(RC_STAGE_FINALIZE, s);
   combine_reductions_kernel<<<1, 1, 0, s>>>(rp, dp, k, red, diag);

@@ -54,6 +54,7 @@ struct rc_mech {
   bool uniform_tmid;
   double Tmin, Tmax;
   std::vector<double> W, P, thermo_host, transport_host;
+  std::vector<double> nasa_lo, nasa_hi, T_mid;  // [ns][7], [ns]: raw NASA-7 (the kinetics table's g_k)
   std::vector<uint8_t> inert;
   double *d_thermo = nullptr;     // ThermoSeg
   double *d_transport = nullptr;  // TransportSeg
@@ -133,5 +134,15 @@ struct ChemWs;  // defined in mlp_sm100.cu
 size_t chem_workspace_bytes(const rc_mech *m, const rc_mlp *n, int64_t ncells);
 size_t chem_workspace_min_bytes(const rc_mlp *n, int64_t ncells);  // the smallest chunk (256 cells)
 int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, size_t ws_bytes, cudaStream_t s);
+// detailed kinetics (kinetics.cu): one 48-double record per reaction + eff [nr][ns] + NASA g table
+struct rc_kin {
+  int nr, ns, device;
+  double *d_tab = nullptr;   // KinSeg
+  double *d_qpart = nullptr; // per-block qdot partials (deterministic sum)
+  size_t tab_doubles = 0;
+};
+int launch_kinetics(const rc_mech *m, const rc_kin *k, const CellsDev &c, cudaStream_t s);
+int launch_qdot_finalize(const double *qpart, int n, double *red, cudaStream_t s);
+
 int launch_combine_reductions(const double *rp, const int64_t *dp, int k, double *red, int64_t *diag, cudaStream_t s);
 int mlp_upload(rc_mlp *n, const rc_mlp_desc *d);
