@@ -64,6 +64,8 @@ def lib():
             ("orc_mlp_forward", d, [vp, i, vp]), ("orc_projection", i, [vp, vp]),
             ("orc_prologue_cell", None, [vp, vp, d, d, vp, vp, vp]), ("orc_step", i, [vp, vp, vp, i]),
             ("orc_pasr_kappa", d, [vp, d, vp, vp, d]),
+            ("orc_laplacian_gamma", None, [i, C.c_int64, vp, vp, vp, vp, vp]),
+            ("orc_laplacian", None, [vp, i, vp, vp, vp, vp, vp]), ("orc_ldu_matvec", None, [vp, vp, vp, vp, vp]),
             ("orc_species_g", d, [vp, i, d]), ("orc_rate_constant", d, [vp, i, d, d]),
             ("orc_kinetics_cell", None, [vp, vp, d, d, vp, vp, vp, vp]), ("orc_kinetics", i, [vp, vp, vp, vp, i]),
         ]:
@@ -242,3 +244,38 @@ def kinetics(mech: Mech, kin: Kin, T, p, Y, tau_mix=None, nthreads: int = 0) -> 
     out["red"] = np.array(c.red[:])
     out["diag"] = np.array(c.diag[:], dtype=np.int64)
     return out
+
+
+class _MeshS(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("dx", C.c_double), ("dy", C.c_double),
+                ("dz", C.c_double)]
+
+
+def laplacian_gamma(ns, rho, D, lam, cp):
+    """gamma [ns+1][n]: rho D_k for species, lambda/cp for energy (NEXT-1 coefficients)."""
+    n = int(np.asarray(rho).shape[0])
+    arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (rho, D, lam, cp)]
+    g = np.empty((ns + 1, n))
+    lib().orc_laplacian_gamma(ns, n, *[_p(a) for a in arrs], _p(g))
+    return g
+
+
+def laplacian(mesh, gamma, halo_lo=None, halo_hi=None):
+    """Algorithm 1 on the periodic mesh / slab: returns (upper [nsys][3N], diag [nsys][N]).
+    mesh = (nx, ny, nz, dx, dy, dz)."""
+    ms = _MeshS(*mesh)
+    g = np.ascontiguousarray(gamma, dtype=np.float64)
+    nsys, N = g.shape
+    up, dg = np.empty((nsys, 3 * N)), np.empty((nsys, N))
+    lo = None if halo_lo is None else np.ascontiguousarray(halo_lo, dtype=np.float64)
+    hi = None if halo_hi is None else np.ascontiguousarray(halo_hi, dtype=np.float64)
+    lib().orc_laplacian(C.byref(ms), nsys, _p(g), _p(lo), _p(hi), _p(up), _p(dg))
+    return up, dg
+
+
+def ldu_matvec(mesh, upper, diag, x):
+    ms = _MeshS(*mesh)
+    y = np.empty_like(np.asarray(x, dtype=np.float64))
+    arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (upper, diag, x)]
+    lib().orc_ldu_matvec(C.byref(ms), *[_p(a) for a in arrs], _p(y))
+    return y

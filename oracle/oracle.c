@@ -681,3 +681,61 @@ int orc_kinetics(const orc_mech *m, const orc_kin *kin, orc_cells *c, double *ws
   c->red[1] = s + comp;
   return 0;
 }
+
+
+/* ====================================================================== Laplacian assembly (NEXT-1)
+ * PAPER.md Algorithm 1: for every face, gamma_f <- interpolation(w, gamma_c) (w = 1/2 on the uniform
+ * mesh), upper, lower <- gamma_f delta_f S_f (delta_f = 1/|d_f|, S_f the face area), then the diagonal
+ * accumulates -upper at the owner and -lower at the neighbour.  Written face by face in face order. */
+void orc_laplacian_gamma(int ns, int64_t n, const double *rho, const double *D, const double *lambda,
+                         const double *cp, double *gamma) {
+  for (int k = 0; k < ns; ++k)
+    for (int64_t c = 0; c < n; ++c) gamma[k * n + c] = rho[c] * D[k * n + c];
+  for (int64_t c = 0; c < n; ++c) gamma[(int64_t)ns * n + c] = lambda[c] / cp[c];
+}
+
+void orc_laplacian(const orc_mesh *m, int nsys, const double *gamma, const double *halo_lo, const double *halo_hi,
+                   double *upper, double *diag) {
+  int64_t nx = m->nx, ny = m->ny, nz = m->nz, N = nx * ny * nz, plane = nx * ny;
+  double SdX = m->dy * m->dz / m->dx, SdY = m->dx * m->dz / m->dy, SdZ = m->dx * m->dy / m->dz;
+  for (int s = 0; s < nsys; ++s) {
+    const double *g = gamma + (int64_t)s * N;
+    double *up = upper + (int64_t)s * 3 * N, *dg = diag + (int64_t)s * N;
+    for (int64_t c = 0; c < N; ++c) dg[c] = 0.0;
+    for (int d = 0; d < 3; ++d)
+      for (int64_t c = 0; c < N; ++c) {
+        int64_t i = c % nx, j = (c / nx) % ny, k = c / plane;
+        int64_t nb;               /* neighbour cell, -1: in the halo plane above */
+        double gN, SdD = d == 0 ? SdX : d == 1 ? SdY : SdZ;
+        if (d == 0) nb = (i + 1 == nx ? 0 : i + 1) + nx * (j + ny * k);
+        else if (d == 1) nb = i + nx * ((j + 1 == ny ? 0 : j + 1) + ny * k);
+        else nb = (k + 1 < nz) ? c + plane : (halo_hi ? -1 : c + plane - N);
+        gN = nb >= 0 ? g[nb] : halo_hi[(int64_t)s * plane + (c - (nz - 1) * plane)];
+        double gf = 0.5 * (g[c] + gN);       /* interpolation(w = 1/2) */
+        double a = gf * SdD;                 /* gamma_f delta_f S_f */
+        up[(int64_t)d * N + c] = a;
+        dg[c] -= a;                          /* diag[owner] -= upper */
+        if (nb >= 0) dg[nb] -= a;            /* diag[neighbour] -= lower (lower = upper) */
+      }
+    if (halo_lo) /* faces from the plane below the slab onto plane 0 (owned by the rank below) */
+      for (int64_t c = 0; c < plane; ++c) {
+        double gf = 0.5 * (halo_lo[(int64_t)s * plane + c] + g[c]);
+        dg[c] -= gf * SdZ;
+      }
+  }
+}
+
+void orc_ldu_matvec(const orc_mesh *m, const double *upper, const double *diag, const double *x, double *y) {
+  int64_t nx = m->nx, ny = m->ny, nz = m->nz, N = nx * ny * nz, plane = nx * ny;
+  for (int64_t c = 0; c < N; ++c) y[c] = diag[c] * x[c];
+  for (int d = 0; d < 3; ++d)
+    for (int64_t c = 0; c < N; ++c) {
+      int64_t i = c % nx, j = (c / nx) % ny, k = c / plane, nb;
+      if (d == 0) nb = (i + 1 == nx ? 0 : i + 1) + nx * (j + ny * k);
+      else if (d == 1) nb = i + nx * ((j + 1 == ny ? 0 : j + 1) + ny * k);
+      else nb = (k + 1 < nz) ? c + plane : c + plane - N;
+      double a = upper[(int64_t)d * N + c];
+      y[c] += a * x[nb];   /* upper: row owner, column neighbour */
+      y[nb] += a * x[c];   /* lower: row neighbour, column owner */
+    }
+}

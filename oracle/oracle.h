@@ -101,6 +101,27 @@ double orc_rate_constant(const orc_kin *kin, int r, double T, double M);
 void orc_kinetics_cell(const orc_mech *m, const orc_kin *kin, double T, double p, const double *Y, double *wdot,
                        double *qnet, double *scale);
 
+/* ---- downstream consumer (reading R22): implicit Laplacian
+ * assembly of PAPER.md Algorithm 1 (lines 137-158) on a periodic Cartesian mesh, ldu storage
+ * (PAPER.md:160-167), ldu -> CSR.  Cells c = i + nx (j + ny k); face (d, c) joins cell c
+ * and its +d neighbour (d = x, y, z; periodic wrap, or the halo plane above the slab in z). ---- */
+typedef struct {
+  int32_t nx, ny, nz;   /* cells; nz = planes of this slab */
+  double dx, dy, dz;    /* m */
+} orc_mesh;
+/* Laplacian coefficients from the property outputs: gamma[k] = rho D_k (species k < ns),
+ * gamma[ns] = lambda / cp (energy); gamma [ns+1][n] */
+void orc_laplacian_gamma(int ns, int64_t n, const double *rho, const double *D, const double *lambda,
+                         const double *cp, double *gamma);
+/* Algorithm 1 for nsys systems: gamma_f = (gamma_P + gamma_N)/2 (linear interpolation, uniform mesh),
+ * upper[f] = lower[f] = gamma_f |S_f| / |d_f|, diag[P] -= upper[f], diag[N] -= lower[f], faces in
+ * order f = d N + c.  halo_lo / halo_hi [nsys][nx ny]: gamma of the planes below / above the slab
+ * (NULL: periodic in z within the slab).  upper [nsys][3 N], diag [nsys][N]. */
+void orc_laplacian(const orc_mesh *m, int nsys, const double *gamma, const double *halo_lo, const double *halo_hi,
+                   double *upper, double *diag);
+/* y = A x for one system in ldu form (periodic slab), x [N], y [N] */
+void orc_ldu_matvec(const orc_mesh *m, const double *upper, const double *diag, const double *x, double *y);
+
 /* ---- whole-field entry points (SoA, host arrays) ---- */
 typedef struct {
   int64_t n, ld;
