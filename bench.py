@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--layerwise", action="store_true", help="rc_mlp_desc.flags = RC_MLP_LAYERWISE (comparison path)")
     ap.add_argument("--pasr", action="store_true", help="LES: PaSR scaling of wdot with per-cell tau_mix (NEXT-4)")
     ap.add_argument("--shared", action="store_true", help="one shared net with n_nets outputs (NEXT-2)")
+    ap.add_argument("--laplacian", action="store_true",
+                    help="add the NEXT-1 consumer: Algorithm 1 Laplacian assembly of the ns+1 species/energy "
+                         "systems (+ ldu->CSR at N=1; z-slab halo exchange over NCCL P2P at N>1); 3D configs")
     ap.add_argument("--chem", default="dnn", choices=["dnn", "kinetics"],
                     help="source term: the DNN (the paper's GPU path) or detailed kinetics (NEXT-3, the CVODE RHS)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -177,6 +180,10 @@ def algorithmic(cfg, bundle, ns, n, precision="bf16"):
         # detailed kinetics: FP64-pipe instructions per cell executed by the kernel (ncu
         # sm__inst_executed_pipe_fp64 per cell, profiles/ncu_kinetics_r02.json), x 2 flop per DFMA slot
         "kinetics_fp64_flops": n * 2 * KIN_FP64_INSTR_PER_CELL.get(cfg.mech, 0),
+        # NEXT-1: in rho, lambda, cp, D_k; out upper (3 faces per cell) and diag of ns+1 systems
+        "laplacian_bytes": n * ((3 + ns) * 8 + 4 * (ns + 1) * 8),
+        # ldu -> CSR: in upper + diag; out 7 columns (int32) + 7 values per system + row pointer
+        "csr_bytes": n * (4 * (ns + 1) * 8 + 7 * 4 + 7 * (ns + 1) * 8 + 8),
         "mlp_flops": n * nets * flops_net,
         "L1_bytes": n * nets * h1 * eb,               # h1 activations written
         # in: raw outputs o (fp32 per net), T, rho, Y; out: wdot, qdot
@@ -226,6 +233,31 @@ def run_ours(a):
         from workload import load_kinetics
         kin = rc.Kinetics(mech, load_kinetics(cfg.mech))
 
+    lap = None
+    if a.laplacian:  # NEXT-1: the block is a z-slab (weak scaling: rank blocks stacked in z) of a periodic box
+        if len(cfg.grid) != 3 or a.strong:
+            raise SystemExit("--laplacian needs a 3D config (C3, C4, C5) and weak scaling")
+        from paper_2312_13513_b200.dist import exchange_halos
+        h_sp = 0.01 / cfg.grid[0]                      # uniform spacing: a ~1 cm box
+        mesh = (*cfg.grid, h_sp, h_sp, h_sp)
+        nsys, plane = ns + 1, cfg.grid[0] * cfg.grid[1]
+        f64 = dict(dtype=torch.float64, device="cuda")
+        lap = {"up": torch.empty(nsys, 3 * n, **f64), "dg": torch.empty(nsys, n, **f64)}
+        if world > 1:
+            lap.update(bot=torch.empty(ns + 3, plane, **f64), top=torch.empty(ns + 3, plane, **f64))
+        else:
+            lap.update(rp=torch.empty(n + 1, dtype=torch.int64, device="cuda"),
+                       col=torch.empty(7 * n, dtype=torch.int32, device="cuda"), val=torch.empty(nsys, 7 * n, **f64))
+
+    def consumer():
+        if world > 1:  # halo planes of the neighbouring slabs (NCCL P2P), then the slab assembly
+            rc.rc_pack_planes(mech, mesh, cells, lap["bot"], lap["top"], stream)
+            lo, hi = exchange_halos(lap["bot"], lap["top"])
+            rc.rc_laplacian(mech, mesh, cells, lap["up"], lap["dg"], lo, hi, rc.RC_LAP_GATHER, stream)
+        else:
+            rc.rc_laplacian(mech, mesh, cells, lap["up"], lap["dg"], None, None, rc.RC_LAP_GATHER, stream)
+            rc.rc_ldu_to_csr(mesh, nsys, lap["up"], lap["dg"], lap["rp"], lap["col"], lap["val"], stream)
+
     def step():
         st.T[:n].copy_(T_guess)                       # each step restarts Newton from the same guess
         if a.chem == "kinetics":                       # a1 + a2 + detailed kinetics instead of a3-a5
@@ -236,6 +268,8 @@ def run_ours(a):
             rc.rc_kinetics(mech, kin, cells, stream)
         else:
             rc.rc_step(mech, mlp, cells, ws, stream)
+        if lap is not None:
+            consumer()
         reduce_a6(st.red, st.diag)                     # a6: global max T and sums (NCCL over NVLink; no-op at N=1)
 
     for _ in range(a.warmup):
@@ -268,7 +302,7 @@ def run_ours(a):
 
     # ---- end to end through the C ABI from pinned HOST buffers (H2D in, D2H out, every step)
     e2e = None
-    if not a.no_e2e and a.chem == "dnn":
+    if not a.no_e2e and a.chem == "dnn" and not a.laplacian:
         e2e = run_e2e(a, rc, mech, mlp, bundle, host, st, ws, n, ns, world, stream)
 
     out = None
@@ -297,6 +331,8 @@ def run_ours(a):
             ("L3", alg["L3_flops"], "TFLOP/s", "tensor", tpeak),
             ("L4", alg["L4_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),  # shared net's output layer (CUDA cores)
             ("kinetics", alg["kinetics_fp64_flops"], "TFLOP/s", "fp64", f64),  # detailed kinetics (NEXT-3)
+            ("laplacian", alg["laplacian_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),     # NEXT-1 assembly
+            ("csr", alg["csr_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),                 # NEXT-1 ldu -> CSR
             ("epilogue", alg["epilogue_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),
         ]:
             t_ms, cnt = per(st_name)
@@ -341,7 +377,8 @@ def run_ours(a):
                              "cell state 0.2 GB) - no flush needed",
                        "precision": a.precision, **({"les_pasr": True} if a.pasr else {}),
                        **({"mlp": "one shared net, n_nets outputs (NEXT-2)"} if a.shared else {}),
-                       **({"chem": "detailed kinetics, 12 reactions (NEXT-3)"} if a.chem == "kinetics" else {})},
+                       **({"chem": "detailed kinetics, 12 reactions (NEXT-3)"} if a.chem == "kinetics" else {}),
+                       **({"consumer": "Laplacian assembly of ns+1 systems (NEXT-1)"} if a.laplacian else {})},
             "roofline": {"kernel": ("fused L1+L2 (z -> h1 1600 on chip -> h2 800, tcgen05 bf16, 4-CTA clusters)"
                                     if fused else "L2 GEMM (h1 1600 -> h2 800, tcgen05)"), "bound": "tensor",
                          "achieved": l2.get("achieved"), "peak": tpeak, "unit": "TFLOP/s",

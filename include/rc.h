@@ -196,6 +196,38 @@ int rc_chem(const rc_mech *m, const rc_mlp *n, const rc_cells *c, void *ws, size
 int rc_step(const rc_mech *m, const rc_mlp *n, const rc_cells *c, void *ws, size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * Downstream consumer (reading R22): implicit Laplacian assembly of
+ * PAPER.md Algorithm 1 (lines 137-158) for the ns species equations and the energy equation with the
+ * coefficients this path produces -- gamma = rho D_k (system k < ns), lambda / cp (system ns) -- on a
+ * periodic Cartesian mesh of uniform spacing, or on a z-slab of one (multi-GPU block).
+ * Cells c = i + nx (j + ny k); face f = d n + c (d = x, y, z) joins cell c and its +d
+ * neighbour (periodic wrap in x, y; in z the wrap or, with halos, the plane above the slab).
+ *   gamma_f = (gamma_P + gamma_N) / 2 (linear interpolation, uniform mesh: w = 1/2)
+ *   upper[f] = lower[f] = gamma_f |S_f| / |d_f|;  diag[P] -= upper[f], diag[N] -= lower[f]
+ * ldu storage: the matrix is symmetric, so lower = upper is not stored.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t nx, ny, nz;             /* cells per direction (nz: planes of this block) */
+  double dx, dy, dz;              /* uniform spacing, m */
+} rc_mesh;
+enum { RC_LAP_GATHER = 0, RC_LAP_ATOMIC = 1 };  /* one thread per cell, diagonal gathered (deterministic) |
+                                                   one thread per face, diagonal by atomicAdd (Algorithm 1) */
+/* c: n = nx ny nz cells with rho, lambda, cp, D (device, as rc_step left them).  halo_lo / halo_hi:
+ * both NULL (periodic in z) or device [(ns + 3)][nx ny] planes (rho, lambda, cp, D_0..D_{ns-1}) of the
+ * cells below plane 0 / above plane nz-1 (rc_pack_planes of the neighbouring ranks).  Out (device,
+ * 8-byte aligned): upper [ns+1][3 n], diag [ns+1][n].  Errors: RC_EINVAL, RC_EALIGN, RC_ECUDA. */
+int rc_laplacian(const rc_mech *m, const rc_mesh *mesh, const rc_cells *c, const double *halo_lo,
+                 const double *halo_hi, double *upper, double *diag, int mode, void *stream);
+/* ldu -> CSR of nsys systems of a periodic block: row_ptr [n+1] (int64), col [7 n]
+ * (int32, ascending per row), val [nsys][7 n].  Needs nx, ny, nz >= 3 (else RC_EUNSUPPORTED). */
+int rc_ldu_to_csr(const rc_mesh *mesh, int nsys, const double *upper, const double *diag, int64_t *row_ptr,
+                  int32_t *col, double *val, void *stream);
+/* The bottom and top planes of this block's rho, lambda, cp, D -> bottom / top [(ns + 3)][nx ny]
+ * (device; either may be NULL): what the neighbouring ranks receive as their halos. */
+int rc_pack_planes(const rc_mech *m, const rc_mesh *mesh, const rc_cells *c, double *bottom, double *top,
+                   void *stream);
+
+/* ---------------------------------------------------------------------------
  * Detailed kinetics (reading R21): the right-hand side the paper's
  * CVODE option integrates ("CVODE ... on CPU or DNN on GPU"; the 9-species /
  * 12-reaction H2 mechanism of PAPER.md:231) -- an alternative source term to the DNN, per cell:
@@ -256,7 +288,9 @@ enum {
   RC_STAGE_L12 = 8,  /* fused layers 1+2 (bf16 at the paper widths; replaces L1 and L2) */
   RC_STAGE_L4 = 9,   /* layer 4 of the shared net (RC_MLP_SHARED) */
   RC_STAGE_KINETICS = 10, /* detailed kinetics (rc_kinetics) */
-  RC_STAGE_COUNT = 11
+  RC_STAGE_LAPLACIAN = 11, /* Laplacian assembly (rc_laplacian) */
+  RC_STAGE_CSR = 12,      /* ldu -> CSR (rc_ldu_to_csr) */
+  RC_STAGE_COUNT = 13
 };
 int rc_profile_enable(int on);
 int rc_profile_read(double *ms /* [RC_STAGE_COUNT] */, int64_t *launches /* [RC_STAGE_COUNT] */, int reset);

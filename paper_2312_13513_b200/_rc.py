@@ -71,6 +71,11 @@ EXPORTS = {
     "rc_kin_create": (C.c_int, [C.c_void_p, C.POINTER(rc_kin_desc), C.POINTER(C.c_void_p)]),
     "rc_kin_destroy": (None, [C.c_void_p]),
     "rc_kinetics": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(rc_cells), C.c_void_p]),
+    "rc_laplacian": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(rc_cells), C.c_void_p, C.c_void_p, C.c_void_p,
+                               C.c_void_p, C.c_int, C.c_void_p]),
+    "rc_ldu_to_csr": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.c_void_p]),
+    "rc_pack_planes": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(rc_cells), C.c_void_p, C.c_void_p, C.c_void_p]),
     "rc_last_launch_count": (C.c_int64, []),
     "rc_profile_enable": (C.c_int, [C.c_int]),
     "rc_profile_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
@@ -195,6 +200,32 @@ def rc_kinetics(mech, kin, cells, stream=None):
     return check(lib().rc_kinetics(mech.h, kin.h, C.byref(cells), _stream(stream)))
 
 
+class rc_mesh(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("dx", C.c_double), ("dy", C.c_double),
+                ("dz", C.c_double)]
+
+
+RC_LAP_GATHER, RC_LAP_ATOMIC = 0, 1
+
+
+def rc_laplacian(mech, mesh, cells, upper, diag, halo_lo=None, halo_hi=None, mode=RC_LAP_GATHER, stream=None):
+    """mesh = (nx, ny, nz, dx, dy, dz); upper [ns+1][3n], diag [ns+1][n] device tensors (NEXT-1)."""
+    m = rc_mesh(*mesh)
+    return check(lib().rc_laplacian(mech.h, C.byref(m), C.byref(cells), _ptr(halo_lo), _ptr(halo_hi), _ptr(upper),
+                                    _ptr(diag), int(mode), _stream(stream)))
+
+
+def rc_ldu_to_csr(mesh, nsys, upper, diag, row_ptr, col, val, stream=None):
+    m = rc_mesh(*mesh)
+    return check(lib().rc_ldu_to_csr(C.byref(m), int(nsys), _ptr(upper), _ptr(diag), _ptr(row_ptr), _ptr(col),
+                                     _ptr(val), _stream(stream)))
+
+
+def rc_pack_planes(mech, mesh, cells, bottom, top, stream=None):
+    m = rc_mesh(*mesh)
+    return check(lib().rc_pack_planes(mech.h, C.byref(m), C.byref(cells), _ptr(bottom), _ptr(top), _stream(stream)))
+
+
 def make_cells(n, ld, mode, T, p, Y, h=None, cp=None, rho=None, mu=None, lam=None, D=None, wdot=None, qdot=None,
                o=None, dt=0.0, red=None, diag=None, tau_mix=None):
     """rc_cells struct from torch device tensors (component-major, stride ld)."""
@@ -239,7 +270,8 @@ def rc_last_launch_count():
     return int(lib().rc_last_launch_count())
 
 
-STAGES = ["thermo", "transport", "prologue", "L1", "L2", "L3", "epilogue", "finalize", "L12", "L4", "kinetics"]
+STAGES = ["thermo", "transport", "prologue", "L1", "L2", "L3", "epilogue", "finalize", "L12", "L4", "kinetics",
+          "laplacian", "csr"]
 
 
 def rc_profile_enable(on=True):

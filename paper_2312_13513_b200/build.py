@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "librc_b200.so")
-SOURCES = ["capi.cpp", "thermo.cu", "transport.cu", "mlp_sm100.cu", "mlp_l1_sm100.cu", "mlp_l2_sm100.cu", "mlp_l12_sm100.cu", "kinetics.cu"]
+SOURCES = ["capi.cpp", "thermo.cu", "transport.cu", "mlp_sm100.cu", "mlp_l1_sm100.cu", "mlp_l2_sm100.cu", "mlp_l12_sm100.cu", "kinetics.cu", "laplacian.cu"]
 HEADERS = ["rc_internal.h", "ptx.cuh", "stream.cuh", "mlp_internal.h", "mlp_common.cuh", os.path.join("..", "..", "include", "rc.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

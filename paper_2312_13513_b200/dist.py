@@ -11,7 +11,7 @@ import torch.distributed as dist
 
 from ._rc import rc_partition
 
-__all__ = ["shard", "GlobalReductions"]
+__all__ = ["shard", "GlobalReductions", "slab", "exchange_halos"]
 
 
 def shard(n_global: int, rank: int | None = None, world: int | None = None):
@@ -47,3 +47,35 @@ class GlobalReductions:
         red[1:2].copy_(self.buf[0:1])
         diag.copy_(self.buf[1:].to(torch.int64))
         return red, diag
+
+
+def slab(nz_global: int, rank: int | None = None, world: int | None = None):
+    """[z0, z1) planes of this rank's z-slab of a periodic box (NEXT-1 Laplacian consumer): contiguous,
+    balanced, every rank at least one plane."""
+    if rank is None:
+        rank = dist.get_rank() if dist.is_initialized() else 0
+    if world is None:
+        world = dist.get_world_size() if dist.is_initialized() else 1
+    if world > nz_global:
+        raise ValueError(f"{world} ranks for {nz_global} planes")
+    return nz_global * rank // world, nz_global * (rank + 1) // world
+
+
+def exchange_halos(bottom: torch.Tensor, top: torch.Tensor, group=None):
+    """The halo exchange of the z-slab decomposition (NCCL peer-to-peer between GPUs, over
+    NVLink/NVSwitch; gloo in the CPU tests): every rank sends its bottom plane to the rank below and its
+    top plane to the rank above on the periodic ring, and receives (halo_lo, halo_hi) = (top plane of the
+    rank below, bottom plane of the rank above).  Planes are the [(ns + 3)][nx ny] packs of
+    rc_pack_planes.  One rank: the periodic wrap onto itself."""
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return top.clone(), bottom.clone()
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    below, above = (rank - 1) % world, (rank + 1) % world
+    lo, hi = torch.empty_like(top), torch.empty_like(bottom)
+    # per peer, sends and receives are matched in posting order: my top is the halo_lo of the rank
+    # above (posted first on both sides), my bottom the halo_hi of the rank below
+    ops = [dist.P2POp(dist.isend, top, above, group), dist.P2POp(dist.isend, bottom, below, group),
+           dist.P2POp(dist.irecv, lo, below, group), dist.P2POp(dist.irecv, hi, above, group)]
+    for r in dist.batch_isend_irecv(ops):
+        r.wait()
+    return lo, hi

@@ -81,3 +81,84 @@ def test_partition_and_global_reductions_gloo():
         assert red[1] == pytest.approx(full["red"][1], rel=1e-12)    # Neumaier sums per rank, then a 2-term sum
         assert diag == list(full["diag"])
     assert res[0][3] == res[1][3] and res[0][4] == res[1][4]
+
+
+# ---------------------------------------------------------------- NEXT-1: z-slab halo exchange
+MESH = (6, 5, 8, 1e-3, 1.2e-3, 0.9e-3)
+NS = 3
+
+
+def _gamma_inputs():
+    """a seeded global field of the Laplacian inputs (rho, lambda, cp, D_k) on MESH, cells in index order"""
+    nx, ny, nz = MESH[:3]
+    rng = np.random.default_rng(11)
+    n = nx * ny * nz
+    return {"rho": rng.uniform(0.1, 1.2, n), "lam": rng.uniform(0.02, 0.2, n), "cp": rng.uniform(1e3, 2e3, n),
+            "D": rng.uniform(1e-5, 1e-4, (NS, n))}
+
+
+def _pack(f, sl):
+    """[(ns + 3)][plane] pack of the planes `sl` of the fields (the layout rc_pack_planes writes)"""
+    return np.concatenate([f["rho"][sl][None], f["lam"][sl][None], f["cp"][sl][None], f["D"][:, sl]])
+
+
+def _halo_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2312_13513_b200.dist import exchange_halos, slab
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        nx, ny, nz, dx, dy, dz = MESH
+        plane = nx * ny
+        f = _gamma_inputs()
+        z0, z1 = slab(nz)
+        loc = slice(z0 * plane, z1 * plane)
+        bottom = torch.from_numpy(_pack(f, slice(z0 * plane, (z0 + 1) * plane)))
+        top = torch.from_numpy(_pack(f, slice((z1 - 1) * plane, z1 * plane)))
+        lo, hi = exchange_halos(bottom, top)
+        g = oracle.laplacian_gamma(NS, f["rho"][loc], f["D"][:, loc], f["lam"][loc], f["cp"][loc])
+        hg = [oracle.laplacian_gamma(NS, h[0], h[3:], h[1], h[2]) for h in (lo.numpy(), hi.numpy())]
+        up, dg = oracle.laplacian((nx, ny, z1 - z0, dx, dy, dz), g, hg[0], hg[1])
+        q.put((rank, z0, z1, lo.numpy(), hi.numpy(), up, dg))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slab_halo_exchange_gloo():
+    """Two ranks own z-slabs of a periodic box; exchange_halos (batch_isend_irecv on the periodic ring,
+    NCCL P2P on the GPU box) delivers the neighbours' boundary planes, and each rank's slab assembly
+    with those halos equals the corresponding rows of the global periodic assembly."""
+    import torch.multiprocessing as mp
+
+    import oracle
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=300) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    nx, ny, nz = MESH[:3]
+    plane, N = nx * ny, nx * ny * nz
+    f = _gamma_inputs()
+    gG = oracle.laplacian_gamma(NS, f["rho"], f["D"], f["lam"], f["cp"])
+    upG, dgG = oracle.laplacian(MESH, gG)
+    assert res[0][1] == 0 and res[-1][2] == nz and res[0][2] == res[1][1]
+    for rank, z0, z1, lo, hi, up, dg in res:
+        # halos: the planes z0 - 1 and z1 of the periodic box
+        assert np.array_equal(lo, _pack(f, slice(((z0 - 1) % nz) * plane, ((z0 - 1) % nz + 1) * plane)))
+        assert np.array_equal(hi, _pack(f, slice((z1 % nz) * plane, (z1 % nz + 1) * plane)))
+        n = (z1 - z0) * plane
+        sl = slice(z0 * plane, z1 * plane)
+        for d in range(3):
+            assert np.array_equal(up[:, d * n:(d + 1) * n], upG[:, d * N:(d + 1) * N][:, sl])
+        np.testing.assert_allclose(dg, dgG[:, sl], rtol=1e-15)
