@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--laplacian", action="store_true",
                     help="add the NEXT-1 consumer: Algorithm 1 Laplacian assembly of the ns+1 species/energy "
                          "systems (+ ldu->CSR at N=1; z-slab halo exchange over NCCL P2P at N>1); 3D configs")
+    ap.add_argument("--graph", action="store_true",
+                    help="replay the step as one CUDA graph (PAPER.md:187); per-kernel timing is then unavailable")
     ap.add_argument("--chem", default="dnn", choices=["dnn", "kinetics"],
                     help="source term: the DNN (the paper's GPU path) or detailed kinetics (NEXT-3, the CVODE RHS)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -276,7 +278,22 @@ def run_ours(a):
         step()
     torch.cuda.synchronize()
     launches_per_step = rc.rc_last_launch_count()     # our kernels per rc_step (the T restore copy is torch's)
-    rc.rc_profile_enable(True)
+    if a.graph:  # the whole step (T restore + rc_step) captured once, replayed every step
+        if world > 1 or a.laplacian or a.chem != "dnn":
+            raise SystemExit("--graph: single-GPU DNN step only")
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cap):
+            st.T[:n].copy_(T_guess)
+            rc.rc_step(mech, mlp, cells, ws, cap)
+        stream.wait_stream(cap)
+        step = graph.replay
+        for _ in range(a.warmup):
+            step()
+        torch.cuda.synchronize()
+    else:
+        rc.rc_profile_enable(True)
     rc.rc_profile_read(reset=True)
     if world > 1:
         dist.barrier()
@@ -378,7 +395,8 @@ def run_ours(a):
                        "precision": a.precision, **({"les_pasr": True} if a.pasr else {}),
                        **({"mlp": "one shared net, n_nets outputs (NEXT-2)"} if a.shared else {}),
                        **({"chem": "detailed kinetics, 12 reactions (NEXT-3)"} if a.chem == "kinetics" else {}),
-                       **({"consumer": "Laplacian assembly of ns+1 systems (NEXT-1)"} if a.laplacian else {})},
+                       **({"consumer": "Laplacian assembly of ns+1 systems (NEXT-1)"} if a.laplacian else {}),
+                       **({"launch": "one CUDA graph per step"} if a.graph else {})},
             "roofline": {"kernel": ("fused L1+L2 (z -> h1 1600 on chip -> h2 800, tcgen05 bf16, 4-CTA clusters)"
                                     if fused else "L2 GEMM (h1 1600 -> h2 800, tcgen05)"), "bound": "tensor",
                          "achieved": l2.get("achieved"), "peak": tpeak, "unit": "TFLOP/s",

@@ -396,3 +396,38 @@ def test_chunking_is_invisible_per_cell():
     with pytest.raises(rc.RcError) as e:
         G.run(c, ws=full[: 1 << 20])
     assert e.value.code == rc._rc.RC_EINVAL
+
+
+def test_cuda_graph_capture_replays_rc_step_bitwise():
+    """SURVEY A16/K10 (the per-step kernel suite launched as a CUDA graph): rc_step
+    captured once with torch.cuda.graph and replayed gives bitwise the eager results (every kernel is
+    deterministic; the tensor maps travel by value in the kernel parameters)."""
+    import torch
+
+    import paper_2312_13513_b200 as rc
+    c = inputs("C2", begin=0, end=4096)
+    G = Gpu("C2")
+    n = 4096
+    st = rc.CellState(n, G.ns, G.n_nets)
+    st.load(c["T_guess"], c["p"], c["Y"], h=c["h"])
+    ws = rc.aligned_workspace(G.mlp, n)
+    cells = st.cells(rc.RC_MODE_H, dt=G.dt)
+    T0 = st.T.clone()
+    rc.rc_step(G.mech, G.mlp, cells, ws)            # eager (also warms the host-side caches)
+    torch.cuda.synchronize()
+    ref = st.host()
+    st.T.copy_(T0)
+    for t in (st.cp, st.rho, st.mu, st.lam, st.D, st.wdot, st.qdot, st.o):
+        t.zero_()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=side):
+        rc.rc_step(G.mech, G.mlp, cells, ws, side)
+    for _ in range(2):                               # replay twice from the restored guess
+        st.T.copy_(T0)
+        graph.replay()
+    torch.cuda.synchronize()
+    out = st.host()
+    for k in ("T", "cp", "rho", "mu", "lam", "D", "wdot", "qdot", "o", "red", "diag"):
+        assert np.array_equal(out[k], ref[k]), k
