@@ -53,6 +53,9 @@ def parse():
                     help="replay the step as one CUDA graph (PAPER.md:187); per-kernel timing is then unavailable")
     ap.add_argument("--chem", default="dnn", choices=["dnn", "kinetics"],
                     help="source term: the DNN (the paper's GPU path) or detailed kinetics (NEXT-3, the CVODE RHS)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU rank logic only (gloo): partition, generation, a6 reductions, NEXT-1 halo exchange")
+    ap.add_argument("--dry-cells", type=int, default=65536, help="--dry-run: local cells generated per rank")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle baseline")
@@ -146,6 +149,62 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows), "source": "NVML, 5 ms polling during the timed steps"}
 
 
+def generate(cfg, idx, world=1):
+    """Host generation of this rank's cells (workload.make_cells_at), in parallel over 1M-cell chunks
+    with this rank's share of the host cores: C5 gives every one of 8 ranks 12.5M cells (~45 s of
+    single-core numpy); the cell values are a pure function of the global index, so the split
+    changes nothing."""
+    from workload import make_cells_at
+    n = idx.size
+    chunk = 1 << 20
+    workers = max(1, min(len(os.sched_getaffinity(0)) // max(1, world), (n + chunk - 1) // chunk))
+    if workers == 1 or n <= 2 * chunk:
+        return make_cells_at(cfg, idx)
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+    parts = [idx[i:i + chunk] for i in range(0, n, chunk)]
+    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("fork")) as ex:
+        res = list(ex.map(make_cells_at, [cfg] * len(parts), parts))
+    return {k: np.concatenate([r[k] for r in res], axis=-1) for k in res[0]}
+
+
+def run_dry(a):
+    """--dry-run: the multi-rank host logic of run_ours on CPU (gloo) -- cell partition, generation of
+    (the first --dry-cells of) the local block, the a6 global reductions, and with --laplacian the
+    z-slab halo exchange -- so a world-size-2 CPU test can drive it (tests/test_multirank.py)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2312_13513_b200.dist import GlobalReductions, exchange_halos, slab
+    from workload import CONFIGS
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    cfg = CONFIGS[a.config]
+    idx, n_global = local_cells(cfg, rank, world, a.strong)
+    sub = idx[:a.dry_cells]
+    host = generate(cfg, sub, world)
+    red = torch.tensor([float(host["T_true"].max()), float(host["p"].sum())], dtype=torch.float64)
+    diag = torch.tensor([0, 0, 0, int((host["Y"] < 0).any(axis=0).sum()), 0], dtype=torch.int64)
+    GlobalReductions("cpu")(red, diag)
+    out = {"dry_run": True, "rank": rank, "world": world, "cells_local": int(idx.size), "first": int(idx[0]),
+           "last": int(idx[-1]), "cells_total": int(idx.size) * world if not a.strong else int(n_global),
+           "red": red.tolist(), "diag": diag.tolist()}
+    if a.laplacian and len(cfg.grid) == 3:
+        nx, ny, nz = cfg.grid
+        z0, z1 = slab(nz * world, rank, world)            # weak scaling: rank blocks stacked in z
+        plane = nx * ny
+        bottom = torch.full((3, plane), float(z0), dtype=torch.float64)
+        top = torch.full((3, plane), float(z1 - 1), dtype=torch.float64)
+        lo, hi = exchange_halos(bottom, top)
+        out["halo"] = [float(lo[0, 0]), float(hi[0, 0])]  # plane indices of the neighbours' boundary planes
+        out["slab"] = [z0, z1]
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def local_cells(cfg, rank, world, strong):
     """Global cell indices owned by this rank.  Weak: a C-sized block per rank of a
     periodic tiling of the config grid; strong: rc_partition of the config."""
@@ -218,7 +277,7 @@ def run_ours(a):
     ns, nets = mech_d["ns"], bundle["n_nets"]
     idx, n_global = local_cells(cfg, rank, world, a.strong)
     n = idx.size
-    host = make_cells_at(cfg, idx)
+    host = generate(cfg, idx, world)
     st = rc.CellState(n, ns, nets, outputs=("cp", "rho", "mu", "lam", "D", "wdot", "qdot"))
     st.load(host["T_true"], host["p"], host["Y"])
     if a.pasr:
@@ -591,5 +650,7 @@ if __name__ == "__main__":
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.dry_run:
+        run_dry(args)
     else:
         run_ours(args)

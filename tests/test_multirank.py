@@ -162,3 +162,46 @@ def test_slab_halo_exchange_gloo():
         for d in range(3):
             assert np.array_equal(up[:, d * n:(d + 1) * n], upG[:, d * N:(d + 1) * N][:, sl])
         np.testing.assert_allclose(dg, dgG[:, sl], rtol=1e-15)
+
+
+# ---------------------------------------------------------------- bench.py's rank logic (--dry-run)
+def _bench_ranks(args, world=2):
+    import json
+    import subprocess
+    import sys
+    port = _free_port()
+    procs = []
+    for r in range(world):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), LOCAL_RANK=str(r), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "bench.py"), "--dry-run", *args], env=env,
+                                      stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+    outs = []
+    for p in procs:
+        o, e = p.communicate(timeout=600)
+        assert p.returncode == 0, e[-2000:]
+        outs.append(json.loads(o.strip().splitlines()[-1]))
+    return sorted(outs, key=lambda d: d["rank"])
+
+
+def test_bench_rank_logic_strong_c5_gloo():
+    """bench.py at N = 2 (strong scaling of C5, the 1e8-cell 8xB200 target): the ranks' rc_partition
+    blocks tile [0, 1e8) with a 128-aligned boundary, each rank generates its cells, and the a6
+    reductions leave the same global values on both ranks."""
+    from workload import CONFIGS
+    r = _bench_ranks(["--config", "C5", "--strong", "--dry-cells", "4096"])
+    n = CONFIGS["C5"].n_cells
+    assert r[0]["first"] == 0 and r[1]["last"] == n - 1 and r[0]["last"] + 1 == r[1]["first"]
+    assert r[1]["first"] % 128 == 0 and r[0]["cells_total"] == n
+    assert r[0]["red"] == r[1]["red"] and r[0]["diag"] == r[1]["diag"]
+    assert 1500.0 < r[0]["red"][0] < 3000.0                         # max T of the generated flame states
+
+
+def test_bench_rank_logic_weak_laplacian_halos_gloo():
+    """bench.py --laplacian at N = 2 (weak scaling: each rank's C3 block is a z-slab of a box stacked in z):
+    the halo exchange delivers the neighbours' boundary planes on the periodic ring."""
+    r = _bench_ranks(["--config", "C3", "--laplacian", "--dry-cells", "1024"])
+    (a0, a1), (b0, b1) = r[0]["slab"], r[1]["slab"]
+    assert a1 == b0 and (b1 - a0) == 512
+    assert r[0]["halo"] == [float(b1 - 1), float(b0)]                # below rank 0: rank 1's top (periodic)
+    assert r[1]["halo"] == [float(a1 - 1), float(a0)]
