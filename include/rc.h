@@ -169,10 +169,10 @@ typedef struct {
                                      (kappa = 1 where wdot = 0).  tau_mix >= 0. */
 } rc_cells;
 
-/* Workspace bytes rc_chem / rc_step use for n cells: the layer-1 input rows of
- * all n cells (32 B per cell in bf16) plus the activations of one cell chunk
- * and partial sums.  A smaller workspace (down to the 256-cell-chunk minimum)
- * runs with smaller chunks.  Alignment 256 B. */
+/* Workspace bytes rc_chem / rc_step use for n cells: the layer-1 input rows and the raw net outputs
+ * of all n cells (32 + 4 n_nets B per cell in bf16) plus the activations of one cell chunk and
+ * partial sums.  A smaller workspace (down to the 256-cell-chunk minimum) runs with smaller chunks.
+ * Alignment 256 B. */
 size_t rc_workspace_bytes(const rc_mech *m, const rc_mlp *n, int64_t ncells);
 
 /* a1: Newton h -> T (h-mode) or h(T) (T-mode); cp, rho.

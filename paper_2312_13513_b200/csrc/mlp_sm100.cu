@@ -348,9 +348,11 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, NS == 0 ? 1 : 2) chem_epi
   __shared__ __align__(8) uint64_t bars[1 + 16];
   __shared__ double red_s[EPI_THREADS / 32];
   const int nse = (ns + 1) & ~1;
-  const int tsz = ThermoSeg::size(ns), psz = (ns * ns + 1) & ~1, pnsz = nn * nse + 32;
+  // P columns by net [nn][nse] | species [32 ints] | b4, y_mean, y_std [nn] each (no global loads per cell)
+  const int tsz = ThermoSeg::size(ns), psz = (ns * ns + 1) & ~1, pnsz = nn * nse + 16 + ((3 * nn + 1) & ~1);
   double *sP = s_tab + tsz, *sPn = sP + psz;
   int *sSpec = reinterpret_cast<int *>(sPn + nn * nse);
+  double *sB4 = sPn + nn * nse + 16, *sYM = sB4 + nn, *sYS = sYM + nn;
   const rcs::Ring<EPI_TILE> ring{reinterpret_cast<uint8_t *>(sPn + pnsz), bars + 1, 2 + ns, nn * a.passes, stages};
   if (threadIdx.x == 0) {
     rcx::mbar_init(&bars[0], 1);
@@ -376,7 +378,12 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, NS == 0 ? 1 : 2) chem_epi
     const int net = e / nse, k = e % nse;
     sPn[e] = k < ns ? sP[k * ns + a.species[net]] : 0.0;
   }
-  for (int e = threadIdx.x; e < nn; e += blockDim.x) sSpec[e] = a.species[e];
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    sSpec[e] = a.species[e];
+    sB4[e] = a.b4[e];
+    sYM[e] = a.ymean[e];
+    sYS[e] = a.ystd[e];
+  }
   __syncthreads();
 
   double qsum = 0.0;
@@ -397,11 +404,11 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, NS == 0 ? 1 : 2) chem_epi
       if (k < ns) v[k] = 0.0;
 #pragma unroll NETUNR
     for (int net = 0; net < nn; ++net) {
-      float o = a.b4[net];
+      float o = (float)sB4[net];
       for (int ps = 0; ps < a.passes; ++ps) o += S4[(net * a.passes + ps) * EPI_TILE];
       if (c.o) c.o[net * c.ld + i] = o;
       const double y = S8[(2 + sSpec[net]) * EPI_TILE];
-      const double dy = inv_boxcox_dy(y > 0.0 ? y : 0.0, (double)o * a.ystd[net] + a.ymean[net], a);
+      const double dy = inv_boxcox_dy(y > 0.0 ? y : 0.0, (double)o * sYS[net] + sYM[net], a);
       const double *pc = sPn + net * nse;  // column species[net] of P, contiguous in k
 #pragma unroll UR
       for (int k = 0; k < CAP; k += 2)
@@ -599,7 +606,8 @@ WsLayout ws_layout(const rc_mlp *n, int cap, int64_t ncells) {
   const bool shared = (n->flags & RC_MLP_SHARED) != 0;
   L.h3 = o; o = al(o + (shared ? (size_t)cap * n->h3 * eb : 0));  // shared net: h3 for the layer-4 kernel
   const int np3 = shared ? 1 : n->h3 / l2_pass_width(n->h3);  // raw outputs per row: one per layer-3 pass
-  L.opart = o; o = al(o + (size_t)n->n_nets * np3 * cap * 4);
+  // raw outputs of EVERY cell of the call (like z): the chemistry epilogue runs once over all cells
+  L.opart = o; o = al(o + (size_t)n->n_nets * np3 * zrows * 4);
   L.total = o;
   return L;
 }
@@ -780,7 +788,7 @@ template <int NS>
 int launch_epilogue_t(const rc_mech *m, const EpiArgs &ea, const CellsDev &c, cudaStream_t s) {
   const int ns = m->ns, nn = ea.n_nets;
   const int stages = 3;
-  const size_t smem = (size_t)(ThermoSeg::size(ns) + ((ns * ns + 1) & ~1) + nn * ((ns + 1) & ~1) + 32) * 8 +
+  const size_t smem = (size_t)(ThermoSeg::size(ns) + ((ns * ns + 1) & ~1) + nn * ((ns + 1) & ~1) + 16 + ((3 * nn + 1) & ~1)) * 8 +
                       rcs::Ring<epi_tile<NS>()>::smem_bytes(2 + ns, nn * ea.passes, stages);
   constexpr int EPI_TILE = epi_tile<NS>(), EPI_THREADS = EPI_TILE + 32;
   const int64_t ntiles = (ea.rows + EPI_TILE - 1) / EPI_TILE;
@@ -932,22 +940,26 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
       L2Args la{mt, n->h2 / NP, nets, (n->h1 + KC - 1) / KC, n->h2, 0, n->d_b2, nullptr, nullptr, cap, (n->h1 % KC) / KATOM};
       if ((rc = launch_l2_pair(NP, prec, m2, la, s))) return rc;
     }
-    // layer 3 + folded layer 4: the same CTA-pair GEMM with the dot epilogue (K = h2, zero-filled to KC)
+    // layer 3 + folded layer 4: the same CTA-pair GEMM with the dot epilogue (K = h2, zero-filled to KC);
+    // the raw outputs land in the all-cells array o [nets][passes][zrows] at this chunk's rows
+    float *oc = opart + c0;
     if (!shared) {
-      L2Args l3{mt, n->h3 / NP3, nets, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, n->d_w4, opart, cap, (n->h2 % KC) / KATOM};
+      L2Args l3{mt, n->h3 / NP3, nets, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, n->d_w4, oc, (int)zrows, (n->h2 % KC) / KATOM};
       if ((rc = launch_l2_pair(NP3, prec, m3, l3, s))) return rc;
     } else {
       // shared net (NEXT-2): layer 3 as a plain GELU layer into h3, then the n_out-wide layer 4
       L2Args l3{mt, n->h3 / NP3, 1, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, nullptr, nullptr, cap, (n->h2 % KC) / KATOM};
       l3.prof_stage = RC_STAGE_L3;
       if ((rc = launch_l2_pair(NP3, prec, m3, l3, s))) return rc;
-      if ((rc = launch_l4(n, w + L.h3, opart, rows, cap, tf32, s))) return rc;
+      if ((rc = launch_l4(n, w + L.h3, oc, rows, (int)zrows, tf32, s))) return rc;
     }
-    EpiArgs ea{c0, rows, cap, nout, shared ? 1 : n->h3 / NP3, n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt, opart,
-               n->d_b4, n->d_ymean, n->d_ystd, m->d_P, m->d_thermo, n->d_species, qpart, {}};
+    launches += 4;
+  }
+  {  // a5 once over every cell of the call (one streaming pass, like the prologue)
+    EpiArgs ea{0, (int)c.n, (int)zrows, nout, shared ? 1 : n->h3 / NP3, n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt,
+               opart, n->d_b4, n->d_ymean, n->d_ystd, m->d_P, m->d_thermo, n->d_species, qpart, {}};
     for (int q = 0; q <= 16; ++q) ea.binom[q] = q <= n->inv_lambda ? binom(n->inv_lambda, q) : 0.0;
     if ((rc = launch_epilogue(m, ea, c, s))) return rc;
-    launches += 5;
   }
   if (c.red) {
     ProfScope prof(RC_STAGE_FINALIZE, s);
