@@ -101,8 +101,9 @@ __global__ void __launch_bounds__(KIN_THREADS) kinetics_kernel(const double *__r
         sR[k * KIN_TILE + j] = 0.0;
       }
     const double lnp0RT = log(KIN_P0 / RC_RU) - lnT;
-#pragma unroll 1
-    for (int r = 0; r < nr; ++r) {
+    // net rate of progress of reaction r (reads only: two reactions are evaluated back to back so
+    // their exp chains overlap; the rate updates follow)
+    auto rate = [&](int r) -> double {
       const double *R = REC + 48 * r;
       const int type = (int)R[R_TYPE];
       const double lnk = R[R_LNA] + R[R_B] * lnT - R[R_ER] * invT;
@@ -145,12 +146,22 @@ __global__ void __launch_bounds__(KIN_THREADS) kinetics_kernel(const double *__r
         fwd *= M;
         rev *= M;
       }
-      const double qn = fwd - rev;
+      return fwd - rev;
+    };
+    auto update = [&](int r, double qn) {
+      const double *R = REC + 48 * r;
 #pragma unroll
       for (int s = 0; s < 6; ++s) {
         const int q = (int)R[R_PSP + s];
         if (q >= 0) sR[q * KIN_TILE + j] = fma(R[R_PNU + s], qn, sR[q * KIN_TILE + j]);
       }
+    };
+#pragma unroll 1
+    for (int r = 0; r < nr; r += 2) {
+      const double q0 = rate(r);
+      const double q1 = r + 1 < nr ? rate(r + 1) : 0.0;
+      update(r, q0);
+      if (r + 1 < nr) update(r + 1, q1);
     }
     // wdot_k = W_k sum_r nu_rk q_r; LES: PaSR factor (rc.h tau_mix, R19); qdot
     double scale = 1.0;
