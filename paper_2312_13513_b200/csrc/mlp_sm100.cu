@@ -144,120 +144,104 @@ __global__ void __launch_bounds__(PRO_THREADS) prologue_kernel(ProArgs a, CellsD
 // row), with its W4 slice (8 outputs x 16 columns) held in registers for all the warp's rows; the
 // 8 per-lane partial dots are combined by a 9-shuffle reduce-scatter (lane 4o holds output o).
 // Outputs beyond 8 run as further passes of 8.
-constexpr int L4_ROWS = 16;     // rows per stage: one bulk copy of 16 contiguous h3 rows
-constexpr int L4_STAGES = 4;
-constexpr int L4_THREADS = 32 + 32 * (L4_ROWS / 2);  // producer warp + one consumer warp per 2 rows
+template <bool TF32> constexpr int l4_warps() { return TF32 ? 2 : 4; }  // per CTA; each streams its own 16-row blocks
+constexpr int L4_MAXO = 32;      // outputs (multiple of 8 after padding)
 
+// m16n8k16 bf16 (or m16n8k8 tf32) warp MMA, fp32 accumulate
 template <bool TF32>
-__global__ void __launch_bounds__(L4_THREADS, 1) l4_kernel(const void *__restrict__ h3, const float *__restrict__ w4,
-                                                           float *__restrict__ o, int rows, int h3n, int nout, int cap,
-                                                           int o0) {
-  constexpr int CJ = 2;  // 8-column chunks per lane (h3 <= 512)
-  constexpr int EB = TF32 ? 4 : 2;
+__device__ __forceinline__ void mma16n8(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  if constexpr (TF32)
+    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  else
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// Layer 4 of the shared net on the warp-level tensor-core MMA: o[16 rows][8 outputs] tiles,
+// K = h3 in atoms of 16 (bf16) / 8 (tf32).  W4 enters as an exact hi + lo pair of operand-type
+// values (two MMAs per atom), so the weights keep fp32 accuracy; h3 is the operand-type value the
+// layer-3 GEMM stored.  Each warp double-buffers its own 16-row blocks of h3 (one bulk copy each).
+template <bool TF32>
+__global__ void __launch_bounds__(32 * l4_warps<TF32>()) l4_kernel(const void *__restrict__ h3, const float *__restrict__ w4,
+                                                           float *__restrict__ o, int rows, int h3n, int nout, int cap) {
+  constexpr int EB = TF32 ? 4 : 2, KA = TF32 ? 8 : 16, L4_WARPS = l4_warps<TF32>();
   extern __shared__ __align__(128) uint8_t l4s[];
-  __shared__ __align__(8) uint64_t full[L4_STAGES], empty[L4_STAGES];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t row_bytes = (uint32_t)h3n * EB, stage_bytes = L4_ROWS * row_bytes;
-  const int ntiles = (rows + L4_ROWS - 1) / L4_ROWS;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < L4_STAGES; ++s) {
-      rcx::mbar_init(&full[s], 1);
-      rcx::mbar_init(&empty[s], L4_ROWS / 2);
+  __shared__ __align__(8) uint64_t full[L4_WARPS][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int nt = (nout + 7) / 8;                       // 8-output n tiles
+  const uint32_t row_bytes = (uint32_t)h3n * EB, blk = 16 * row_bytes;
+  // W4 hi / lo as [n][k] operand values (32-bit words: bf16 pairs or tf32)
+  uint32_t *wh = reinterpret_cast<uint32_t *>(l4s);
+  const int wwords = nt * 8 * h3n * EB / 4;
+  uint32_t *wl = wh + wwords;
+  uint8_t *abuf = reinterpret_cast<uint8_t *>(wl + wwords) + warp * 2 * blk;
+  for (int e = threadIdx.x; e < nt * 8 * h3n; e += blockDim.x) {
+    const int n = e / h3n, k = e % h3n;
+    const float w = n < nout ? w4[(size_t)n * h3n + k] : 0.f;
+    if constexpr (TF32) {
+      const float hi = rcm::tf32_rn(w);
+      reinterpret_cast<float *>(wh)[e] = hi;
+      reinterpret_cast<float *>(wl)[e] = rcm::tf32_rn(w - hi);
+    } else {
+      const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+      reinterpret_cast<__nv_bfloat16 *>(wh)[e] = hi;
+      reinterpret_cast<__nv_bfloat16 *>(wl)[e] = __float2bfloat16_rn(w - __bfloat162float(hi));
     }
+  }
+  if (lane == 0) {
+    rcx::mbar_init(&full[warp][0], 1);
+    rcx::mbar_init(&full[warp][1], 1);
     rcx::fence_mbar_init();
   }
   __syncthreads();
-  if (warp == 0) {  // producer: one bulk copy per 16-row tile
-    if (lane == 0) {
-      int it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        const int s = it % L4_STAGES;
-        if (it >= L4_STAGES) rcx::mbar_wait_sleep(&empty[s], (uint32_t)(it / L4_STAGES - 1) & 1u);
-        const int nr = rows - t * L4_ROWS < L4_ROWS ? rows - t * L4_ROWS : L4_ROWS;
-        rcx::mbar_arrive_expect_tx(&full[s], nr * row_bytes);
-        rcx::bulk_g2s(l4s + s * stage_bytes, static_cast<const uint8_t *>(h3) + (size_t)t * stage_bytes, nr * row_bytes,
-                      &full[s]);
-      }
-    }
-    return;
-  }
-  const int nch = h3n / 8;
-  float w[CJ][8][8];
-#pragma unroll
-  for (int j = 0; j < CJ; ++j)
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int c = lane + 32 * j, k = 8 * c + i, out = o0 + q;
-        w[j][i][q] = (c < nch && out < nout) ? w4[(size_t)out * h3n + k] : 0.f;
-      }
-  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-  const int q = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
-  const int cw = warp - 1;  // consumer warp: rows 2 cw, 2 cw + 1 of each tile
+  const int nblk = (rows + 15) / 16, wstride = gridDim.x * L4_WARPS;
+  auto issue = [&](int b, int slot) {
+    const int nr = rows - b * 16 < 16 ? rows - b * 16 : 16;
+    rcx::mbar_arrive_expect_tx(&full[warp][slot], nr * row_bytes);
+    rcx::bulk_g2s(abuf + slot * blk, static_cast<const uint8_t *>(h3) + (size_t)b * blk, nr * row_bytes, &full[warp][slot]);
+  };
   int it = 0;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-    const int s = it % L4_STAGES;
-    rcx::mbar_wait(&full[s], (uint32_t)(it / L4_STAGES) & 1u);
-    const uint8_t *st = l4s + s * stage_bytes;
-    float x[2][CJ][8];
-#pragma unroll
-    for (int rr = 0; rr < 2; ++rr)
-#pragma unroll
-      for (int j = 0; j < CJ; ++j) {
-        const int c = lane + 32 * j;
-        const uint8_t *src = st + (2 * cw + rr) * row_bytes + c * 8 * EB;
-        if (c < nch) {
-          if constexpr (TF32) {
-            const float4 a = *reinterpret_cast<const float4 *>(src), b = *reinterpret_cast<const float4 *>(src + 16);
-            x[rr][j][0] = a.x; x[rr][j][1] = a.y; x[rr][j][2] = a.z; x[rr][j][3] = a.w;
-            x[rr][j][4] = b.x; x[rr][j][5] = b.y; x[rr][j][6] = b.z; x[rr][j][7] = b.w;
-          } else {
-            const uint4 v = *reinterpret_cast<const uint4 *>(src);
-            const uint32_t u[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              x[rr][j][2 * i] = __uint_as_float(u[i] << 16);
-              x[rr][j][2 * i + 1] = __uint_as_float(u[i] & 0xffff0000u);
-            }
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) x[rr][j][i] = 0.f;
-        }
-      }
-    __syncwarp();
-    if (lane == 0) rcx::mbar_arrive(&empty[s]);  // stage rows read into registers
-#pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
-      const int r = t * L4_ROWS + 2 * cw + rr;
-      float acc[8];
-#pragma unroll
-      for (int qq = 0; qq < 8; ++qq) acc[qq] = 0.f;
-#pragma unroll
-      for (int j = 0; j < CJ; ++j)
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int qq = 0; qq < 8; ++qq) acc[qq] = fmaf(x[rr][j][i], w[j][i][qq], acc[qq]);
-      // reduce-scatter over the warp: xor 16 halves the outputs a lane holds (8 -> 4), xor 8
-      // (4 -> 2), xor 4 (2 -> 1), then xor 2 and xor 1 sum the last one
-      float u[4], tt[2];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float send = b4 ? acc[i] : acc[i + 4], keep = b4 ? acc[i + 4] : acc[i];
-        u[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  const int b0 = blockIdx.x * L4_WARPS + warp;
+  if (lane == 0 && b0 < nblk) issue(b0, 0);
+  for (int b = b0; b < nblk; b += wstride, ++it) {
+    const int slot = it & 1;
+    if (lane == 0 && b + wstride < nblk) issue(b + wstride, slot ^ 1);  // the other buffer is free (read last round)
+    rcx::mbar_wait(&full[warp][slot], (uint32_t)(it >> 1) & 1u);
+    const uint8_t *A = abuf + slot * blk;
+    const int nr = rows - b * 16 < 16 ? rows - b * 16 : 16;
+    for (int n0 = 0; n0 < nt; ++n0) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f}, acl[4] = {0.f, 0.f, 0.f, 0.f};  // hi and lo chains
+      for (int k0 = 0; k0 < h3n; k0 += KA) {
+        uint32_t af[4];
+        // A fragment (row-major 16 x KA): a0 (g, c), a1 (g + 8, c), a2 (g, c + KA/2), a3 (g + 8, c + KA/2)
+        const int c = TF32 ? k0 + t : k0 + 2 * t;
+        const int ga = g < nr ? g : 0, gb = g + 8 < nr ? g + 8 : 0;  // rows past the block end: any valid row
+        af[0] = *reinterpret_cast<const uint32_t *>(A + ga * row_bytes + c * EB);
+        af[1] = *reinterpret_cast<const uint32_t *>(A + gb * row_bytes + c * EB);
+        af[2] = *reinterpret_cast<const uint32_t *>(A + ga * row_bytes + (c + KA / 2) * EB);
+        af[3] = *reinterpret_cast<const uint32_t *>(A + gb * row_bytes + (c + KA / 2) * EB);
+        // B fragment (col-major KA x 8 = W4 [n][k]): b0 (k = c, n = g), b1 (k = c + KA/2, n = g)
+        const int wi = ((n0 * 8 + g) * h3n + c) * EB / 4, wj = ((n0 * 8 + g) * h3n + c + KA / 2) * EB / 4;
+        mma16n8<TF32>(acc, af, wh[wi], wh[wj]);
+        mma16n8<TF32>(acl, af, wl[wi], wl[wj]);
       }
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const float send = b3 ? u[i] : u[i + 2], keep = b3 ? u[i + 2] : u[i];
-        tt[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      for (int e = 0; e < 4; ++e) acc[e] += acl[e];
+      // D fragment: d0, d1 (row g, outputs 2t, 2t+1), d2, d3 (row g + 8)
+      const int r0 = b * 16 + g, r1 = r0 + 8, q0 = n0 * 8 + 2 * t;
+      if (g < nr) {
+        if (q0 < nout) o[(size_t)q0 * cap + r0] = acc[0];
+        if (q0 + 1 < nout) o[(size_t)(q0 + 1) * cap + r0] = acc[1];
       }
-      float v = (b2 ? tt[1] : tt[0]) + __shfl_xor_sync(0xffffffffu, b2 ? tt[0] : tt[1], 4);
-      v += __shfl_xor_sync(0xffffffffu, v, 2);
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
-      if ((lane & 3) == 0 && o0 + q < nout && r < rows) o[(size_t)(o0 + q) * cap + r] = v;
+      if (g + 8 < nr) {
+        if (q0 < nout) o[(size_t)q0 * cap + r1] = acc[2];
+        if (q0 + 1 < nout) o[(size_t)(q0 + 1) * cap + r1] = acc[3];
+      }
     }
+    __syncwarp();  // every lane has read this buffer before it is refilled (two rounds later)
   }
 }
 
@@ -802,18 +786,18 @@ int launch_epilogue_t(const rc_mech *m, const EpiArgs &ea, const CellsDev &c, cu
 }
 
 int launch_l4(const rc_mlp *n, const void *h3, float *o, int rows, int cap, bool tf32, cudaStream_t s) {
-  if (n->h3 > 512 || n->h3 % 8) return rc_fail(RC_EUNSUPPORTED, "shared net: layer-4 kernel needs h3 <= 512");
+  if (n->n_nets > L4_MAXO || n->h3 % 16) return rc_fail(RC_EUNSUPPORTED, "shared net: layer 4 needs <= 32 outputs, h3 % 16 == 0");
   ProfScope prof(RC_STAGE_L4, s);
-  const size_t smem = (size_t)L4_STAGES * L4_ROWS * n->h3 * (tf32 ? 4 : 2);
+  const int EB = tf32 ? 4 : 2, nt = (n->n_nets + 7) / 8, W = tf32 ? l4_warps<true>() : l4_warps<false>();
+  const size_t smem = 2 * (size_t)nt * 8 * n->h3 * EB + (size_t)W * 2 * 16 * n->h3 * EB;
+  if (smem > 227 * 1024) return rc_fail(RC_EUNSUPPORTED, "shared net: layer-4 shared memory (%zu B)", smem);
   const void *k = tf32 ? (const void *)l4_kernel<true> : (const void *)l4_kernel<false>;
-  int64_t grid = rc_resident_blocks(k, L4_THREADS, smem);
-  const int64_t ntiles = (rows + L4_ROWS - 1) / L4_ROWS;
-  if (grid > ntiles) grid = ntiles;
-  for (int o0 = 0; o0 < n->n_nets; o0 += 8) {
-    if (tf32) l4_kernel<true><<<(unsigned)grid, L4_THREADS, smem, s>>>(h3, n->d_w4, o, rows, n->h3, n->n_nets, cap, o0);
-    else l4_kernel<false><<<(unsigned)grid, L4_THREADS, smem, s>>>(h3, n->d_w4, o, rows, n->h3, n->n_nets, cap, o0);
-    RC_LAUNCH_CHECK();
-  }
+  int64_t grid = rc_resident_blocks(k, 32 * W, smem);
+  const int64_t want = ((rows + 15) / 16 + W - 1) / W;
+  if (grid > want) grid = want;
+  if (tf32) l4_kernel<true><<<(unsigned)grid, 32 * W, smem, s>>>(h3, n->d_w4, o, rows, n->h3, n->n_nets, cap);
+  else l4_kernel<false><<<(unsigned)grid, 32 * W, smem, s>>>(h3, n->d_w4, o, rows, n->h3, n->n_nets, cap);
+  RC_LAUNCH_CHECK();
   return RC_OK;
 }
 
