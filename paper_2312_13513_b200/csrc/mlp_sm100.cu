@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, NS == 0 ? 1 : 2) chem_epi
   constexpr int EPI_TILE = epi_tile<NS>(), EPI_THREADS = EPI_TILE + 32;
   constexpr int CAP = NS ? NS : RC_MAX_NS;
   constexpr int UR = NS ? NS : 1;
-  constexpr int NETUNR = NS == 9 ? 8 : 1;
+  constexpr int NETUNR = 2;  // partial unroll: the fully unrolled net loop overflowed the instruction cache
   const int ns = NS ? NS : a.ns;
   const int nn = a.n_nets;
   extern __shared__ __align__(16) double s_tab[];  // thermo segment | P | P columns by net | species | ring
