@@ -135,3 +135,31 @@ def test_ldu_to_csr_matches_scipy(props):
         # and the CSR operator equals the oracle's ldu product
         x = np.random.default_rng(s).normal(size=N)
         np.testing.assert_allclose(A @ x, oracle.ldu_matvec(MESH, upn[s], dgn[s], x), rtol=1e-12, atol=1e-12 * np.abs(dgn[s]).max())
+
+
+def test_ch4_21_systems():
+    """CH4 set: 20 species + energy = 21 systems through the runtime-ns path of the assembly; faces
+    bitwise, diagonals 1e-14, CSR values equal to the ldu entries."""
+    import torch
+
+    import paper_2312_13513_b200 as rc
+    m = mech("ch4_20sp")
+    om = oracle.Mech(m)
+    mesh = (10, 9, 8, 5e-5, 5e-5, 5e-5)
+    n = 720
+    c = make_cells("C4", 7_000_000, 7_000_000 + n)
+    r = oracle.step(om, None, c["T_true"], c["p"], c["Y"], mode="T", chem=False)
+    g = oracle.laplacian_gamma(20, r["rho"], r["D"], r["lambda"], r["cp"])
+    upO, dgO = oracle.laplacian(mesh, g)
+    M = rc.Mechanism(m)
+    st = rc.CellState(n, 20, 0)
+    st.load(c["T_true"], c["p"], c["Y"])
+    for k, v in (("rho", r["rho"]), ("lam", r["lambda"]), ("cp", r["cp"])):
+        getattr(st, k)[:n].copy_(torch.from_numpy(np.ascontiguousarray(v)))
+    st.D[:, :n].copy_(torch.from_numpy(np.ascontiguousarray(r["D"])))
+    up = torch.empty(21, 3 * n, dtype=torch.float64, device="cuda")
+    dg = torch.empty(21, n, dtype=torch.float64, device="cuda")
+    rc.rc_laplacian(M, mesh, st.cells(rc.RC_MODE_T), up, dg)
+    torch.cuda.synchronize()
+    assert np.array_equal(up.cpu().numpy(), upO)
+    np.testing.assert_allclose(dg.cpu().numpy(), dgO, rtol=1e-14)

@@ -56,3 +56,16 @@ def test_paper_shape_full_chunk_sampled(prec, tol, dtol):
     o = run_oracle("C2", cs, b=b)
     gs = {k: g[k][:, cols] if g[k].ndim == 2 else g[k][cols] for k in ("o", "wdot", "qdot")}
     _check(gs, o, tol, dtol, f"C2 precision {prec}")
+
+
+def test_ch4_shared_net_19_outputs():
+    """CH4 (Ns = 20, 19 outputs: three 8-output MMA tiles in layer 4, the last one padded), bf16,
+    small widths so every tile of 2,000 cells is checked."""
+    b = make_bundle("ch4_20sp", hidden=(64, 32, 16), shared=True)
+    assert b["n_nets"] == 19
+    c = inputs("C4", begin=3_000_000, end=3_002_000)
+    o = run_oracle("C4", c, b=b)
+    g = Gpu("C4", precision=0, b=b).run(c)
+    eo, ew = rel_fro(g["o"], o["o"]), rel_fro(g["wdot"], o["wdot"])
+    print(f"\n  shared net CH4: o {eo:.2e} wdot {ew:.2e}")
+    assert eo <= BF16_TOL and ew <= BF16_DERIVED_TOL
