@@ -35,8 +35,8 @@ struct L12Args {
   int m_tiles, nets, chunks, N, stages;
   const float *bias;  // b2 [nets][N]
 };
-bool l12_supported(int h1, int h2, int kz);
-int launch_l12(int KZ, const CUtensorMap *maps, const L12Args &a, cudaStream_t s);
+bool l12_supported(int h1, int h2, int kz, bool tf32);
+int launch_l12(int KZ, bool tf32, const CUtensorMap *maps, const L12Args &a, cudaStream_t s);
 
 // maps: {A, B piece 1, B piece 2, out store, A lo, B1 lo, B2 lo, out lo store, bias operand piece 1,
 //        bias operand piece 2} (lo: precision 2 only; bias operand tiles: bf16 only)

@@ -62,17 +62,26 @@ __device__ long long g_l12trace[4][6][64][4];
 
 // R = ring depth: chunk g uses W2 stage and A slot g % R, so one barrier per chunk tells the
 // layer-2 issuer that both operands are in place (every wait between MMAs costs a tensor-pipe bubble)
-template <int KZ, int R>
+// TF: the TF32 mode (RC_TF32): fp32 (tf32-rounded) operands, kind::tf32 MMAs, a 128-byte operand row
+// holds 32 elements, so a chunk is 32 h1 columns (K = 32 of layer 2, the same 4 MMA K atoms of 32
+// bytes); erf-form GELU in fp32 with one tf32 rounding; b2 enters as a K = 8 (hi, lo) tf32 operand.
+template <int KZ, int R, bool TF>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
     l12_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapW1,
                const __grid_constant__ CUtensorMap mapW2a, const __grid_constant__ CUtensorMap mapW2b,
                const __grid_constant__ CUtensorMap mapOut, const __grid_constant__ CUtensorMap mapBa,
                const __grid_constant__ CUtensorMap mapBb, L12Args a) {
-  constexpr uint32_t Z_BYTES = 128 * KZ * 2, W1_CH = 32 * KZ * 2;  // W1: 32 rows per CTA and chunk
-  // KZ = 16: this CTA's W1 rows of all its pair's chunks of a net (13 KB, one 5D box per net);
-  // KZ = 32 (CH4): a 4-deep ring of per-chunk W1 rows (8 KB instead of 26 KB, so the W2/A ring
-  // stays 4 deep)
-  constexpr bool W1RING = KZ == 32;
+  constexpr int EB = TF ? 4 : 2;                  // operand element bytes
+  constexpr int CW = TF ? 32 : 64;                // h1 columns per chunk: one 128-byte operand row
+  constexpr uint32_t FMT = rcm::Elem<TF>::FMT;
+  constexpr int KATOM = rcm::Elem<TF>::KATOM;
+  constexpr uint32_t Z_BYTES = 128 * KZ * EB, W1_CH = (CW / 2) * KZ * EB;  // W1: CW/2 rows per CTA and chunk
+  // KZ = 16 (bf16): this CTA's W1 rows of all its pair's chunks of a net (13 KB, one 5D box per net);
+  // KZ = 32 (CH4) and TF32: a 4-deep ring of per-chunk W1 rows (8 KB instead of 26 KB, so the W2/A
+  // ring stays 4 deep)
+  constexpr bool W1RING = KZ == 32 || TF;
+  constexpr uint32_t STGB = TF ? 2048 : 1024;     // h2 store staging buffer: 32 rows x 16 columns
+  constexpr int NSTG = TF ? 1 : 2;                // staging buffers per drain warp
   constexpr int RW = 4;
   constexpr uint32_t STAGE_BYTES = W2T;                             // TMA bytes per CTA
   constexpr uint32_t BK_BYTES = (NP / 2) * 32, BK_AL = 7168;        // b2 as a K = 16 operand: 200 rows x 32 B
@@ -87,8 +96,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
   uint8_t *sA = sW + S * STAGE;              // R x SLOT
   uint8_t *sZ = sA + R * SLOT;               // 2 x Z_BYTES
   uint8_t *sW1 = sZ + 2 * ((Z_BYTES + 1023u) & ~1023u);  // this CTA's W1 rows of its pair's chunks of the net
-  uint8_t *sST = sW1 + (W1RING ? RW * W1_CH : ((((a.chunks + 1) / 2) * W1_CH + 1023u) & ~1023u));  // 8 drain warps x 2 x 1 KB h2 staging
-  uint8_t *sBK = sST + (NEPI - NPROD) * 2 * 1024;  // 2 x b2 operand tile (with the z tile of the same buffer)
+  uint8_t *sST = sW1 + (W1RING ? RW * W1_CH : ((((a.chunks + 1) / 2) * W1_CH + 1023u) & ~1023u));  // drain h2 staging
+  uint8_t *sBK = sST + (NEPI - NPROD) * NSTG * STGB;  // 2 x b2 operand tile (with the z tile of the same buffer)
   uint8_t *sOnes = sBK + 2 * BK_AL;                // 128 rows x 16 bf16 ones: the A side of the b2 MMA
   uint64_t *bar = reinterpret_cast<uint64_t *>(sOnes + 4096);
   // ready[i]: leader = both operands of chunk i in both CTAs (its slot: own copier or incoming copy;
@@ -134,14 +143,15 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
     rcx::mbar_init(c2emptyB, 2 * (NEPI - NPROD));  // piece 2
     rcx::fence_mbar_init();
   }
-  for (int i = threadIdx.x; i < 1024; i += L12_THREADS) reinterpret_cast<uint32_t *>(sOnes)[i] = 0x3F803F80u;
+  // the ones tile: 128 rows x 32 bytes of 1.0 (bf16 pairs or fp32)
+  for (int i = threadIdx.x; i < 1024; i += L12_THREADS) reinterpret_cast<uint32_t *>(sOnes)[i] = TF ? 0x3F800000u : 0x3F803F80u;
   rcm::fence_async_smem();  // the ones tile is read by the tensor core (async proxy)
   if (warp == W_MMA) rcx::tmem_alloc_pair(tmem_slot, 512);
   rcx::tc_fence_before();
   rcx::cluster_sync();
   rcx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int C = a.chunks;  // 64-column h1 chunks (K chunks of layer 2)
+  const int C = a.chunks;  // CW-column h1 chunks (K chunks of layer 2)
   const int pairs = a.m_tiles / 2;
   const int total = a.nets * pairs;
   const int cl = blockIdx.x >> 2, ncl = gridDim.x >> 2;
@@ -180,7 +190,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           const int j = (int)(nwr % RW);
           rcx::mbar_wait_sleep(&w1empty[j], ((nwr / RW) & 1) ^ 1);
           rcx::mbar_arrive_expect_tx_cluster(w1full0 + j * 8, W1_CH);
-          rcx::tma_load_3d_pair(sW1 + j * W1_CH, &mapW1, &w1full[j], 0, wc * 64 + prank * 32, wt / pairs);
+          rcx::tma_load_3d_pair(sW1 + j * W1_CH, &mapW1, &w1full[j], 0, wc * CW + prank * (CW / 2), wt / pairs);
           // next own chunk: c + 2 in the tile, else the first own chunk of the next tile
           wg = (wc + 2 < C) ? wg + 2 : (wg / C + 1) * C + (uint32_t)pr;
         }
@@ -200,8 +210,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           rcx::mbar_wait_sleep(&freed[s], ((g / S) & 1) ^ 1);
           rcx::mbar_arrive_expect_tx_cluster(ready0 + s * 8, STAGE_BYTES);
           uint8_t *st = sW + s * STAGE;
-          rcx::tma_load_3d_pair(st, &mapW2a, &ready[s], c * 64, pr * NP + prank * H1, net);
-          rcx::tma_load_3d_pair(st + H1 * 128, &mapW2b, &ready[s], c * 64, pr * NP + P1 + prank * H2, net);
+          rcx::tma_load_3d_pair(st, &mapW2a, &ready[s], c * CW, pr * NP + prank * H1, net);
+          rcx::tma_load_3d_pair(st + H1 * 128, &mapW2b, &ready[s], c * CW, pr * NP + P1 + prank * H2, net);
           if (c == C / 2 && tile + ncl < total) load_zb(tile + ncl, it + 1);
         }
       }
@@ -210,7 +220,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
     {  // ------------------------------ layer-1 MMA issuer (pair leaders; converged warp, elected lane issues)
       // Runs ahead of the layer-2 issuer by up to NA1 chunks (the layer-1 accumulators), so the
       // GELU + DSMEM exchange of a half-chunk overlaps several layer-2 chunk periods.
-      constexpr uint32_t id1 = rcx::make_idesc(1u, 256, 64);
+      constexpr uint32_t id1 = rcx::make_idesc(FMT, 256, CW);
       uint32_t g = 0, nw = 0;
       int it = 0, cur_net = -1;
       for (int tile = cl; tile < total; tile += ncl, ++it) {
@@ -225,7 +235,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
         TR(4, it * C, 0);
         rcx::mbar_wait_sleep(&zfull[zb], (it >> 1) & 1);
         TR(4, it * C, 1);
-        const uint64_t dz = rcm::desc_sw<KZ * 2>(sZ + zb * ((Z_BYTES + 1023u) & ~1023u));
+        const uint64_t dz = rcm::desc_sw<KZ * EB>(sZ + zb * ((Z_BYTES + 1023u) & ~1023u));
         for (int c = pr; c < C; c += 2, ++g) {  // g counts this pair's chunks
           const uint32_t b = g % NA1;
           TR(4, it * C + c, 2);
@@ -234,11 +244,11 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           const int j = (int)(g % RW);  // W1RING entry of this own chunk (g counts own chunks)
           if (W1RING) rcx::mbar_wait(&w1full[j], (g / RW) & 1);
           rcx::tc_fence_after();
-          const uint64_t dw = rcm::desc_sw<KZ * 2>(W1RING ? sW1 + j * W1_CH : sW1 + (c >> 1) * W1_CH);
+          const uint64_t dw = rcm::desc_sw<KZ * EB>(W1RING ? sW1 + j * W1_CH : sW1 + (c >> 1) * W1_CH);
           if (rcx::elect_one()) {
 #pragma unroll
-            for (int k = 0; k < KZ / 16; ++k)
-              rcx::mma_bf16_pair(tmem + TMEM_ACC1 + b * 64, dz + 2 * k, dw + 2 * k, id1, k != 0);
+            for (int k = 0; k < KZ / KATOM; ++k)
+              rcm::mma_pair<TF>(tmem + TMEM_ACC1 + b * 64, dz + 2 * k, dw + 2 * k, id1, k != 0);
             rcx::mma_commit_pair_mask(&a1full[b], pair_mask);
             if (W1RING) rcx::mma_commit_pair_mask(&w1empty[j], pair_mask);
           }
@@ -251,7 +261,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
   } else if (warp == W_MMA) {
     if (prank == 0) {  // ------------------------------------------------ layer-2 MMA issuer (pair leaders)
       // the whole warp runs the loop converged; one elected lane issues (descriptors stay uniform)
-      constexpr uint32_t idp1 = rcx::make_idesc(1u, 256, P1), idp2 = rcx::make_idesc(1u, 256, P2);
+      constexpr uint32_t idp1 = rcx::make_idesc(FMT, 256, P1), idp2 = rcx::make_idesc(FMT, 256, P2);
       uint32_t G = 0;
       int it = 0;
       for (int tile = cl; tile < total; tile += ncl, ++it, G += C) {
@@ -275,19 +285,19 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
             rcx::mbar_wait_sleep(c2empty, (it & 1) ^ 1);
             rcx::tc_fence_after();
             if (rcx::elect_one()) {
-              rcx::mma_bf16_pair(tmem, d1, dbk, idp1, 0);
-              rcx::mma_bf16_pair(tmem, da, db, idp1, 1);
+              rcm::mma_pair<TF>(tmem, d1, dbk, idp1, 0);
+              rcm::mma_pair<TF>(tmem, da, db, idp1, 1);
             }
             __syncwarp();
             rcx::mbar_wait(c2emptyB, (it & 1) ^ 1);
             rcx::tc_fence_after();
             if (rcx::elect_one()) {
-              rcx::mma_bf16_pair(tmem + P1, d1, dbk + ((H1 * 32) >> 4), idp2, 0);
-              rcx::mma_bf16_pair(tmem + P1, da, db + ((H1 * 128) >> 4), idp2, 1);
+              rcm::mma_pair<TF>(tmem + P1, d1, dbk + ((H1 * 32) >> 4), idp2, 0);
+              rcm::mma_pair<TF>(tmem + P1, da, db + ((H1 * 128) >> 4), idp2, 1);
 #pragma unroll
               for (int k = 1; k < 4; ++k) {
-                rcx::mma_bf16_pair(tmem, da + 2 * k, db + 2 * k, idp1, 1);
-                rcx::mma_bf16_pair(tmem + P1, da + 2 * k, db + ((H1 * 128) >> 4) + 2 * k, idp2, 1);
+                rcm::mma_pair<TF>(tmem, da + 2 * k, db + 2 * k, idp1, 1);
+                rcm::mma_pair<TF>(tmem + P1, da + 2 * k, db + ((H1 * 128) >> 4) + 2 * k, idp2, 1);
               }
               rcx::mma_commit_pair_mask(&freed[s], (uint16_t)0xF);
             }
@@ -297,9 +307,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           }
           if (rcx::elect_one()) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {  // K16 steps: 32-byte atoms along the 128-byte rows
-              rcx::mma_bf16_pair(tmem, da + 2 * k, db + 2 * k, idp1, 1);
-              rcx::mma_bf16_pair(tmem + P1, da + 2 * k, db + ((H1 * 128) >> 4) + 2 * k, idp2, 1);
+            for (int k = 0; k < 4; ++k) {  // K atoms: 32-byte steps along the 128-byte rows
+              rcm::mma_pair<TF>(tmem, da + 2 * k, db + 2 * k, idp1, 1);
+              rcm::mma_pair<TF>(tmem + P1, da + 2 * k, db + ((H1 * 128) >> 4) + 2 * k, idp2, 1);
             }
             rcx::mma_commit_pair_mask(&freed[s], (uint16_t)0xF);  // all four CTAs wait for both pairs
           }
@@ -358,31 +368,50 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
       rcx::mbar_wait_sleep(&a1full[b], (lg / NA1) & 1);
       if (warp == 0) TR(1, g, 1);
       rcx::tc_fence_after();
-      uint32_t v[2][16];
-      rcx::tmem_ld16(tmem + tq + TMEM_ACC1 + b * 64 + ph * 32, v[0]);
-      rcx::tmem_ld16(tmem + tq + TMEM_ACC1 + b * 64 + ph * 32 + 16, v[1]);
-      rcx::tmem_ld_wait();
-      rcx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) rcx::mbar_arrive_cluster(a1empty0 + b * 8);
-      ++lg;
-      uint32_t pk[2][8];
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          pk[h][j] = rcm::gelu_half_f16x2_bf16x2(rcm::cvt_f16x2(__uint_as_float(v[h][2 * j]), __uint_as_float(v[h][2 * j + 1])));
-      const int slot = (int)(g % R);
-      rcx::mbar_wait_sleep(&freed[slot], ((g / R) & 1) ^ 1);  // both pairs are done with the slot
-      if (warp == 0) TR(1, g, 2);
-      // columns [32 ph, 32 ph + 32) of the chunk = 16-byte units 4 ph .. 4 ph + 3 of the 128-byte row
-      uint8_t *r = sA + slot * SLOT + row * 128;
+      uint8_t *r = sA + (g % R) * SLOT + row * 128;
       const int x = row & 7;
+      if constexpr (TF) {  // 16 fp32 columns per warp: GELU, one tf32 rounding
+        uint32_t v[16];
+        rcx::tmem_ld16(tmem + tq + TMEM_ACC1 + b * 64 + ph * 16, v);
+        rcx::tmem_ld_wait();
+        rcx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) rcx::mbar_arrive_cluster(a1empty0 + b * 8);
+        ++lg;
+        float y[16];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        *reinterpret_cast<uint4 *>(r + (((4 * ph + u) ^ x) << 4)) =
-            make_uint4(pk[u >> 1][4 * (u & 1)], pk[u >> 1][4 * (u & 1) + 1], pk[u >> 1][4 * (u & 1) + 2],
-                       pk[u >> 1][4 * (u & 1) + 3]);
+        for (int j = 0; j < 16; ++j) y[j] = rcm::tf32_rn(rcm::gelu_erf_f32(__uint_as_float(v[j])));
+        const int slot = (int)(g % R);
+        rcx::mbar_wait_sleep(&freed[slot], ((g / R) & 1) ^ 1);  // both pairs are done with the slot
+        // columns [16 ph, 16 ph + 16) of the chunk = 16-byte units 4 ph .. 4 ph + 3 of the 128-byte row
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          *reinterpret_cast<float4 *>(r + (((4 * ph + u) ^ x) << 4)) = make_float4(y[4 * u], y[4 * u + 1], y[4 * u + 2], y[4 * u + 3]);
+      } else {
+        uint32_t v[2][16];
+        rcx::tmem_ld16(tmem + tq + TMEM_ACC1 + b * 64 + ph * 32, v[0]);
+        rcx::tmem_ld16(tmem + tq + TMEM_ACC1 + b * 64 + ph * 32 + 16, v[1]);
+        rcx::tmem_ld_wait();
+        rcx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) rcx::mbar_arrive_cluster(a1empty0 + b * 8);
+        ++lg;
+        uint32_t pk[2][8];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            pk[h][j] = rcm::gelu_half_f16x2_bf16x2(rcm::cvt_f16x2(__uint_as_float(v[h][2 * j]), __uint_as_float(v[h][2 * j + 1])));
+        const int slot = (int)(g % R);
+        rcx::mbar_wait_sleep(&freed[slot], ((g / R) & 1) ^ 1);  // both pairs are done with the slot
+        if (warp == 0) TR(1, g, 2);
+        // columns [32 ph, 32 ph + 32) of the chunk = 16-byte units 4 ph .. 4 ph + 3 of the 128-byte row
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          *reinterpret_cast<uint4 *>(r + (((4 * ph + u) ^ x) << 4)) =
+              make_uint4(pk[u >> 1][4 * (u & 1)], pk[u >> 1][4 * (u & 1) + 1], pk[u >> 1][4 * (u & 1) + 2],
+                         pk[u >> 1][4 * (u & 1) + 3]);
+      }
       rcm::fence_async_smem();
       __syncwarp();
       if (lane == 0) rcx::mbar_arrive(&own[my % R]);
@@ -400,7 +429,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
     const int nch = 13 - hh;
     auto grp = [&](int c) { return c < 8 ? 8 * hh + c : 16 + 5 * hh + (c - 8); };
     const uint32_t c2empty0 = rcx::map_cta(c2empty, lead), c2emptyB0 = rcx::map_cta(c2emptyB, lead);
-    uint8_t *stg_base = sST + w * 2 * 1024;  // two 1 KB TMA-store staging buffers per warp
+    uint8_t *stg_base = sST + w * NSTG * STGB;  // TMA-store staging: two 1 KB buffers (bf16), one 2 KB (tf32)
     uint32_t nst = 0;
     const int ntiles = cl < total ? (total - 1 - cl) / ncl + 1 : 0;
     for (int it = 0; it < ntiles; ++it) {
@@ -410,6 +439,63 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
       if (warp == 8) TR(3, it, 0);
       rcx::tc_fence_after();
       const int grow = mp * 256 + prank * 128 + q * 32;
+      if constexpr (TF) {
+        // fp32 accumulators (b2 included by the MMA): GELU and one tf32 rounding per group of 16
+        // columns straight from TMEM; piece 1 is released after its second half is loaded, piece 2
+        // as soon as it is loaded (the values wait in registers)
+        uint8_t *stg = stg_base;
+        auto gelu_store = [&](const uint32_t *v, int c) {
+          float gg[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) gg[j] = rcm::tf32_rn(rcm::gelu_erf_f32(__uint_as_float(v[j])));
+          if (lane == 0) rcm::bulk_wait_read0();  // the previous store has read the staging buffer
+          __syncwarp();
+          const int xx = (lane >> 1) & 3;  // [32 rows][64 B] staging, 64-byte TMA swizzle
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<float4 *>(stg + lane * 64 + ((u ^ xx) << 4)) =
+                make_float4(gg[4 * u], gg[4 * u + 1], gg[4 * u + 2], gg[4 * u + 3]);
+          rcm::fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            rcm::tma_store_3d(&mapOut, stg, pr * NP + grp(c) * 16, grow, net);
+            rcm::bulk_commit();
+          }
+        };
+        {
+          uint32_t v[64];
+          rcm::tmem_ld32(tmem + tq + grp(0) * 16, *reinterpret_cast<uint32_t(*)[32]>(v));
+          rcm::tmem_ld32(tmem + tq + grp(2) * 16, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+          rcx::tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) gelu_store(v + 16 * c, c);
+        }
+        {
+          uint32_t v[64];
+          rcm::tmem_ld32(tmem + tq + grp(4) * 16, *reinterpret_cast<uint32_t(*)[32]>(v));
+          rcm::tmem_ld32(tmem + tq + grp(6) * 16, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+          rcx::tmem_ld_wait();
+          rcx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) rcx::mbar_arrive_cluster(c2empty0);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) gelu_store(v + 16 * c, 4 + c);
+        }
+        {
+          uint32_t v[80];
+          rcm::tmem_ld32(tmem + tq + grp(8) * 16, *reinterpret_cast<uint32_t(*)[32]>(v));
+          rcm::tmem_ld32(tmem + tq + grp(10) * 16, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+          if (hh == 0) rcx::tmem_ld16(tmem + tq + grp(12) * 16, *reinterpret_cast<uint32_t(*)[16]>(v + 64));
+          rcx::tmem_ld_wait();
+          rcx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) rcx::mbar_arrive_cluster(c2emptyB0);
+          if (warp == 8) TR(3, it, 1);
+#pragma unroll
+          for (int c = 0; c < 5; ++c)
+            if (c < nch - 8) gelu_store(v + 16 * c, 8 + c);
+        }
+      } else {
       uint32_t pk[13][8];
       // accumulator columns (n groups from v, b2 already included) -> bf16 pairs
       auto cvt = [&](const uint32_t *v, int c, int n) {
@@ -471,6 +557,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
           ++nst;
         }
       }
+      }
       if (warp == 8) TR(3, it, 2);
     }
     if (lane == 0) rcm::bulk_wait_all();
@@ -485,24 +572,27 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
 }
 
 constexpr int L12_RING = 4;  // W2 stage / h1 slot ring depth
-// dynamic shared memory of the fused kernel; KZ = 16 keeps the W1 rows of a whole net (grows with h1)
-size_t l12_smem(int KZ, int chunks) {
-  const size_t Z_AL = ((size_t)128 * KZ * 2 + 1023) & ~(size_t)1023;
+// dynamic shared memory of the fused kernel; KZ = 16 bf16 keeps the W1 rows of a whole net (grows with h1)
+size_t l12_smem(int KZ, int chunks, bool tf) {
+  const size_t EB = tf ? 4 : 2, CW = tf ? 32 : 64;
+  const size_t Z_AL = ((size_t)128 * KZ * EB + 1023) & ~(size_t)1023;
   const size_t STAGE = ((size_t)W2T + 1023) & ~(size_t)1023;
-  const size_t w1 = KZ == 32 ? 4 * (size_t)32 * KZ * 2 : ((size_t)((chunks + 1) / 2) * 32 * KZ * 2 + 1023) & ~(size_t)1023;
-  return 1024 + L12_RING * (SLOT + STAGE) + 2 * Z_AL + w1 + (NEPI - NPROD) * 2 * 1024 + 2 * 7168 + 4096 + 1024;
+  const size_t W1_CH = CW / 2 * KZ * EB;
+  const size_t w1 = (KZ == 32 || tf) ? 4 * W1_CH : (((size_t)(chunks + 1) / 2) * W1_CH + 1023) & ~(size_t)1023;
+  const size_t stg = (NEPI - NPROD) * (tf ? 1 * 2048 : 2 * 1024);
+  return 1024 + L12_RING * (SLOT + STAGE) + 2 * Z_AL + w1 + stg + 2 * 7168 + 4096 + 1024;
 }
 constexpr size_t L12_SMEM_MAX = 232448;
 
-template <int KZ>
+template <int KZ, bool TF>
 int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
   constexpr int R = L12_RING;
-  const size_t smem = l12_smem(KZ, a.chunks);
+  const size_t smem = l12_smem(KZ, a.chunks, TF);
   if (smem > L12_SMEM_MAX) return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel: shared memory");
   a.stages = R;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(l12_kernel<KZ, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L12_SMEM_MAX);
+    cudaFuncSetAttribute(l12_kernel<KZ, R, TF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L12_SMEM_MAX);
     attr = true;
   }
   // persistent grid: only as many clusters of four as can be resident at once (a 4-CTA cluster
@@ -520,13 +610,13 @@ int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (cudaOccupancyMaxActiveClusters(&resident, l12_kernel<KZ, R>, &cfg) != cudaSuccess || resident <= 0)
+    if (cudaOccupancyMaxActiveClusters(&resident, l12_kernel<KZ, R, TF>, &cfg) != cudaSuccess || resident <= 0)
       resident = mlp_num_sms() / 4;
   }
   const int total = a.nets * (a.m_tiles / 2);
   int clusters = resident;
   if (clusters > total) clusters = total;
-  l12_kernel<KZ, R><<<4 * clusters, L12_THREADS, smem, s>>>(M[0], M[1], M[2], M[3], M[4], M[5], M[6], a);
+  l12_kernel<KZ, R, TF><<<4 * clusters, L12_THREADS, smem, s>>>(M[0], M[1], M[2], M[3], M[4], M[5], M[6], a);
   RC_LAUNCH_CHECK();
   return RC_OK;
 }
@@ -535,9 +625,12 @@ int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
 
 // decided at create / workspace-sizing time (mlp_sm100.cu fused_path), so a shape the fused kernel
 // cannot hold (e.g. KZ = 16 with h1 >= 2496: the whole-net W1 rows outgrow shared memory) takes the
-// layer-wise path from the start instead of failing after the prologue launch
-bool l12_supported(int h1, int h2, int kz) {
-  return h1 % 64 == 0 && h1 >= 128 && h2 == 2 * NP && (kz == 16 || kz == 32) && l12_smem(kz, h1 / 64) <= L12_SMEM_MAX;
+// layer-wise path from the start instead of failing after the prologue launch.  TF32: KZ = 16 only
+// (the 32-wide z rows of CH4 do not fit beside the fp32 staging: CH4 TF32 runs layer-wise).
+bool l12_supported(int h1, int h2, int kz, bool tf) {
+  const int cw = tf ? 32 : 64;
+  if (tf && kz != 16) return false;
+  return h1 % 64 == 0 && h1 >= 128 && h2 == 2 * NP && (kz == 16 || kz == 32) && l12_smem(kz, h1 / cw, tf) <= L12_SMEM_MAX;
 }
 
 #ifdef L12TRACE
@@ -546,9 +639,13 @@ extern "C" __attribute__((visibility("default"))) int rc_debug_l12trace(void *ho
 }
 #endif
 
-int launch_l12(int KZ, const CUtensorMap *maps, const L12Args &a, cudaStream_t s) {
+int launch_l12(int KZ, bool tf, const CUtensorMap *maps, const L12Args &a, cudaStream_t s) {
   ProfScope prof(RC_STAGE_L12, s);
-  if (KZ == 16) return launch_t<16>(maps, a, s);
-  if (KZ == 32) return launch_t<32>(maps, a, s);
+  if (tf) {
+    if (KZ == 16) return launch_t<16, true>(maps, a, s);
+    return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel (tf32): K = %d", KZ);
+  }
+  if (KZ == 16) return launch_t<16, false>(maps, a, s);
+  if (KZ == 32) return launch_t<32, false>(maps, a, s);
   return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel: K = %d", KZ);
 }

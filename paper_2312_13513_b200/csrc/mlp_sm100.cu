@@ -572,7 +572,8 @@ struct WsLayout {
 // cell in bf16), the activations and partial outputs for one chunk of `cap` cells
 // the fused layer-1/2 kernel runs (bf16, widths it holds, not RC_MLP_LAYERWISE): no h1 buffer
 bool fused_path(const rc_mlp *n) {
-  return n->precision == RC_BF16 && l12_supported(n->h1, n->h2, n->kpad1) && !(n->flags & RC_MLP_LAYERWISE);
+  return (n->precision == RC_BF16 || n->precision == RC_TF32) &&
+         l12_supported(n->h1, n->h2, n->kpad1, n->precision == RC_TF32) && !(n->flags & RC_MLP_LAYERWISE);
 }
 
 WsLayout ws_layout(const rc_mlp *n, int cap, int64_t ncells) {
@@ -672,6 +673,8 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
   // b2, b3 as an extra K = 16 operand of the layer-2/3 MMAs (the A side is a tile of ones):
   // column 0 = bf16(b), column 1 = bf16(b - bf16(b)), so the accumulator starts at b to ~2^-17
   std::vector<uint16_t> B2k(tf32 ? 0 : (size_t)nets * h2 * 16, 0), B3k(tf32 ? 0 : (size_t)nets * h3 * 16, 0);
+  // TF32 (fused layer-1/2 kernel): b2 as a K = 8 tf32 operand, (tf32(b), tf32(b - tf32(b)), 0...)
+  std::vector<float> B2f(tf32 && !x3 ? (size_t)nets * h2 * 8 : 0, 0.f);
   auto bias_operand = [](double b, uint16_t *row) {
     const uint16_t hi = f2bf((float)b);
     uint32_t hb = (uint32_t)hi << 16;
@@ -715,6 +718,11 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
     for (int r = 0; r < h2; ++r) {
       b2[(size_t)i * h2 + r] = (float)p[r];
       if (!tf32) bias_operand(p[r], &B2k[((size_t)i * h2 + r) * 16]);
+      if (tf32 && !x3) {
+        const float hi = f2tf32((float)p[r]);
+        B2f[((size_t)i * h2 + r) * 8] = hi;
+        B2f[((size_t)i * h2 + r) * 8 + 1] = f2tf32((float)(p[r] - (double)hi));
+      }
     }
     p += h2;
     for (size_t e = 0; e < (size_t)h3 * h2; ++e) {
@@ -754,6 +762,7 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
             up((void **)&n->d_ymean, d->y_mean, nout * 8) && up((void **)&n->d_ystd, d->y_std, nout * 8) &&
             up((void **)&n->d_species, d->species_of_net, nout * 4);
   if (ok && !tf32) ok = up(&n->d_b2k, B2k.data(), B2k.size() * 2) && up(&n->d_b3k, B3k.data(), B3k.size() * 2);
+  if (ok && tf32 && !x3) ok = up(&n->d_b2k, B2f.data(), B2f.size() * 4);
   if (ok && x3)
     ok = up(&n->d_W1lo, L1v.data(), L1v.size() * 4) && up(&n->d_W2lo, L2v.data(), L2v.size() * 4) &&
          up(&n->d_W3lo, L3v.data(), L3v.size() * 4);
@@ -862,14 +871,17 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   // fused layers 1+2 (bf16, paper widths); RC_MLP_LAYERWISE forces the layer-wise path (comparisons)
   const bool fused = fused_path(n);
   CUtensorMap m12[7];
+  // (TF32: 32-element K chunks, 16 W1 rows per CTA and chunk, b2 as a K = 8 fp32 operand)
+  const int BKK = tf32 ? 8 : 16;
   if (fused && ((rc = make_map(&m12[0], z, KZ, cap, 1, BM, KZ, EB)) ||
-                (rc = KZ == 32 ? make_map(&m12[1], n->d_W1, KZ, n->h1, nets, 32, KZ, EB)  // per-chunk W1 ring
-                               : make_map_w1_groups(&m12[1], n->d_W1, KZ, n->h1, nets)) ||
-                (rc = make_map(&m12[2], n->d_W2, n->h1, n->h2, nets, 128, 64, EB)) ||
-                (rc = make_map(&m12[3], n->d_W2, n->h1, n->h2, nets, 72, 64, EB)) ||
+                (rc = tf32 ? make_map(&m12[1], n->d_W1, KZ, n->h1, nets, 16, KZ, EB)       // per-chunk W1 ring
+                      : KZ == 32 ? make_map(&m12[1], n->d_W1, KZ, n->h1, nets, 32, KZ, EB)
+                                 : make_map_w1_groups(&m12[1], n->d_W1, KZ, n->h1, nets)) ||
+                (rc = make_map(&m12[2], n->d_W2, n->h1, n->h2, nets, 128, KC, EB)) ||
+                (rc = make_map(&m12[3], n->d_W2, n->h1, n->h2, nets, 72, KC, EB)) ||
                 (rc = make_map(&m12[4], h2, n->h2, cap, nets, 32, 16, EB)) ||
-                (rc = make_map(&m12[5], n->d_b2k, 16, n->h2, nets, 128, 16, EB)) ||
-                (rc = make_map(&m12[6], n->d_b2k, 16, n->h2, nets, 72, 16, EB))))
+                (rc = make_map(&m12[5], n->d_b2k, BKK, n->h2, nets, 128, BKK, EB)) ||
+                (rc = make_map(&m12[6], n->d_b2k, BKK, n->h2, nets, 72, BKK, EB))))
     return rc;
   if (!x3) {  // the lo slots are never read: any valid map
     for (int k = 0; k < 3; ++k) m1[3 + k] = m1[k];
@@ -914,8 +926,8 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
     }
     if (fused) {
       // layers 1+2 in one kernel: h1 stays on chip; clusters of two CTA pairs share h1 chunks
-      L12Args g12{mt, nets, n->h1 / 64, n->h2, 0, n->d_b2};
-      if ((rc = launch_l12(KZ, m12, g12, s))) return rc;
+      L12Args g12{mt, nets, n->h1 / (tf32 ? 32 : 64), n->h2, 0, n->d_b2};
+      if ((rc = launch_l12(KZ, tf32, m12, g12, s))) return rc;
     } else {
       // layer 1: h1 = GELU(z W1^T) (b1 folded into z's constant-1 columns)
       L1Args g1{mt, (n->h1 + bn1 - 1) / bn1, nets, n->h1, 0, cap};
