@@ -457,8 +457,8 @@ def run_ours(a):
                        **({"chem": "detailed kinetics, 12 reactions (NEXT-3)"} if a.chem == "kinetics" else {}),
                        **({"consumer": "Laplacian assembly of ns+1 systems (NEXT-1)"} if a.laplacian else {}),
                        **({"launch": "one CUDA graph per step"} if a.graph else {})},
-            "roofline": {"kernel": ("fused L1+L2 (z -> h1 1600 on chip -> h2 800, tcgen05 bf16, 4-CTA clusters)"
-                                    if fused else "L2 GEMM (h1 1600 -> h2 800, tcgen05)"), "bound": "tensor",
+            "roofline": {"kernel": (f"fused L1+L2 (z -> h1 1600 on chip -> h2 800, tcgen05 {a.precision}, 4-CTA clusters)"
+                                    if fused else f"L2 GEMM (h1 1600 -> h2 800, tcgen05 {a.precision})"), "bound": "tensor",
                          "achieved": l2.get("achieved"), "peak": tpeak, "unit": "TFLOP/s",
                          "frac": l2.get("frac"), "traffic": traffic,
                          "peak_source": f"{pk_src} {SUSTAINED} (MEASURED_PEAKS.json)"
