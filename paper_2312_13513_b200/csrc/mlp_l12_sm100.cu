@@ -573,21 +573,24 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
 
 constexpr int L12_RING = 4;  // W2 stage / h1 slot ring depth
 // dynamic shared memory of the fused kernel; KZ = 16 bf16 keeps the W1 rows of a whole net (grows with h1)
-size_t l12_smem(int KZ, int chunks, bool tf) {
+size_t l12_smem(int KZ, int chunks, bool tf, int R = L12_RING) {
   const size_t EB = tf ? 4 : 2, CW = tf ? 32 : 64;
   const size_t Z_AL = ((size_t)128 * KZ * EB + 1023) & ~(size_t)1023;
   const size_t STAGE = ((size_t)W2T + 1023) & ~(size_t)1023;
   const size_t W1_CH = CW / 2 * KZ * EB;
   const size_t w1 = (KZ == 32 || tf) ? 4 * W1_CH : (((size_t)(chunks + 1) / 2) * W1_CH + 1023) & ~(size_t)1023;
   const size_t stg = (NEPI - NPROD) * (tf ? 1 * 2048 : 2 * 1024);
-  return 1024 + L12_RING * (SLOT + STAGE) + 2 * Z_AL + w1 + stg + 2 * 7168 + 4096 + 1024;
+  return 1024 + R * (SLOT + STAGE) + 2 * Z_AL + w1 + stg + 2 * 7168 + 4096 + 1024;
 }
 constexpr size_t L12_SMEM_MAX = 232448;
 
+// ring depth: 4, except TF32 with the 32-wide z rows of CH4 (3: the fp32 z tiles take the room)
+template <int KZ, bool TF> constexpr int l12_ring() { return TF && KZ == 32 ? 3 : L12_RING; }
+
 template <int KZ, bool TF>
 int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
-  constexpr int R = L12_RING;
-  const size_t smem = l12_smem(KZ, a.chunks, TF);
+  constexpr int R = l12_ring<KZ, TF>();
+  const size_t smem = l12_smem(KZ, a.chunks, TF, R);
   if (smem > L12_SMEM_MAX) return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel: shared memory");
   a.stages = R;
   static bool attr = false;
@@ -625,12 +628,11 @@ int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
 
 // decided at create / workspace-sizing time (mlp_sm100.cu fused_path), so a shape the fused kernel
 // cannot hold (e.g. KZ = 16 with h1 >= 2496: the whole-net W1 rows outgrow shared memory) takes the
-// layer-wise path from the start instead of failing after the prologue launch.  TF32: KZ = 16 only
-// (the 32-wide z rows of CH4 do not fit beside the fp32 staging: CH4 TF32 runs layer-wise).
+// layer-wise path from the start instead of failing after the prologue launch.  TF32 with KZ = 32
+// (CH4) runs a 3-deep W2/A ring: its fp32 z tiles take the room of the fourth stage.
 bool l12_supported(int h1, int h2, int kz, bool tf) {
-  const int cw = tf ? 32 : 64;
-  if (tf && kz != 16) return false;
-  return h1 % 64 == 0 && h1 >= 128 && h2 == 2 * NP && (kz == 16 || kz == 32) && l12_smem(kz, h1 / cw, tf) <= L12_SMEM_MAX;
+  const int cw = tf ? 32 : 64, R = tf && kz == 32 ? 3 : L12_RING;
+  return h1 % 64 == 0 && h1 >= 128 && h2 == 2 * NP && (kz == 16 || kz == 32) && l12_smem(kz, h1 / cw, tf, R) <= L12_SMEM_MAX;
 }
 
 #ifdef L12TRACE
@@ -643,6 +645,7 @@ int launch_l12(int KZ, bool tf, const CUtensorMap *maps, const L12Args &a, cudaS
   ProfScope prof(RC_STAGE_L12, s);
   if (tf) {
     if (KZ == 16) return launch_t<16, true>(maps, a, s);
+    if (KZ == 32) return launch_t<32, true>(maps, a, s);
     return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel (tf32): K = %d", KZ);
   }
   if (KZ == 16) return launch_t<16, false>(maps, a, s);
