@@ -272,8 +272,8 @@ __device__ __forceinline__ double ipow(double a, int e) {
 // dY = Y^ ((1 + u)^n - 1) with u = lambda Delta / b (and Y* = 0, dY = -Y^ when a <= 0, i.e.
 // u <= -1), and (1 + u)^n - 1 = sum_{m=1..n} C(n, m) u^m by Horner: the relative error of dY
 // is that of u, i.e. of b, with no cancellation between Y* and Y^ (the "factorised" dY of
-// SURVEY.md §8(a) a5).  b = Y^^lambda: fp32 MUFU seed (~1e-7) + one fp64 Newton step on
-// b^n = Y^ (error x (n-1)/2 squared: ~5e-14).  Tiny Y^ (fp32 seed out of range) and a
+// SURVEY.md §8(a) a5).  1/b = Y^^(-lambda): fp32 MUFU seed (~1e-7) + one division-free fp64
+// Newton step on Y^ r^n = 1 (error x (n+1)/2 squared: ~5e-14).  Tiny Y^ (fp32 seed out of range) and a
 // non-integer or large 1/lambda take the direct pow() form.
 // the general form: Y^ = 0 (b = 0), Y^ below the fp32 seed's range, or 1/lambda not 10
 __device__ __noinline__ double inv_boxcox_dy_general(double ys, double delta, const EpiArgs &a) {
@@ -296,13 +296,15 @@ __device__ __noinline__ double inv_boxcox_dy_general(double ys, double delta, co
 // lambda_BC = 0.1 (R3, n = 10) with Y^ >= 1e-30: MUFU seed, one Newton step, 9-FMA Horner
 __device__ __forceinline__ double inv_boxcox_dy(double ys, double delta, const EpiArgs &a) {
   if (a.inv_lambda != 10 || !(ys >= 1e-30)) return inv_boxcox_dy_general(ys, delta, a);
+  // r = 1/b = Y^^(-lambda): MUFU seed, then one Newton step on Y^ r^10 = 1 (no division:
+  // r <- r + r (1 - Y^ r^10) / 10), relative error ~(11/2) 1e-14; u = lambda Delta r
   float l2, e2;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"((float)ys));
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e2) : "f"(0.1f * l2));
-  double b = (double)e2;
-  const double b2 = b * b, b4 = b2 * b2, b8 = b4 * b4;
-  b = fma(ys * rcx::rcp_f64(b8 * b) - b, 0.1, b);  // Newton on b^10 = Y^
-  const double u = (a.lambda * delta) * rcx::rcp_f64(b);
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e2) : "f"(-0.1f * l2));
+  double r = (double)e2;
+  const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+  r = fma(0.1 * r, fma(-ys, r8 * r2, 1.0), r);
+  const double u = (a.lambda * delta) * r;
   constexpr double C10[10] = {10.0, 45.0, 120.0, 210.0, 252.0, 210.0, 120.0, 45.0, 10.0, 1.0};
   double g = C10[9];
 #pragma unroll
