@@ -34,8 +34,13 @@ struct KinSeg {
   __host__ __device__ static int IW(int ns) { return W(ns) + ((ns + 1) & ~1); }
   __host__ __device__ static int REC(int ns) { return IW(ns) + ((ns + 1) & ~1); }
   __host__ __device__ static int EFF(int ns, int nr) { return REC(ns) + 48 * nr; }
-  __host__ __device__ static int size(int ns, int nr) { return (EFF(ns, nr) + nr * ((ns + 1) & ~1) + 1) & ~1; }
+  // IREC [nr][24] int32 (12 doubles per reaction): type, reversible, sum nu, then the species of the
+  // reactant / product slots and of the nonzero-nu pairs as scratch-column offsets k * KIN_TILE
+  // (-1: empty), then the pair nu
+  __host__ __device__ static int IREC(int ns, int nr) { return (EFF(ns, nr) + nr * ((ns + 1) & ~1) + 1) & ~1; }
+  __host__ __device__ static int size(int ns, int nr) { return IREC(ns, nr) + 12 * nr; }
 };
+enum { I_TYPE = 0, I_REV = 1, I_DNU = 2, I_REAC = 3, I_PROD = 6, I_PSP = 9, I_PNU = 15, I_N = 24 };
 enum {
   R_LNA = 0, R_B = 1, R_ER = 2, R_TYPE = 3, R_REV = 4, R_DNU = 5, R_REAC = 6, R_PROD = 9, R_PSP = 12, R_PNU = 18,
   R_LNA0 = 24, R_B0 = 25, R_ER0 = 26, R_TA = 27, R_IT3 = 28, R_IT1 = 29, R_T2 = 30
@@ -76,6 +81,7 @@ __global__ void __launch_bounds__(KIN_THREADS) kinetics_kernel(const double *__r
   rcx::mbar_wait(&bars[0], 0);
   const double *G = ks + KinSeg::G(ns), *TM = ks + KinSeg::TM(ns), *W = ks + KinSeg::W(ns);
   const double *IW = ks + KinSeg::IW(ns), *REC = ks + KinSeg::REC(ns), *EFF = ks + KinSeg::EFF(ns, nr);
+  const int *IREC = reinterpret_cast<const int *>(ks + KinSeg::IREC(ns, nr));
   const int nse = (ns + 1) & ~1;
   const double *hlo = sT + ThermoSeg::hlo(ns), *hhi = sT + ThermoSeg::hhi(ns);
 
@@ -103,13 +109,17 @@ __global__ void __launch_bounds__(KIN_THREADS) kinetics_kernel(const double *__r
     const double lnp0RT = log(KIN_P0 / RC_RU) - lnT;
     // net rate of progress of reaction r (reads only: two reactions are evaluated back to back so
     // their exp chains overlap; the rate updates follow)
+    // per-thread scratch columns: sC / sG / sR + q * KIN_TILE + j (q = species offset from IREC)
+    const double *cC = sC + j, *cG = sG + j;
+    double *cR = sR + j;
     auto rate = [&](int r) -> double {
       const double *R = REC + 48 * r;
-      const int type = (int)R[R_TYPE];
+      const int *I = IREC + I_N * r;
+      const int type = I[I_TYPE];
       const double lnk = R[R_LNA] + R[R_B] * lnT - R[R_ER] * invT;
       double kf = exp(lnk), M = 0.0;
       if (type >= 1)
-        for (int k = 0; k < ns; ++k) M = fma(EFF[r * nse + k], sC[k * KIN_TILE + j], M);
+        for (int k = 0; k < ns; ++k) M = fma(EFF[r * nse + k], cC[k * KIN_TILE], M);
       if (type == 2) {  // falloff: k = k_inf Pr / (1 + Pr) F
         const double Pr = exp(R[R_LNA0] + R[R_B0] * lnT - R[R_ER0] * invT - lnk) * M;
         double F = 1.0;
@@ -124,22 +134,22 @@ __global__ void __launch_bounds__(KIN_THREADS) kinetics_kernel(const double *__r
       }
       double fwd = kf, rev = 0.0;
 #pragma unroll
-      for (int s = 0; s < 3; ++s) {
-        const int q = (int)R[R_REAC + s];
-        if (q >= 0) fwd *= sC[q * KIN_TILE + j];
+      for (int q = 0; q < 3; ++q) {
+        const int o = I[I_REAC + q];
+        if (o >= 0) fwd *= cC[o];
       }
-      if (R[R_REV] != 0.0) {  // k_r = k_f / K_c, K_c = exp(-sum nu g) (p0 / (R T))^(sum nu)
+      if (I[I_REV]) {  // k_r = k_f / K_c, K_c = exp(-sum nu g) (p0 / (R T))^(sum nu)
         double sg = 0.0;
 #pragma unroll
-        for (int s = 0; s < 6; ++s) {
-          const int q = (int)R[R_PSP + s];
-          if (q >= 0) sg = fma(R[R_PNU + s], sG[q * KIN_TILE + j], sg);
+        for (int q = 0; q < 6; ++q) {
+          const int o = I[I_PSP + q];
+          if (o >= 0) sg = fma((double)I[I_PNU + q], cG[o], sg);
         }
-        rev = kf * exp(sg - R[R_DNU] * lnp0RT);
+        rev = kf * exp(sg - (double)I[I_DNU] * lnp0RT);
 #pragma unroll
-        for (int s = 0; s < 3; ++s) {
-          const int q = (int)R[R_PROD + s];
-          if (q >= 0) rev *= sC[q * KIN_TILE + j];
+        for (int q = 0; q < 3; ++q) {
+          const int o = I[I_PROD + q];
+          if (o >= 0) rev *= cC[o];
         }
       }
       if (type == 1) {
@@ -149,11 +159,11 @@ __global__ void __launch_bounds__(KIN_THREADS) kinetics_kernel(const double *__r
       return fwd - rev;
     };
     auto update = [&](int r, double qn) {
-      const double *R = REC + 48 * r;
+      const int *I = IREC + I_N * r;
 #pragma unroll
-      for (int s = 0; s < 6; ++s) {
-        const int q = (int)R[R_PSP + s];
-        if (q >= 0) sR[q * KIN_TILE + j] = fma(R[R_PNU + s], qn, sR[q * KIN_TILE + j]);
+      for (int q = 0; q < 6; ++q) {
+        const int o = I[I_PSP + q];
+        if (o >= 0) cR[o] = fma((double)I[I_PNU + q], qn, cR[o]);
       }
     };
 #pragma unroll 1
@@ -305,6 +315,18 @@ int kin_build(const rc_mech *m, const rc_kin_desc *d, rc_kin *k) {
       R[R_T2] = tr[3];
     }
     for (int sp = 0; sp < ns; ++sp) t[KinSeg::EFF(ns, nr) + r * nse + sp] = d->eff[(size_t)r * ns + sp];
+    int32_t *I = reinterpret_cast<int32_t *>(&t[KinSeg::IREC(ns, nr)]) + I_N * r;
+    I[I_TYPE] = type;
+    I[I_REV] = d->reversible[r] ? 1 : 0;
+    I[I_DNU] = dnu;
+    for (int q = 0; q < 3; ++q) {
+      I[I_REAC + q] = R[R_REAC + q] >= 0 ? (int)R[R_REAC + q] * KIN_TILE : -1;
+      I[I_PROD + q] = R[R_PROD + q] >= 0 ? (int)R[R_PROD + q] * KIN_TILE : -1;
+    }
+    for (int q = 0; q < 6; ++q) {
+      I[I_PSP + q] = R[R_PSP + q] >= 0 ? (int)R[R_PSP + q] * KIN_TILE : -1;
+      I[I_PNU + q] = (int)R[R_PNU + q];
+    }
   }
   k->nr = nr;
   k->ns = ns;
