@@ -66,3 +66,23 @@ def test_no_cpu_fallback_without_library(tmp_path, monkeypatch, rclib):
     monkeypatch.setattr(rclib, "_lib", None)
     with pytest.raises(ImportError):
         rclib.lib()
+
+
+def test_next_row_entry_points_reject_bad_arguments_before_any_cuda_call(rclib):
+    """NEXT-row calls validate on the host and return a status without touching the device (so these
+    run on a CPU box): NULL handles, missing arrays, a mesh the CSR conversion cannot hold."""
+    import ctypes as C
+    L = rclib.lib()
+    cells = rclib.rc_cells()
+    mesh = rclib.rc_mesh(2, 3, 4, 1e-3, 1e-3, 1e-3)
+    # rc_kinetics / rc_laplacian / rc_pack_planes with a NULL mechanism
+    assert L.rc_kinetics(None, None, C.byref(cells), None) == rclib.RC_EINVAL
+    assert L.rc_laplacian(None, C.byref(mesh), C.byref(cells), None, None, None, None, 0, None) == rclib.RC_EINVAL
+    assert L.rc_pack_planes(None, C.byref(mesh), C.byref(cells), None, None, None) == rclib.RC_EINVAL
+    # CSR needs nx, ny, nz >= 3 (7 distinct columns per row)
+    assert L.rc_ldu_to_csr(C.byref(mesh), 1, None, None, None, None, None, None) == rclib.RC_EUNSUPPORTED
+    big = rclib.rc_mesh(4, 4, 4, 1e-3, 1e-3, -1.0)
+    assert L.rc_ldu_to_csr(C.byref(big), 1, None, None, None, None, None, None) == rclib.RC_EINVAL
+    # rc_kin_create with a NULL description
+    h = C.c_void_p()
+    assert L.rc_kin_create(None, None, C.byref(h)) == rclib.RC_EINVAL

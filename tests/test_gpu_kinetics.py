@@ -79,3 +79,26 @@ def test_c2_sample_ragged_and_pasr():
         g, _ = _run(c, c["T_true"], tau=tau, ld=1040)
         e, _ = _check(g, o, m)
         print(f"\n  kinetics C2 sample (PaSR {tau is not None}): max error / gross rate {e:.2e}")
+
+
+def test_kinetics_argument_errors():
+    import paper_2312_13513_b200 as rc
+    from workload import load_mech
+    M = rc.Mechanism(mech("h2_9sp"))
+    K = rc.Kinetics(M, load_kinetics("h2_9sp"))
+    st = rc.CellState(64, 9, 0)                          # no wdot allocated
+    with pytest.raises(rc.RcError) as e:
+        rc.rc_kinetics(M, K, st.cells(rc.RC_MODE_T, chem=False))
+    assert e.value.code == rc._rc.RC_EINVAL
+    # a mechanism of another size
+    M20 = rc.Mechanism(load_mech("ch4_20sp"))
+    st20 = rc.CellState(64, 20, 0, sources=True)
+    with pytest.raises(rc.RcError):
+        rc.rc_kinetics(M20, K, st20.cells(rc.RC_MODE_T))
+    # a reaction with four reactant molecules is refused at create
+    k = load_kinetics("h2_9sp")
+    k["nu_f"] = k["nu_f"].copy()
+    k["nu_f"][0, 3] = 4
+    with pytest.raises(rc.RcError) as e:
+        rc.Kinetics(M, k)
+    assert e.value.code == rc._rc.RC_EUNSUPPORTED

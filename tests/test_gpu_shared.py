@@ -69,3 +69,12 @@ def test_ch4_shared_net_19_outputs():
     eo, ew = rel_fro(g["o"], o["o"]), rel_fro(g["wdot"], o["wdot"])
     print(f"\n  shared net CH4: o {eo:.2e} wdot {ew:.2e}")
     assert eo <= BF16_TOL and ew <= BF16_DERIVED_TOL
+
+
+def test_shared_flag_rejects_tf32x3():
+    import paper_2312_13513_b200 as rc
+    M = rc.Mechanism(mech("h2_9sp"))
+    b = make_bundle("h2_9sp", hidden=(64, 32, 16), shared=True)
+    with pytest.raises(rc.RcError) as e:
+        rc.MLPBundle(M, b, rc.RC_TF32X3)
+    assert e.value.code == rc._rc.RC_EUNSUPPORTED
