@@ -266,19 +266,21 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[a.config]
+    # this rank's cells, generated on the host BEFORE any CUDA context or NCCL communicator exists
+    # (generate() forks worker processes for large blocks)
+    idx, n_global = local_cells(cfg, rank, world, a.strong)
+    n = idx.size
+    host = generate(cfg, idx, world)
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = CONFIGS[a.config]
     mech_d = load_mech(cfg.mech)
     bundle = make_bundle(cfg.mech, hidden=cfg.hidden, shared=a.shared)
     mech = rc.Mechanism(mech_d)
     prec = {"bf16": rc.RC_BF16, "tf32": rc.RC_TF32, "tf32x3": rc.RC_TF32X3}[a.precision]
     mlp = rc.MLPBundle(mech, bundle, prec, flags=rc._rc.RC_MLP_LAYERWISE if a.layerwise else 0)
     ns, nets = mech_d["ns"], bundle["n_nets"]
-    idx, n_global = local_cells(cfg, rank, world, a.strong)
-    n = idx.size
-    host = generate(cfg, idx, world)
     st = rc.CellState(n, ns, nets, outputs=("cp", "rho", "mu", "lam", "D", "wdot", "qdot"))
     st.load(host["T_true"], host["p"], host["Y"])
     if a.pasr:

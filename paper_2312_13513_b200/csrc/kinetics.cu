@@ -12,6 +12,7 @@
 // per-CTA shared-memory scratch ([ns][TILE], conflict-free), and reads the reaction records as
 // broadcasts.
 #include <cmath>
+#include <cstring>
 
 #include "ptx.cuh"
 #include "rc_internal.h"
@@ -315,7 +316,7 @@ int kin_build(const rc_mech *m, const rc_kin_desc *d, rc_kin *k) {
       R[R_T2] = tr[3];
     }
     for (int sp = 0; sp < ns; ++sp) t[KinSeg::EFF(ns, nr) + r * nse + sp] = d->eff[(size_t)r * ns + sp];
-    int32_t *I = reinterpret_cast<int32_t *>(&t[KinSeg::IREC(ns, nr)]) + I_N * r;
+    int32_t I[I_N] = {0};  // copied into the table's bytes below (the table is one device buffer)
     I[I_TYPE] = type;
     I[I_REV] = d->reversible[r] ? 1 : 0;
     I[I_DNU] = dnu;
@@ -327,6 +328,7 @@ int kin_build(const rc_mech *m, const rc_kin_desc *d, rc_kin *k) {
       I[I_PSP + q] = R[R_PSP + q] >= 0 ? (int)R[R_PSP + q] * KIN_TILE : -1;
       I[I_PNU + q] = (int)R[R_PNU + q];
     }
+    std::memcpy(reinterpret_cast<char *>(t.data() + KinSeg::IREC(ns, nr)) + sizeof(I) * r, I, sizeof(I));
   }
   k->nr = nr;
   k->ns = ns;
