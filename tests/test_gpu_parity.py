@@ -322,13 +322,18 @@ def test_out_of_range_h_bisects_like_oracle():
     assert max_rel(g["T"], o["T"]) <= FP64_TOL
 
 
-def test_sharded_equals_unsharded_bitwise():
+@pytest.mark.parametrize("prec", [0, 1])
+def test_sharded_equals_unsharded_bitwise(prec):
     """Cells are independent: running G shards (rc_partition) one after another
-    reproduces the unsharded per-cell outputs bit for bit."""
+    reproduces the unsharded per-cell outputs bit for bit, for the fused
+    bf16 and TF32 kernels alike; a repeated run is bitwise identical (deterministic)."""
     import paper_2312_13513_b200 as rc
     c = inputs("C2", begin=300000, end=300000 + 5000)
-    G = Gpu("C2")
+    G = Gpu("C2", precision=prec)
     whole = G.run(c)
+    again = G.run(c)
+    for k in ("T", "cp", "rho", "mu", "lambda", "qdot", "D", "wdot", "o", "red", "diag"):
+        assert np.array_equal(again[k], whole[k]), k
     for world in (2, 3):
         for r in range(world):
             b, e = rc.rc_partition(5000, r, world)
