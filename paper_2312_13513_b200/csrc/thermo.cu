@@ -12,6 +12,8 @@
 // mixture are formed once per range (12 ns DFMA), so each Newton iteration is
 // two Horner polynomials and a reciprocal instead of a loop over species
 // ("computation consolidation").
+#include <type_traits>
+
 #include "ptx.cuh"
 #include "rc_internal.h"
 #include "stream.cuh"
@@ -22,6 +24,12 @@ namespace {
 __device__ __forceinline__ double2 lds_f64x2(const double *p) {
   double2 v;
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(rcx::smem_u32(p)));
+  return v;
+}
+
+__device__ __forceinline__ double lds_f64(const double *p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(rcx::smem_u32(p)));
   return v;
 }
 
@@ -69,6 +77,7 @@ __global__ void __launch_bounds__(THERMO_THREADS, 3) thermo_kernel(const double 
   const double *invW = s_tab + ThermoSeg::invW(ns), *tmid = s_tab + ThermoSeg::tmid(ns);
   constexpr int CAP = NS ? NS : RC_MAX_NS;
   constexpr int UR = NS ? NS : 1;
+  constexpr int UR1 = NS ? (NS > 10 ? 5 : NS) : 1;  // the mixture pass: a partial unroll for Ns = 20 (no spill)
 
   int n_bisect = 0, n_maxit = 0, n_neg = 0, n_bad = 0;
   double Tloc_max = 0.0;
@@ -79,39 +88,109 @@ __global__ void __launch_bounds__(THERMO_THREADS, 3) thermo_kernel(const double 
     // mixture NASA coefficients per range and 1/W = sum Y_k / W_k.  The table is read with
     // volatile shared loads next to their use: a fully unrolled loop would otherwise hoist the
     // whole coefficient table into registers.
-    double Y[CAP];
     bool neg = false;
-#pragma unroll UR
-    for (int k = 0; k < CAP; ++k)
-      if (k < ns) {
-        Y[k] = S8[(2 + k) * THERMO_TILE];
-        neg |= Y[k] < 0.0;
-      }
-    double Hl[6] = {0, 0, 0, 0, 0, 0}, Hh[6] = {0, 0, 0, 0, 0, 0}, sW = 0.0;
-#pragma unroll UR
-    for (int k = 0; k < CAP; ++k)
-      if (k < ns) {
-#pragma unroll
-        for (int q = 0; q < 6; q += 2) {
-          const double2 lo = lds_f64x2(hlo + 6 * k + q), hi = lds_f64x2(hhi + 6 * k + q);
-          Hl[q] = fma(Y[k], lo.x, Hl[q]);
-          Hl[q + 1] = fma(Y[k], lo.y, Hl[q + 1]);
-          Hh[q] = fma(Y[k], hi.x, Hh[q]);
-          Hh[q + 1] = fma(Y[k], hi.y, Hh[q + 1]);
-        }
-        sW = fma(Y[k], invW[k], sW);
-      }
     const double p = S8[THERMO_TILE];
-    auto eval = [&](double T, double &h, double &cp) {
-      if constexpr (UNIFORM) {
-        const bool lo = T <= Tmid;
-        double a0 = lo ? Hl[0] : Hh[0], a1 = lo ? Hl[1] : Hh[1], a2 = lo ? Hl[2] : Hh[2];
-        double a3 = lo ? Hl[3] : Hh[3], a4 = lo ? Hl[4] : Hh[4], a5 = lo ? Hl[5] : Hh[5];
+    double T = S8[0], hT, cpT;
+    double rho;
+    if constexpr (UNIFORM) {
+      // One T_mid for every species: the mixture polynomial of ONE range, a[6] = sum_k Y_k a_k,
+      // formed for the range T lies in and re-formed only when an iterate crosses T_mid (a cell
+      // rarely does): 6 ns instead of 12 ns DFMA and no per-evaluation range selects.
+      double sW = 0.0, a[6];
+      bool lo_rng = false;
+      auto mix = [&](bool lo, auto unroll) {
+        const double *tb = lo ? hlo : hhi;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) a[q] = 0.0;
+        auto term = [&](int k) {
+          const double yk = lds_f64(S8 + (2 + k) * THERMO_TILE);  // re-read: no Ns registers held
+#pragma unroll
+          for (int q = 0; q < 6; q += 2) {
+            const double2 v = lds_f64x2(tb + 6 * k + q);
+            a[q] = fma(yk, v.x, a[q]);
+            a[q + 1] = fma(yk, v.y, a[q + 1]);
+          }
+          return yk;
+        };
+        if constexpr (decltype(unroll)::value) {  // first pass: also 1/W and the negative-Y count
+#pragma unroll UR1
+          for (int k = 0; k < CAP; ++k)
+            if (k < ns) {
+              const double yk = term(k);
+              neg |= yk < 0.0;
+              sW = fma(yk, invW[k], sW);
+            }
+        } else {  // an iterate crossed T_mid: rare, kept small
+#pragma unroll 1
+          for (int k = 0; k < ns; ++k) term(k);
+        }
+        lo_rng = lo;
+      };
+      auto eval = [&](double T, double &h, double &cp) {
+        if ((T <= Tmid) != lo_rng) mix(T <= Tmid, std::false_type{});
         // Estrin form (dependency depth 3 instead of 5: the Newton iteration is a latency chain)
         const double T2 = T * T;
-        h = fma(T2 * T2, fma(T, a4, a3), fma(T2, fma(T, a2, a1), fma(T, a0, a5)));
-        cp = fma(T2 * T2, 5.0 * a4, fma(T2, fma(T, 4.0 * a3, 3.0 * a2), fma(T, 2.0 * a1, a0)));
-      } else {  // per-species ranges (T_mid differs between species)
+        h = fma(T2 * T2, fma(T, a[4], a[3]), fma(T2, fma(T, a[2], a[1]), fma(T, a[0], a[5])));
+        cp = fma(T2 * T2, 5.0 * a[4], fma(T2, fma(T, 4.0 * a[3], 3.0 * a[2]), fma(T, 2.0 * a[1], a[0])));
+      };
+      if (hmode) {
+        const double hs = S8[(2 + ns) * THERMO_TILE];
+        T = fmin(fmax(T, Tmin), Tmax);
+        mix(T <= Tmid, std::true_type{});
+        int clamp_hits = 0;
+        bool done = false, fresh = false;
+#pragma unroll 1
+        for (int it = 1; it <= 50; ++it) {
+          eval(T, hT, cpT);
+          double Tn = T + (hs - hT) * rcx::rcp_f64_fast(cpT);
+          bool clamped = false;
+          if (Tn < Tmin) { Tn = Tmin; clamped = true; }
+          if (Tn > Tmax) { Tn = Tmax; clamped = true; }
+          clamp_hits = clamped ? clamp_hits + 1 : 0;
+          if (clamp_hits >= 2) break;
+          if (!clamped && fabs(Tn - T) <= 1e-10 * Tn) {
+            // cp(T) stands for cp(Tn) when the last step is below 1e-13 T (relative change of cp
+            // <= (T cp'/cp) 1e-13 < 1e-13; DESIGN.md §6 thermo): the usual case, quadratic convergence
+            fresh = fabs(Tn - T) <= 1e-13 * Tn && (Tn <= Tmid) == (T <= Tmid);
+            T = Tn;
+            done = true;
+            break;
+          }
+          T = Tn;
+          if (it == 50) ++n_maxit;
+        }
+        if (!done) {  // bisection on [Tmin, Tmax]; h increasing since cp > 0
+          ++n_bisect;
+          double lo = Tmin, hi = Tmax;
+#pragma unroll 1
+          while (hi - lo > 1e-10 * (0.5 * (lo + hi))) {
+            double mid = 0.5 * (lo + hi), hm, cm;
+            eval(mid, hm, cm);
+            if (hm < hs) lo = mid; else hi = mid;
+          }
+          T = 0.5 * (lo + hi);
+        }
+        c.T[i] = T;
+        if (!fresh) eval(T, hT, cpT);
+      } else {
+        mix(T <= Tmid, std::true_type{});
+        eval(T, hT, cpT);
+        if (c.h) c.h[i] = hT;
+      }
+      rho = p * rcx::rcp_f64_fast(RC_RU * T * sW);
+    } else {  // per-species ranges (T_mid differs between species)
+      double Y[CAP];
+#pragma unroll UR
+      for (int k = 0; k < CAP; ++k)
+        if (k < ns) {
+          Y[k] = S8[(2 + k) * THERMO_TILE];
+          neg |= Y[k] < 0.0;
+        }
+      double sW = 0.0;
+#pragma unroll UR
+      for (int k = 0; k < CAP; ++k)
+        if (k < ns) sW = fma(Y[k], invW[k], sW);
+      auto eval = [&](double T, double &h, double &cp) {
         h = 0.0;
         cp = 0.0;
 #pragma unroll UR
@@ -123,43 +202,42 @@ __global__ void __launch_bounds__(THERMO_THREADS, 3) thermo_kernel(const double 
             h = fma(Y[k], hk, h);
             cp = fma(Y[k], ck, cp);
           }
-      }
-    };
-    double T = S8[0], hT, cpT;
-    if (hmode) {
-      const double hs = S8[(2 + ns) * THERMO_TILE];
-      T = fmin(fmax(T, Tmin), Tmax);
-      int clamp_hits = 0;
-      bool done = false;
+      };
+      if (hmode) {
+        const double hs = S8[(2 + ns) * THERMO_TILE];
+        T = fmin(fmax(T, Tmin), Tmax);
+        int clamp_hits = 0;
+        bool done = false;
 #pragma unroll 1
-      for (int it = 1; it <= 50; ++it) {
-        eval(T, hT, cpT);
-        double Tn = T + (hs - hT) * rcx::rcp_f64_fast(cpT);
-        bool clamped = false;
-        if (Tn < Tmin) { Tn = Tmin; clamped = true; }
-        if (Tn > Tmax) { Tn = Tmax; clamped = true; }
-        clamp_hits = clamped ? clamp_hits + 1 : 0;
-        if (clamp_hits >= 2) break;
-        if (!clamped && fabs(Tn - T) <= 1e-10 * Tn) { T = Tn; done = true; break; }
-        T = Tn;
-        if (it == 50) ++n_maxit;
-      }
-      if (!done) {  // bisection on [Tmin, Tmax]; h increasing since cp > 0
-        ++n_bisect;
-        double lo = Tmin, hi = Tmax;
-#pragma unroll 1
-        while (hi - lo > 1e-10 * (0.5 * (lo + hi))) {
-          double mid = 0.5 * (lo + hi), hm, cm;
-          eval(mid, hm, cm);
-          if (hm < hs) lo = mid; else hi = mid;
+        for (int it = 1; it <= 50; ++it) {
+          eval(T, hT, cpT);
+          double Tn = T + (hs - hT) * rcx::rcp_f64_fast(cpT);
+          bool clamped = false;
+          if (Tn < Tmin) { Tn = Tmin; clamped = true; }
+          if (Tn > Tmax) { Tn = Tmax; clamped = true; }
+          clamp_hits = clamped ? clamp_hits + 1 : 0;
+          if (clamp_hits >= 2) break;
+          if (!clamped && fabs(Tn - T) <= 1e-10 * Tn) { T = Tn; done = true; break; }
+          T = Tn;
+          if (it == 50) ++n_maxit;
         }
-        T = 0.5 * (lo + hi);
+        if (!done) {
+          ++n_bisect;
+          double lo = Tmin, hi = Tmax;
+#pragma unroll 1
+          while (hi - lo > 1e-10 * (0.5 * (lo + hi))) {
+            double mid = 0.5 * (lo + hi), hm, cm;
+            eval(mid, hm, cm);
+            if (hm < hs) lo = mid; else hi = mid;
+          }
+          T = 0.5 * (lo + hi);
+        }
+        c.T[i] = T;
       }
-      c.T[i] = T;
+      eval(T, hT, cpT);
+      if (!hmode && c.h) c.h[i] = hT;
+      rho = p / (RC_RU * T * sW);
     }
-    eval(T, hT, cpT);
-    if (!hmode && c.h) c.h[i] = hT;
-    const double rho = p / (RC_RU * T * sW);
     if (c.cp) c.cp[i] = cpT;
     if (c.rho) c.rho[i] = rho;
     n_neg += neg;
