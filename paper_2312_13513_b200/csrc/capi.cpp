@@ -239,6 +239,20 @@ extern "C" int rc_mech_create(const rc_mech_desc *d, rc_mech **out) {
         for (int b = 0; b < ne; ++b) s += E[a * ns + k] * G[a * ne + b] * E[b * ns + j];
       m->P[k * ns + j] = (k == j ? 1.0 : 0.0) - s;
     }
+  // the same projection in factored form for the chemistry epilogue: F = G E, P = I - E^T F
+  std::vector<double> EF(2 * ne * ns, 0.0);
+  for (int a = 0; a < ne; ++a)
+    for (int k = 0; k < ns; ++k) {
+      double f = 0.0;
+      for (int b = 0; b < ne; ++b) f += G[a * ne + b] * E[b * ns + k];
+      EF[a * ns + k] = f;
+      EF[(ne + a) * ns + k] = E[a * ns + k];
+    }
+  if (cudaMalloc(&m->d_EF, EF.size() * 8) != cudaSuccess ||
+      cudaMemcpy(m->d_EF, EF.data(), EF.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+    rc_mech_destroy(m);
+    return rc_fail(RC_ENOMEM, "rc_mech_create: cudaMalloc failed");
+  }
   if (cudaMalloc(&m->d_thermo, th.size() * 8) != cudaSuccess ||
       cudaMalloc(&m->d_transport, tr.size() * 8) != cudaSuccess ||
       cudaMalloc(&m->d_P, (size_t)((ns * ns + 1) & ~1) * 8) != cudaSuccess ||  // padded: 16-byte bulk copies
@@ -261,6 +275,7 @@ extern "C" void rc_mech_destroy(rc_mech *m) {
   cudaFree(m->d_thermo);
   cudaFree(m->d_transport);
   cudaFree(m->d_P);
+  cudaFree(m->d_EF);
   delete m;
 }
 
@@ -311,6 +326,8 @@ extern "C" int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *d, rc_mlp **ou
   n->dt = d->dt;
   n->kpad1 = d_in + 2 <= 16 ? 16 : 32;  // z row: d_in inputs, two constant-1 bias columns, zero padding
   n->species_of_net.assign(d->species_of_net, d->species_of_net + d->n_nets);
+  n->species_identity = true;
+  for (int i = 0; i < d->n_nets; ++i) n->species_identity &= d->species_of_net[i] == i;
   cudaGetDevice(&n->device);
   int rc = mlp_upload(n, d);
   if (rc != RC_OK) { rc_mlp_destroy(n); return rc; }

@@ -53,8 +53,10 @@ struct ProArgs {
   int64_t lo_off;   // elements
 };
 
-constexpr int PRO_TILE = 256;                 // cells per stage = consumer threads
-constexpr int PRO_THREADS = PRO_TILE + 32;    // + the producer warp (stream.cuh run_ws)
+// cells per stage = consumer threads (+ the producer warp, stream.cuh run_ws).  256-cell tiles for
+// the H2 set (3 CTAs/SM with 3 stages); 128 for larger mechanisms, where a 256-cell stage of 2 + Ns
+// fp64 rows (45 KB at Ns = 20) would leave one CTA (8 consumer warps) per SM
+template <int TILE> constexpr int pro_threads() { return TILE + 32; }
 
 // one z row (d_in transformed inputs, two 1.0 bias columns, zeros) -> bf16 or tf32 (hi[, lo])
 __device__ __forceinline__ void store_z_row(const ProArgs &a, int64_t r, const float (&x)[32]) {
@@ -89,11 +91,18 @@ __device__ __forceinline__ void store_z_row(const ProArgs &a, int64_t r, const f
 
 // a3 for every cell of the call: T, p, Y streamed through the TMA tile ring (stream.cuh), one
 // thread per cell writes its z row; rows [rows, rows_pad) of the 256-row tiles are zero
-__global__ void __launch_bounds__(PRO_THREADS) prologue_kernel(ProArgs a, CellsDev c, int stages) {
+template <int PRO_TILE>
+__global__ void __launch_bounds__(pro_threads<PRO_TILE>()) prologue_kernel(ProArgs a, CellsDev c, int stages) {
+  constexpr int PRO_THREADS = pro_threads<PRO_TILE>();
   extern __shared__ __align__(16) uint8_t pro_smem[];
   __shared__ __align__(8) uint64_t bars[16];
+  __shared__ float s_xm[32], s_xs[32];  // z-score constants (d_in <= 30)
   const rcs::Ring<PRO_TILE> ring{pro_smem, bars, 2 + a.ns, 0, stages};
   if (threadIdx.x == 0) ring.init(PRO_TILE / 32);
+  if (threadIdx.x < 32) {
+    s_xm[threadIdx.x] = threadIdx.x < a.d_in ? a.xmean[threadIdx.x] : 0.f;
+    s_xs[threadIdx.x] = threadIdx.x < a.d_in ? a.xinvstd[threadIdx.x] : 0.f;
+  }
   __syncthreads();
   auto src8 = [&](int r) -> const double * {
     return (r == 0 ? c.T : r == 1 ? c.p : c.Y + (size_t)(r - 2) * c.ld) + a.c0;
@@ -106,8 +115,8 @@ __global__ void __launch_bounds__(PRO_THREADS) prologue_kernel(ProArgs a, CellsD
     float x[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = 0.f;
-    x[0] = ((float)S8[0] - a.xmean[0]) * a.xinvstd[0];
-    x[1] = ((float)S8[PRO_TILE] - a.xmean[1]) * a.xinvstd[1];
+    x[0] = ((float)S8[0] - s_xm[0]) * s_xs[0];
+    x[1] = ((float)S8[PRO_TILE] - s_xm[1]) * s_xs[1];
 #pragma unroll
     for (int k = 0; k < 30; ++k)
       if (k < a.ns) {
@@ -121,7 +130,7 @@ __global__ void __launch_bounds__(PRO_THREADS) prologue_kernel(ProArgs a, CellsD
           asm("ex2.approx.f32 %0, %1;" : "=f"(e2) : "f"(a.lambda * l2));
           b = e2;
         }
-        x[2 + k] = ((b - 1.f) * a.inv_lambda - a.xmean[2 + k]) * a.xinvstd[2 + k];  // Box-Cox, z-score
+        x[2 + k] = ((b - 1.f) * a.inv_lambda - s_xm[2 + k]) * s_xs[2 + k];  // Box-Cox, z-score
       }
 #pragma unroll
     for (int j = 0; j < 32; ++j)
@@ -253,6 +262,8 @@ struct EpiArgs {
   const float *opart, *b4;     // raw net outputs [nets][passes][cap] (column quarters summed by layer 3)
   const double *ymean, *ystd, *P, *thermo;
   const int *species;
+  const double *EF;  // [2][ne][ns]: F = (E E^T)^-1 E, then E (the factored P = I - E^T F)
+  int ne;
   double *qpart;  // [gridDim.x], accumulated across chunks in stream order
   double binom[17];  // C(n, m), m = 0..n, n = inv_lambda <= 16 (factorised inverse Box-Cox)
 };
@@ -322,7 +333,11 @@ __device__ __forceinline__ double2 lds2_epi(const double *p) {
 // eight consumer warps per SM) unless the Ns = 20 register/shared footprint needs 128
 template <int NS> constexpr int epi_tile() { return NS == 20 ? 128 : 256; }
 
-template <int NS>
+// NE > 0: net `net` predicts species `net` (the usual layout: the inert species last) and the mechanism
+// has NE elements; the projection is then applied in factored form, v = dY - E^T (F dY), with F dY
+// accumulated per net (NE FMAs instead of Ns) and dY kept in registers (the net loop is fully
+// unrolled, so dY_net has a static register).  NE == 0: the outer product with the columns of P.
+template <int NS, int NE>
 __global__ void __launch_bounds__(epi_tile<NS>() + 32, NS == 0 ? 1 : 2) chem_epilogue_kernel(EpiArgs a, CellsDev c, int stages) {
   constexpr int EPI_TILE = epi_tile<NS>(), EPI_THREADS = EPI_TILE + 32;
   constexpr int CAP = NS ? NS : RC_MAX_NS;
@@ -335,10 +350,13 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, NS == 0 ? 1 : 2) chem_epi
   __shared__ double red_s[EPI_THREADS / 32];
   const int nse = (ns + 1) & ~1;
   // P columns by net [nn][nse] | species [32 ints] | b4, y_mean, y_std [nn] each (no global loads per cell)
-  const int tsz = ThermoSeg::size(ns), psz = (ns * ns + 1) & ~1, pnsz = nn * nse + 16 + ((3 * nn + 1) & ~1);
+  // NE > 0: [nn][NE] F columns by net, then [ns][NE] E columns, in the Pn slot
+  const int tsz = ThermoSeg::size(ns), psz = (ns * ns + 1) & ~1,
+            pnsz = (NE ? ((nn + ns) * NE + 1) & ~1 : nn * nse) + 16 + ((3 * nn + 1) & ~1);
   double *sP = s_tab + tsz, *sPn = sP + psz;
-  int *sSpec = reinterpret_cast<int *>(sPn + nn * nse);
-  double *sB4 = sPn + nn * nse + 16, *sYM = sB4 + nn, *sYS = sYM + nn;
+  const int pnt = NE ? ((nn + ns) * NE + 1) & ~1 : nn * nse;
+  int *sSpec = reinterpret_cast<int *>(sPn + pnt);
+  double *sB4 = sPn + pnt + 16, *sYM = sB4 + nn, *sYS = sYM + nn;
   const rcs::Ring<EPI_TILE> ring{reinterpret_cast<uint8_t *>(sPn + pnsz), bars + 1, 2 + ns, nn * a.passes, stages};
   if (threadIdx.x == 0) {
     rcx::mbar_init(&bars[0], 1);
@@ -360,9 +378,16 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, NS == 0 ? 1 : 2) chem_epi
   const double *invW = s_tab + ThermoSeg::invW(ns);
   // the columns of P gathered by net and stored contiguously: Pn[net][k] = P[k][species[net]]
   // (the other columns multiply dY = 0), padded to an even length for 16-byte loads
-  for (int e = threadIdx.x; e < nn * nse; e += blockDim.x) {
-    const int net = e / nse, k = e % nse;
-    sPn[e] = k < ns ? sP[k * ns + a.species[net]] : 0.0;
+  if constexpr (NE > 0) {
+    for (int e = threadIdx.x; e < (nn + ns) * NE; e += blockDim.x) {
+      const int r = e / NE, q = e % NE;  // r < nn: F column of net r's species (= r); else E column r - nn
+      sPn[e] = r < nn ? a.EF[q * ns + r] : a.EF[(NE + q) * ns + (r - nn)];
+    }
+  } else {
+    for (int e = threadIdx.x; e < nn * nse; e += blockDim.x) {
+      const int net = e / nse, k = e % nse;
+      sPn[e] = k < ns ? sP[k * ns + a.species[net]] : 0.0;
+    }
   }
   for (int e = threadIdx.x; e < nn; e += blockDim.x) {
     sSpec[e] = a.species[e];
@@ -384,25 +409,55 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, NS == 0 ? 1 : 2) chem_epi
     // net loop: dY of net's species (inverse Box-Cox), accumulated straight into the projection
     // v = P dY as an outer product with column `species[net]` of P (species without a net
     // contribute 0); the loop stays rolled for large mechanisms (instruction-cache footprint)
-    double v[CAP];
-#pragma unroll UR
-    for (int k = 0; k < CAP; ++k)
-      if (k < ns) v[k] = 0.0;
-#pragma unroll NETUNR
-    for (int net = 0; net < nn; ++net) {
-      float o = (float)sB4[net];
-      for (int ps = 0; ps < a.passes; ++ps) o += S4[(net * a.passes + ps) * EPI_TILE];
+    auto net_out = [&](int net) {  // raw output o of the net (layer 3's passes summed), b4 added
+      float o = (float)sB4[net] + S4[net * a.passes * EPI_TILE];
+#pragma unroll 1
+      for (int ps = 1; ps < a.passes; ++ps) o += S4[(net * a.passes + ps) * EPI_TILE];
       if (c.o) c.o[net * c.ld + i] = o;
-      const double y = S8[(2 + sSpec[net]) * EPI_TILE];
-      const double dy = inv_boxcox_dy(y > 0.0 ? y : 0.0, (double)o * sYS[net] + sYM[net], a);
-      const double *pc = sPn + net * nse;  // column species[net] of P, contiguous in k
-#pragma unroll UR
-      for (int k = 0; k < CAP; k += 2)
-        if (k < ns) {
-          const double2 pp = lds2_epi(pc + k);
-          v[k] = fma(pp.x, dy, v[k]);
-          if (k + 1 < ns) v[k + 1] = fma(pp.y, dy, v[k + 1]);
+      return o;
+    };
+    double v[CAP];
+    if constexpr (NE > 0) {
+      double w[NE];
+#pragma unroll
+      for (int e = 0; e < NE; ++e) w[e] = 0.0;
+#pragma unroll
+      for (int net = 0; net < CAP; ++net) {
+        v[net] = 0.0;
+        if (net < nn) {
+          const float o = net_out(net);
+          const double y = S8[(2 + net) * EPI_TILE];
+          const double dy = inv_boxcox_dy(y > 0.0 ? y : 0.0, (double)o * sYS[net] + sYM[net], a);
+          v[net] = dy;
+#pragma unroll
+          for (int e = 0; e < NE; ++e) w[e] = fma(sPn[net * NE + e], dy, w[e]);  // F dY
         }
+      }
+#pragma unroll
+      for (int k = 0; k < CAP; ++k) {  // v = dY - E^T (F dY)
+        double t = 0.0;
+#pragma unroll
+        for (int e = 0; e < NE; ++e) t = fma(sPn[(nn + k) * NE + e], w[e], t);
+        v[k] -= t;
+      }
+    } else {
+#pragma unroll UR
+      for (int k = 0; k < CAP; ++k)
+        if (k < ns) v[k] = 0.0;
+#pragma unroll NETUNR
+      for (int net = 0; net < nn; ++net) {
+        const float o = net_out(net);
+        const double y = S8[(2 + sSpec[net]) * EPI_TILE];
+        const double dy = inv_boxcox_dy(y > 0.0 ? y : 0.0, (double)o * sYS[net] + sYM[net], a);
+        const double *pc = sPn + net * nse;  // column species[net] of P, contiguous in k
+#pragma unroll UR
+        for (int k = 0; k < CAP; k += 2)
+          if (k < ns) {
+            const double2 pp = lds2_epi(pc + k);
+            v[k] = fma(pp.x, dy, v[k]);
+            if (k + 1 < ns) v[k + 1] = fma(pp.y, dy, v[k + 1]);
+          }
+      }
     }
     // sources; LES: PaSR factor kappa = tau_c / (tau_c + tau_mix) = 1 / (1 + tau_mix / tau_c) with
     // 1 / tau_c = (1/2 sum_k |wdot_k| / W_k) / sum_k C+_k (rc.h tau_mix, R19)
@@ -779,19 +834,20 @@ double binom(int n, int m) {
   return r;
 }
 
-template <int NS>
+template <int NS, int NE>
 int launch_epilogue_t(const rc_mech *m, const EpiArgs &ea, const CellsDev &c, cudaStream_t s) {
   const int ns = m->ns, nn = ea.n_nets;
   const int stages = 3;
-  const size_t smem = (size_t)(ThermoSeg::size(ns) + ((ns * ns + 1) & ~1) + nn * ((ns + 1) & ~1) + 16 + ((3 * nn + 1) & ~1)) * 8 +
+  const int pn = NE ? ((nn + ns) * NE + 1) & ~1 : nn * ((ns + 1) & ~1);
+  const size_t smem = (size_t)(ThermoSeg::size(ns) + ((ns * ns + 1) & ~1) + pn + 16 + ((3 * nn + 1) & ~1)) * 8 +
                       rcs::Ring<epi_tile<NS>()>::smem_bytes(2 + ns, nn * ea.passes, stages);
   constexpr int EPI_TILE = epi_tile<NS>(), EPI_THREADS = EPI_TILE + 32;
   const int64_t ntiles = (ea.rows + EPI_TILE - 1) / EPI_TILE;
-  int64_t grid = rc_resident_blocks((const void *)chem_epilogue_kernel<NS>, EPI_THREADS, smem);
+  int64_t grid = rc_resident_blocks((const void *)chem_epilogue_kernel<NS, NE>, EPI_THREADS, smem);
   if (grid > ntiles) grid = ntiles;
   if (grid > QPART_BLOCKS) grid = QPART_BLOCKS;
   ProfScope prof(RC_STAGE_EPILOGUE, s);
-  chem_epilogue_kernel<NS><<<(unsigned)grid, EPI_THREADS, smem, s>>>(ea, c, stages);
+  chem_epilogue_kernel<NS, NE><<<(unsigned)grid, EPI_THREADS, smem, s>>>(ea, c, stages);
   RC_LAUNCH_CHECK();
   return RC_OK;
 }
@@ -812,10 +868,13 @@ int launch_l4(const rc_mlp *n, const void *h3, float *o, int rows, int cap, bool
   return RC_OK;
 }
 
-int launch_epilogue(const rc_mech *m, const EpiArgs &ea, const CellsDev &c, cudaStream_t s) {
-  if (m->ns == 9) return launch_epilogue_t<9>(m, ea, c, s);
-  if (m->ns == 20) return launch_epilogue_t<20>(m, ea, c, s);
-  return launch_epilogue_t<0>(m, ea, c, s);
+int launch_epilogue(const rc_mech *m, const rc_mlp *n, const EpiArgs &ea, const CellsDev &c, cudaStream_t s) {
+  // factored projection when net i predicts species i (checked at rc_mlp_create) and the element
+  // count has an instance
+  const bool ident = n->species_identity;
+  if (m->ns == 9) return ident && m->ne == 3 ? launch_epilogue_t<9, 3>(m, ea, c, s) : launch_epilogue_t<9, 0>(m, ea, c, s);
+  if (m->ns == 20) return ident && m->ne == 4 ? launch_epilogue_t<20, 4>(m, ea, c, s) : launch_epilogue_t<20, 0>(m, ea, c, s);
+  return launch_epilogue_t<0, 0>(m, ea, c, s);
 }
 }  // namespace
 
@@ -906,13 +965,20 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
     ProArgs pa{0, (int)c.n, (int)zrows, n->d_in, n->ns, KZ, (float)n->lambda_bc, (float)(1.0 / n->lambda_bc),
                n->d_xmean, n->d_xinvstd, z, prec, (int64_t)(zlo / EB)};
     ProfScope prof(RC_STAGE_PROLOGUE, s);
-    const int pstages = 3;
-    const size_t psmem = rcs::Ring<PRO_TILE>::smem_bytes(2 + n->ns, 0, pstages);
-    int64_t pgrid = rc_resident_blocks((const void *)prologue_kernel, PRO_THREADS, psmem);
-    const int64_t ptiles = (c.n + PRO_TILE - 1) / PRO_TILE;
-    if (pgrid > ptiles) pgrid = ptiles;
-    if (pgrid < 1) pgrid = 1;  // n == 0 cannot reach here; padding rows only would need one CTA
-    prologue_kernel<<<(unsigned)pgrid, PRO_THREADS, psmem, s>>>(pa, c, pstages);
+    auto launch_pro = [&](auto tile_c) {
+      constexpr int TILE = decltype(tile_c)::value;
+      const int pstages = 3;
+      const size_t psmem = rcs::Ring<TILE>::smem_bytes(2 + n->ns, 0, pstages);
+      int64_t pgrid = rc_resident_blocks((const void *)prologue_kernel<TILE>, pro_threads<TILE>(), psmem);
+      const int64_t ptiles = (c.n + TILE - 1) / TILE;
+      if (pgrid > ptiles) pgrid = ptiles;
+      if (pgrid < 1) pgrid = 1;  // n == 0 cannot reach here; padding rows only would need one CTA
+      prologue_kernel<TILE><<<(unsigned)pgrid, pro_threads<TILE>(), psmem, s>>>(pa, c, pstages);
+    };
+    if (n->ns <= 12)
+      launch_pro(std::integral_constant<int, 256>{});
+    else
+      launch_pro(std::integral_constant<int, 128>{});
     RC_LAUNCH_CHECK();
   }
   for (int64_t c0 = 0; c0 < c.n; c0 += cap) {
@@ -955,9 +1021,9 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   }
   {  // a5 once over every cell of the call (one streaming pass, like the prologue)
     EpiArgs ea{0, (int)c.n, (int)zrows, nout, shared ? 1 : n->h3 / NP3, n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt,
-               opart, n->d_b4, n->d_ymean, n->d_ystd, m->d_P, m->d_thermo, n->d_species, qpart, {}};
+               opart, n->d_b4, n->d_ymean, n->d_ystd, m->d_P, m->d_thermo, n->d_species, m->d_EF, m->ne, qpart, {}};
     for (int q = 0; q <= 16; ++q) ea.binom[q] = q <= n->inv_lambda ? binom(n->inv_lambda, q) : 0.0;
-    if ((rc = launch_epilogue(m, ea, c, s))) return rc;
+    if ((rc = launch_epilogue(m, n, ea, c, s))) return rc;
   }
   if (c.red) {
     ProfScope prof(RC_STAGE_FINALIZE, s);

@@ -260,6 +260,42 @@ def test_inverse_box_cox_nonpositive_base():
         assert np.array_equal(g["diag"], o["diag"]), (g["diag"], o["diag"])
 
 
+@pytest.mark.parametrize("mname,cfg,perm", [("h2_9sp", "C1", "identity"), ("h2_9sp", "C1", "reversed"),
+                                            ("h2_9sp", "C1", "subset"), ("ch4_20sp", "C4", "identity"),
+                                            ("ch4_20sp", "C4", "reversed")])
+def test_projection_both_forms_exact_outputs(mname, cfg, perm):
+    """The epilogue applies P = I - E^T (E E^T)^-1 E in factored form when net i predicts species i
+    (the mechanisms' layout) and as columns of P otherwise; both against the oracle's P (step 9) on
+    exact outputs: zero hidden weights and a distinct fp32-exact b4 per net, so o is exact on both sides and
+    wdot / qdot differ only by fp64 rounding.  'reversed' maps net i to species n_nets - 1 - i,
+    'subset' drops every other net (species without a net get dY = 0)."""
+    from workload import make_bundle
+    b = make_bundle(mname, hidden=(64, 32, 16))
+    nn = b["n_nets"]
+    if perm == "reversed":
+        b["species_of_net"] = b["species_of_net"][::-1].copy()
+    elif perm == "subset":
+        keep = np.arange(0, nn, 2)
+        b["n_nets"], b["species_of_net"] = keep.size, b["species_of_net"][keep].copy()
+        for k in ("params", "y_mean", "y_std"):
+            b[k] = b[k][keep].copy()
+    b["params"][:] = 0.0
+    b["params"][:, -1] = 0.25 + np.arange(b["n_nets"]) / 64.0   # exact in fp32 (the kernel's o)
+    cols = None if cfg == "C1" else _sample(cfg, 96)
+    c = inputs(cfg) if cols is None else inputs(cfg, idx=cols)
+    o = run_oracle(cfg, c, b=b)
+    g = Gpu(cfg, b=b).run(c)
+    assert np.array_equal(g["o"], o["o"].astype(np.float32))
+    assert rel_fro(g["wdot"], o["wdot"]) <= 1e-12, rel_fro(g["wdot"], o["wdot"])
+    assert max_rel(g["qdot"], o["qdot"]) <= 1e-9
+    assert np.array_equal(g["diag"], o["diag"]), (g["diag"], o["diag"])
+    m = mech(mname)
+    W = (m["atoms"] * m["W_elem"][:, None]).sum(0)
+    E = m["atoms"] * m["W_elem"][:, None] / W[None, :]
+    tot = np.abs(g["wdot"]).sum(axis=0) + 1e-300
+    assert np.all(np.abs(E @ g["wdot"]) <= 1e-12 * tot[None, :])
+
+
 @pytest.mark.parametrize("prec,tol,dtol", [(1, 1e-3, 2e-3), (2, 1e-3, 1e-3)])
 def test_ch4_tf32_modes_sample(prec, tol, dtol):
     """C4 (d_in 22 -> 32-wide z rows, 19 nets) in the TF32 and TF32X3 modes."""
