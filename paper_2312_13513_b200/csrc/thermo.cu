@@ -45,11 +45,14 @@ __device__ __forceinline__ void warp_max_T(double *dst, double T) {
     atomicMax((unsigned long long *)dst, (unsigned long long)__double_as_longlong(v));
 }
 
-constexpr int THERMO_TILE = 256;                  // cells per stage = consumer threads per CTA
-constexpr int THERMO_THREADS = THERMO_TILE + 32;  // + the producer warp (stream.cuh run_ws)
+// cells per stage = consumer threads per CTA (+ the producer warp, stream.cuh run_ws): 256 for the
+// H2 set; 128 otherwise, where a 256-cell stage of 3 + Ns fp64 rows (47 KB at Ns = 20) leaves one
+// CTA (8 consumer warps) per SM
+template <int NS> constexpr int thermo_tile() { return NS == 9 ? 256 : 128; }
 
 template <int NS, bool UNIFORM>
-__global__ void __launch_bounds__(THERMO_THREADS, 3) thermo_kernel(const double *__restrict__ tab, int ns_rt, CellsDev c, int stages) {
+__global__ void __launch_bounds__(thermo_tile<NS>() + 32, 3) thermo_kernel(const double *__restrict__ tab, int ns_rt, CellsDev c, int stages) {
+  constexpr int THERMO_TILE = thermo_tile<NS>();
   extern __shared__ __align__(16) double s_tab[];
   __shared__ __align__(8) uint64_t bars[1 + 16];
   const int ns = NS ? NS : ns_rt;
@@ -258,6 +261,7 @@ int launch_thermo_t(const rc_mech *m, const CellsDev &c, cudaStream_t s) {
   const int rows = 2 + m->ns + (c.mode == RC_MODE_H ? 1 : 0);
   // 3 stages: two tiles in flight per CTA behind the one being computed
   const int stages = 3;
+  constexpr int THERMO_TILE = thermo_tile<NS>(), THERMO_THREADS = THERMO_TILE + 32;
   const size_t smem = (size_t)ThermoSeg::size(m->ns) * 8 + rcs::Ring<THERMO_TILE>::smem_bytes(rows, 0, stages);
   const int64_t ntiles = (c.n + THERMO_TILE - 1) / THERMO_TILE;
   int64_t grid = rc_resident_blocks((const void *)thermo_kernel<NS, U>, THERMO_THREADS, smem);
