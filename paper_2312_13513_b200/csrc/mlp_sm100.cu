@@ -332,13 +332,17 @@ __device__ __forceinline__ double2 lds2_epi(const double *p) {
 // cells per stage = consumer threads (+ the producer warp, stream.cuh run_ws): 256 (two CTAs of
 // eight consumer warps per SM) unless the Ns = 20 register/shared footprint needs 128
 template <int NS> constexpr int epi_tile() { return NS == 20 ? 128 : 256; }
+// Ns = 20: two stages (one tile in flight per CTA while one is computed) and three CTAs per SM: the
+// per-cell chain (19 inverse transforms) is latency-bound at the two CTAs three stages allow
+template <int NS> constexpr int epi_stages() { return NS == 20 ? 2 : 3; }
+template <int NS> constexpr int epi_min_ctas() { return NS == 0 ? 1 : NS == 20 ? 3 : 2; }
 
 // NE > 0: net `net` predicts species `net` (the usual layout: the inert species last) and the mechanism
 // has NE elements; the projection is then applied in factored form, v = dY - E^T (F dY), with F dY
 // accumulated per net (NE FMAs instead of Ns) and dY kept in registers (the net loop is fully
 // unrolled, so dY_net has a static register).  NE == 0: the outer product with the columns of P.
 template <int NS, int NE>
-__global__ void __launch_bounds__(epi_tile<NS>() + 32, NS == 0 ? 1 : 2) chem_epilogue_kernel(EpiArgs a, CellsDev c, int stages) {
+__global__ void __launch_bounds__(epi_tile<NS>() + 32, epi_min_ctas<NS>()) chem_epilogue_kernel(EpiArgs a, CellsDev c, int stages) {
   constexpr int EPI_TILE = epi_tile<NS>(), EPI_THREADS = EPI_TILE + 32;
   constexpr int CAP = NS ? NS : RC_MAX_NS;
   constexpr int UR = NS ? NS : 1;
@@ -391,7 +395,7 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, NS == 0 ? 1 : 2) chem_epi
   }
   for (int e = threadIdx.x; e < nn; e += blockDim.x) {
     sSpec[e] = a.species[e];
-    sB4[e] = a.b4[e];
+    reinterpret_cast<float *>(sB4)[e] = a.b4[e];  // fp32, as the net output it is added to
     sYM[e] = a.ymean[e];
     sYS[e] = a.ystd[e];
   }
@@ -410,7 +414,7 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, NS == 0 ? 1 : 2) chem_epi
     // v = P dY as an outer product with column `species[net]` of P (species without a net
     // contribute 0); the loop stays rolled for large mechanisms (instruction-cache footprint)
     auto net_out = [&](int net) {  // raw output o of the net (layer 3's passes summed), b4 added
-      float o = (float)sB4[net] + S4[net * a.passes * EPI_TILE];
+      float o = reinterpret_cast<const float *>(sB4)[net] + S4[net * a.passes * EPI_TILE];
 #pragma unroll 1
       for (int ps = 1; ps < a.passes; ++ps) o += S4[(net * a.passes + ps) * EPI_TILE];
       if (c.o) c.o[net * c.ld + i] = o;
@@ -837,7 +841,7 @@ double binom(int n, int m) {
 template <int NS, int NE>
 int launch_epilogue_t(const rc_mech *m, const EpiArgs &ea, const CellsDev &c, cudaStream_t s) {
   const int ns = m->ns, nn = ea.n_nets;
-  const int stages = 3;
+  const int stages = epi_stages<NS>();
   const int pn = NE ? ((nn + ns) * NE + 1) & ~1 : nn * ((ns + 1) & ~1);
   const size_t smem = (size_t)(ThermoSeg::size(ns) + ((ns * ns + 1) & ~1) + pn + 16 + ((3 * nn + 1) & ~1)) * 8 +
                       rcs::Ring<epi_tile<NS>()>::smem_bytes(2 + ns, nn * ea.passes, stages);
