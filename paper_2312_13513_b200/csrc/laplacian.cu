@@ -41,7 +41,7 @@ struct Gamma {
 
 // grid (ceil(nx / 256), ny, nz): thread (i, j, k) without integer division; the coefficients of the
 // 7-point stencil are formed per system from the neighbours' properties (rho, lambda/cp read once)
-__global__ void __launch_bounds__(256) lap_gather_kernel(LapGeo g, Gamma G, int nsys, double *upper, double *diag) {
+__global__ void __launch_bounds__(256, 4) lap_gather_kernel(LapGeo g, Gamma G, int nsys, double *upper, double *diag) {
   const bool halo = G.halo[0] != nullptr;
   const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, k = blockIdx.z;
   if (i >= g.nx) return;
@@ -57,34 +57,60 @@ __global__ void __launch_bounds__(256) lap_gather_kernel(LapGeo g, Gamma G, int 
                          top ? c + g.plane - g.n : c + g.plane,
                          bot ? c - g.plane + g.n : c - g.plane};
   const bool hz[7] = {false, false, false, false, false, top && halo, bot && halo};
-  double rho[7], le[7];  // rho and lambda / cp of the 7 stencil cells
+  double rho[7];  // rho of the 7 stencil cells (lambda / cp is formed for the energy system at the end)
+#pragma unroll
+  for (int q = 0; q < 7; ++q) rho[q] = hz[q] ? G.halo[q == 5 ? 1 : 0][p] : G.rho[nb[q]];
+  double *up = upper + c, *dg = diag + c;
+  auto emit = [&](const double (&gm)[7]) {
+    // owner's operand order: gamma_f = (gamma_owner + gamma_neighbour) / 2
+    const double axp = 0.5 * __dadd_rn(gm[0], gm[1]) * g.S[0], axm = 0.5 * __dadd_rn(gm[2], gm[0]) * g.S[0];
+    const double ayp = 0.5 * __dadd_rn(gm[0], gm[3]) * g.S[1], aym = 0.5 * __dadd_rn(gm[4], gm[0]) * g.S[1];
+    const double azp = 0.5 * __dadd_rn(gm[0], gm[5]) * g.S[2], azm = 0.5 * __dadd_rn(gm[6], gm[0]) * g.S[2];
+    up[0] = axp;
+    up[g.n] = ayp;
+    up[2 * g.n] = azp;
+    dg[0] = -(((axp + axm) + (ayp + aym)) + (azp + azm));
+    up += 3 * g.n;
+    dg += g.n;
+  };
+  // species systems: per stencil cell a pointer to its D_s (block or halo plane), advanced by its
+  // stride each system; the loads of system s + 1 are issued before system s is finished (two systems
+  // of loads in flight per thread: the pass is bound by L2/HBM latency, ncu long_scoreboard)
+  const int nspec = nsys - 1 < G.ns ? nsys - 1 : G.ns;
+  const double *dp[7];
+  int64_t ds[7];
 #pragma unroll
   for (int q = 0; q < 7; ++q) {
-    if (hz[q]) {
-      const double *b = G.halo[q == 5 ? 1 : 0];
-      rho[q] = b[p];
-      le[q] = b[g.plane + p] / b[2 * g.plane + p];
-    } else {
-      rho[q] = G.rho[nb[q]];
-      le[q] = G.lam[nb[q]] / G.cp[nb[q]];
-    }
+    dp[q] = hz[q] ? G.halo[q == 5 ? 1 : 0] + 3 * g.plane + p : G.D + nb[q];
+    ds[q] = hz[q] ? g.plane : G.ld;
   }
+  double cur[7], nxt[7];
+#pragma unroll
+  for (int q = 0; q < 7; ++q) cur[q] = nspec > 0 ? *dp[q] : 0.0;
 #pragma unroll 1
-  for (int s = 0; s < nsys; ++s) {
+  for (int s = 0; s < nspec; ++s) {
+    if (s + 1 < nspec)
+#pragma unroll
+      for (int q = 0; q < 7; ++q) nxt[q] = dp[q][(s + 1) * ds[q]];
     double gm[7];
 #pragma unroll
-    for (int q = 0; q < 7; ++q)
-      gm[q] = s == G.ns ? le[q]
-                        : rho[q] * (hz[q] ? G.halo[q == 5 ? 1 : 0][(3 + s) * g.plane + p] : G.D[s * G.ld + nb[q]]);
-    // owner's operand order: gamma_f = (gamma_owner + gamma_neighbour) / 2
-    const double axp = 0.5 * (gm[0] + gm[1]) * g.S[0], axm = 0.5 * (gm[2] + gm[0]) * g.S[0];
-    const double ayp = 0.5 * (gm[0] + gm[3]) * g.S[1], aym = 0.5 * (gm[4] + gm[0]) * g.S[1];
-    const double azp = 0.5 * (gm[0] + gm[5]) * g.S[2], azm = 0.5 * (gm[6] + gm[0]) * g.S[2];
-    double *up = upper + (size_t)s * 3 * g.n;
-    up[c] = axp;
-    up[g.n + c] = ayp;
-    up[2 * g.n + c] = azp;
-    diag[(size_t)s * g.n + c] = -(((axp + axm) + (ayp + aym)) + (azp + azm));
+    for (int q = 0; q < 7; ++q) gm[q] = __dmul_rn(rho[q], cur[q]);  // rounded: no FMA into the face sums
+    emit(gm);
+#pragma unroll
+    for (int q = 0; q < 7; ++q) cur[q] = nxt[q];
+  }
+  if (nsys > nspec) {  // energy: gamma = lambda / cp
+    double gm[7];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      if (hz[q]) {
+        const double *b = G.halo[q == 5 ? 1 : 0];
+        gm[q] = b[g.plane + p] / b[2 * g.plane + p];
+      } else {
+        gm[q] = G.lam[nb[q]] / G.cp[nb[q]];
+      }
+    }
+    emit(gm);
   }
 }
 
@@ -162,12 +188,25 @@ __global__ void __launch_bounds__(256) ldu_to_csr_kernel(LapGeo g, int nsys, con
   __syncwarp();
   for (int q = lane; q < nrow * 7; q += 32) col[7 * c0 + q] = sc[q];
   __syncwarp();
-  for (int s = 0; s < nsys; ++s) {
+  // per entry: its source (diag or upper) and the stride to the next system; the next system's seven
+  // values are loaded before this one is staged (the pass is latency-bound, ncu long_scoreboard)
+  const double *src[7];
+  int64_t sstr[7];
 #pragma unroll
-    for (int e = 0; e < 7; ++e) {
-      const int64_t sl = slot[ord[e]];
-      stg[w][lane * 7 + e] = sl < 0 ? diag[(size_t)s * g.n + c] : upper[(size_t)s * 3 * g.n + sl];
-    }
+  for (int e = 0; e < 7; ++e) {
+    const int64_t sl = slot[ord[e]];
+    src[e] = sl < 0 ? diag + c : upper + sl;
+    sstr[e] = sl < 0 ? g.n : 3 * g.n;
+  }
+  double cur[7], nxt[7];
+#pragma unroll
+  for (int e = 0; e < 7; ++e) cur[e] = nsys > 0 ? src[e][0] : 0.0;
+  for (int s = 0; s < nsys; ++s) {
+    if (s + 1 < nsys)
+#pragma unroll
+      for (int e = 0; e < 7; ++e) nxt[e] = src[e][(s + 1) * sstr[e]];
+#pragma unroll
+    for (int e = 0; e < 7; ++e) stg[w][lane * 7 + e] = cur[e];
     __syncwarp();
     double *dst = val + (size_t)s * 7 * g.n + 7 * c0;
     if (nrow == 32 && ((uintptr_t)dst & 15u) == 0) {
@@ -176,6 +215,8 @@ __global__ void __launch_bounds__(256) ldu_to_csr_kernel(LapGeo g, int nsys, con
       for (int q = lane; q < nrow * 7; q += 32) dst[q] = stg[w][q];
     }
     __syncwarp();
+#pragma unroll
+    for (int e = 0; e < 7; ++e) cur[e] = nxt[e];
   }
 }
 
