@@ -437,8 +437,26 @@ def run_ours(a):
             except (OSError, ValueError):
                 traffic = None
         mlp_ms = sum(per(s)[0] for s in ("L1", "L2", "L3", "L12", "L4"))
+        # the roofline object describes the dominant kernel of the step that ran: the MLP's layer-1/2
+        # GEMM for the DNN chemistry; the kinetics kernel when --chem kinetics replaces it (NEXT-3)
+        if a.chem == "kinetics" and "kinetics" in kernels:
+            kk = kernels["kinetics"]
+            roofline = {"kernel": "kinetics_kernel (12 reactions, falloff, reverse rates; fp64)", "bound": "fp64",
+                        "achieved": kk["achieved"], "peak": kk["peak"], "unit": kk["unit"], "frac": kk["frac"],
+                        "traffic": None, "peak_source": f64_src,
+                        "work_per_launch": "2 * KIN_FP64_INSTR_PER_CELL * cells FLOP (ncu-calibrated FP64 instruction count)"}
+        else:
+            roofline = {"kernel": (f"fused L1+L2 (z -> h1 1600 on chip -> h2 800, tcgen05 {a.precision}, 4-CTA clusters)"
+                                   if fused else f"L2 GEMM (h1 1600 -> h2 800, tcgen05 {a.precision})"), "bound": "tensor",
+                        "achieved": l2.get("achieved"), "peak": tpeak, "unit": "TFLOP/s",
+                        "frac": l2.get("frac"), "traffic": traffic,
+                        "peak_source": f"{pk_src} {SUSTAINED} (MEASURED_PEAKS.json)"
+                                       + ("" if a.precision == "bf16" else f" x {tratio:.3f} ({a.precision}, nominal ratio)"),
+                        "work_per_launch": ("2*cells_chunk*(d_in*1600 + 1600*800)*nets FLOP" if fused
+                                            else "2*cells_chunk*1600*800*nets FLOP")}
         out = {
-            "metric": "Mcells/s per thermo+transport+DNN-chem step",
+            "metric": ("Mcells/s per thermo+transport+DNN-chem step" if a.chem == "dnn"
+                       else "Mcells/s per thermo+transport+detailed-kinetics step (NEXT-3)"),
             "value": round(value, 4),
             "unit": "Mcells/s",
             "n_gpus": world,
@@ -448,7 +466,8 @@ def run_ours(a):
             "higher_is_better": True,
             "scaling": "strong" if a.strong else "weak",
             "vs_baseline": None,
-            "dtype": f"{a.precision} MLP (fp32 accumulate) + f64 thermo/transport/epilogue",
+            "dtype": (f"{a.precision} MLP (fp32 accumulate) + f64 thermo/transport/epilogue" if a.chem == "dnn"
+                      else "f64 (thermo, transport, detailed kinetics)"),
             "data": "synthetic (seeded manifold states, random-init paper-shape MLP weights)",
             "config": {"workload": f"{cfg.name}: {cfg.note}", "cells_per_gpu": int(n), "cells_total": int(total_cells),
                        "mech": cfg.mech, "hidden": list(cfg.hidden), "nets": nets, "parallelism": f"cells dp{world}",
@@ -459,14 +478,7 @@ def run_ours(a):
                        **({"chem": "detailed kinetics, 12 reactions (NEXT-3)"} if a.chem == "kinetics" else {}),
                        **({"consumer": "Laplacian assembly of ns+1 systems (NEXT-1)"} if a.laplacian else {}),
                        **({"launch": "one CUDA graph per step"} if a.graph else {})},
-            "roofline": {"kernel": (f"fused L1+L2 (z -> h1 1600 on chip -> h2 800, tcgen05 {a.precision}, 4-CTA clusters)"
-                                    if fused else f"L2 GEMM (h1 1600 -> h2 800, tcgen05 {a.precision})"), "bound": "tensor",
-                         "achieved": l2.get("achieved"), "peak": tpeak, "unit": "TFLOP/s",
-                         "frac": l2.get("frac"), "traffic": traffic,
-                         "peak_source": f"{pk_src} {SUSTAINED} (MEASURED_PEAKS.json)"
-                                        + ("" if a.precision == "bf16" else f" x {tratio:.3f} ({a.precision}, nominal ratio)"),
-                         "work_per_launch": ("2*cells_chunk*(d_in*1600 + 1600*800)*nets FLOP" if fused
-                                             else "2*cells_chunk*1600*800*nets FLOP")},
+            "roofline": roofline,
             "mlp_tflops": round(alg["mlp_flops"] / (mlp_ms * 1e-3) / 1e12, 2) if mlp_ms else None,
             "kernels": kernels,
             "clocks": clk.summary(),
