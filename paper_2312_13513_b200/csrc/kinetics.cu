@@ -88,25 +88,33 @@ __global__ void __launch_bounds__(KIN_THREADS) kinetics_kernel(const double *__r
 
   double qsum = 0.0;
   int n_bad = 0;
-  ring.run_ws(c.n, src8, src4, [&](int st, int64_t tile, int j) {
+  // the stage is read once, into the per-thread scratch columns, and released before the reaction
+  // loop (stream.cuh run_ws_release): the ring needs only one or two stages, so four CTAs fit per SM
+  ring.run_ws_release(c.n, src8, src4, [&](int st, int64_t tile, int j, auto &&release) {
     const int64_t i = tile * KIN_TILE + j;
-    if (i >= c.n) return;
+    const bool valid = i < c.n;  // lanes past the end stay until the release
     const double *S8 = ring.row8(st, 0) + j;
-    const double T = S8[0], p = S8[KIN_TILE];
+    const double T = valid ? S8[0] : 1000.0, p = valid ? S8[KIN_TILE] : KIN_P0;
     const double lnT = log(T), invT = 1.0 / T;
-    double sW = 0.0;
+    double sW = 0.0, conc = 0.0;
 #pragma unroll UR
     for (int k = 0; k < CAP; ++k)
-      if (k < ns) sW = fma(S8[(2 + k) * KIN_TILE], IW[k], sW);
+      if (k < ns) {
+        const double y = valid ? S8[(2 + k) * KIN_TILE] : 0.0;
+        sW = fma(y, IW[k], sW);
+        conc = fma(y > 0.0 ? y : 0.0, IW[k], conc);  // PaSR: sum_k C+_k / rho
+      }
     const double rho = p / (RC_RU * T * sW);
 #pragma unroll UR
     for (int k = 0; k < CAP; ++k)
       if (k < ns) {
-        sC[k * KIN_TILE + j] = rho * S8[(2 + k) * KIN_TILE] * IW[k];
+        sC[k * KIN_TILE + j] = rho * (valid ? S8[(2 + k) * KIN_TILE] : 0.0) * IW[k];
         const double *a = G + 16 * k + (T <= TM[k] ? 0 : 8);
         sG[k * KIN_TILE + j] = fma(a[1], lnT, a[0]) + T * fma(T, fma(T, fma(T, a[5], a[4]), a[3]), a[2]) + a[6] * invT;
         sR[k * KIN_TILE + j] = 0.0;
       }
+    release();
+    if (!valid) return;
     const double lnp0RT = log(KIN_P0 / RC_RU) - lnT;
     // net rate of progress of reaction r (reads only: two reactions are evaluated back to back so
     // their exp chains overlap; the rate updates follow)
@@ -177,14 +185,10 @@ __global__ void __launch_bounds__(KIN_THREADS) kinetics_kernel(const double *__r
     // wdot_k = W_k sum_r nu_rk q_r; LES: PaSR factor (rc.h tau_mix, R19); qdot
     double scale = 1.0;
     if (c.tau_mix) {
-      double act = 0.0, conc = 0.0;
+      double act = 0.0;
 #pragma unroll UR
       for (int k = 0; k < CAP; ++k)
-        if (k < ns) {
-          const double y = S8[(2 + k) * KIN_TILE];
-          act += fabs(W[k] * sR[k * KIN_TILE + j]) * IW[k];
-          conc = fma(y > 0.0 ? y : 0.0, IW[k], conc);
-        }
+        if (k < ns) act += fabs(W[k] * sR[k * KIN_TILE + j]) * IW[k];
       const double r = act > 0.0 ? 0.5 * act / (rho * conc) : 0.0;
       scale = 1.0 / fma(c.tau_mix[i], r, 1.0);
     }
@@ -221,7 +225,7 @@ __global__ void __launch_bounds__(KIN_THREADS) kinetics_kernel(const double *__r
 
 template <int NS>
 int launch_kinetics_t(const rc_mech *m, const rc_kin *k, const CellsDev &c, cudaStream_t s) {
-  const int ns = m->ns, stages = 3;
+  const int ns = m->ns, stages = 1;
   const size_t smem = (size_t)(KinSeg::size(ns, k->nr) + ThermoSeg::size(ns) + 3 * ns * KIN_TILE) * 8 +
                       rcs::Ring<KIN_TILE>::smem_bytes(2 + ns, 0, stages);
   const int64_t ntiles = (c.n + KIN_TILE - 1) / KIN_TILE;

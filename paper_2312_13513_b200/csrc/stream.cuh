@@ -117,6 +117,40 @@ struct Ring {
       if ((threadIdx.x & 31) == 0) rcx::mbar_arrive(&empty[s]);
     }
   }
+
+  // run_ws with an early release: body(s, t, j, release) copies what it needs out of stage s and
+  // then calls release() -- once, from every lane of the warp (no lane may return before it) -- so
+  // the producer refills the stage while the warp is still computing; one or two stages then keep
+  // the HBM stream going for kernels whose per-cell arithmetic dwarfs the copy.
+  template <class F8, class F4, class Body>
+  __device__ __forceinline__ void run_ws_release(int64_t n, F8 &&src8, F4 &&src4, Body &&body) const {
+    const int64_t ntiles = (n + TILE - 1) / TILE;
+    uint64_t *empty = full + stages;
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) {
+      if ((threadIdx.x & 31) == 0) {
+        int it = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+          const int s = it % stages;
+          if (it >= stages) rcx::mbar_wait_sleep(&empty[s], (uint32_t)(it / stages - 1) & 1u);
+          issue(s, t, n, src8, src4);
+        }
+      }
+      __syncwarp();
+      return;
+    }
+    const int j = threadIdx.x - 32;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int s = it % stages;
+      rcx::mbar_wait(&full[s], (uint32_t)(it / stages) & 1u);
+      auto release = [&]() {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) rcx::mbar_arrive(&empty[s]);
+      };
+      body(s, t, j, release);
+    }
+  }
 };
 
 }  // namespace rcs
