@@ -78,14 +78,15 @@ def capture(path):
         for key, (m, mul) in KEYS.items():
             if m not in d:  # some metrics carry a section prefix ("TPC.TriageCompute.<name>")
                 m = next((c for c in h if c.endswith("." + m) or c.endswith(m)), m)
-            if m not in d or d[m] in ("", "n/a"):
+            if m not in d or d[m] in ("", "n/a", "no data"):
                 continue
             v = float(d[m].replace(",", ""))
             if mul is not None:
                 v = v * SCALE.get(u.get(m, ""), 1) * mul if key == "duration_us" else v * SCALE.get(u.get(m, ""), 1)
             e[key] = round(v, 4) if isinstance(v, float) else v
-        stalls = {m.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(d[m] or 0) for m in h
-                  if m.startswith("smsp__pcsamp_warps_issue_stalled_") and not m.endswith("not_issued")}
+        stalls = {m.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(d[m].replace(",", "") or 0) for m in h
+                  if m.startswith("smsp__pcsamp_warps_issue_stalled_") and not m.endswith("not_issued")
+                  and d[m] not in ("n/a", "no data")}
         tot = sum(stalls.values())
         if tot:
             e["stall_top"] = {k2: round(v / tot, 3) for k2, v in sorted(stalls.items(), key=lambda kv: -kv[1])[:6]}
