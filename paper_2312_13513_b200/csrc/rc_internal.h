@@ -26,11 +26,11 @@ struct ThermoSeg {        // doubles, offsets relative to the segment start
   // [.. + 6ns)        hhi[k][j]
   // [.. + ns)         invW[k]
   // [.. + ns)         Tmid[k]
-  __host__ __device__ static int hlo(int) { return 4; }
-  __host__ __device__ static int hhi(int ns) { return 4 + 6 * ns; }
-  __host__ __device__ static int invW(int ns) { return 4 + 12 * ns; }
-  __host__ __device__ static int tmid(int ns) { return 4 + 13 * ns; }
-  __host__ __device__ static int size(int ns) { return (4 + 14 * ns + 1) & ~1; }  // even -> 16-byte multiple
+  __host__ __device__ static constexpr int hlo(int) { return 4; }
+  __host__ __device__ static constexpr int hhi(int ns) { return 4 + 6 * ns; }
+  __host__ __device__ static constexpr int invW(int ns) { return 4 + 12 * ns; }
+  __host__ __device__ static constexpr int tmid(int ns) { return 4 + 13 * ns; }
+  __host__ __device__ static constexpr int size(int ns) { return (4 + 14 * ns + 1) & ~1; }  // even -> 16-byte multiple
 };
 
 struct TransportSeg {
@@ -39,14 +39,14 @@ struct TransportSeg {
   // up to even, rows 16-byte aligned): with c1_kj = (W_j/W_k)^(1/4), c2_kj = 1/sqrt(8(1+W_k/W_j)),
   // M0 = c2, M1 = 2 c2 c1, M2 = c2 c1^2, so that sum_j X_j Phi_kj = A_k + s_k (B_k + s_k C_k)
   // with A = M0 X, B = M1 (X/s), C = M2 (X/s^2) and s_k = sqrt(mu_k)
-  __host__ __device__ static int nse(int ns) { return (ns + 1) & ~1; }
-  __host__ __device__ static int visc(int) { return 0; }
-  __host__ __device__ static int cond(int ns) { return 5 * ns; }
-  __host__ __device__ static int diff(int ns) { return 10 * ns; }
-  __host__ __device__ static int W(int ns) { return 10 * ns + 6 * (ns * (ns + 1) / 2); }
-  __host__ __device__ static int invW(int ns) { return W(ns) + nse(ns); }
-  __host__ __device__ static int M(int ns, int q) { return W(ns) + 2 * nse(ns) + q * ns * nse(ns); }
-  __host__ __device__ static int size(int ns) { return M(ns, 3); }
+  __host__ __device__ static constexpr int nse(int ns) { return (ns + 1) & ~1; }
+  __host__ __device__ static constexpr int visc(int) { return 0; }
+  __host__ __device__ static constexpr int cond(int ns) { return 5 * ns; }
+  __host__ __device__ static constexpr int diff(int ns) { return 10 * ns; }
+  __host__ __device__ static constexpr int W(int ns) { return 10 * ns + 6 * (ns * (ns + 1) / 2); }
+  __host__ __device__ static constexpr int invW(int ns) { return W(ns) + nse(ns); }
+  __host__ __device__ static constexpr int M(int ns, int q) { return W(ns) + 2 * nse(ns) + q * ns * nse(ns); }
+  __host__ __device__ static constexpr int size(int ns) { return M(ns, 3); }
 };
 
 struct rc_mech {
