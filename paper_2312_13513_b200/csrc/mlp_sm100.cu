@@ -337,8 +337,8 @@ template <int NS> constexpr int epi_tile() { return NS == 20 ? 128 : 256; }
 template <int NS> constexpr int epi_stages() { return NS == 20 ? 2 : 3; }
 template <int NS> constexpr int epi_min_ctas() { return NS == 0 ? 1 : NS == 20 ? 3 : 2; }
 
-// NE > 0: net `net` predicts species `net` (the usual layout: the inert species last) and the mechanism
-// has NE elements; the projection is then applied in factored form, v = dY - E^T (F dY), with F dY
+// NE > 0: net `net` predicts species `net` (the usual layout: the inert species last), layer 3 ran in
+// one pass (h3 = 400, the paper width), the mechanism has one T_mid and NE elements; the projection is then applied in factored form, v = dY - E^T (F dY), with F dY
 // accumulated per net (NE FMAs instead of Ns) and dY kept in registers (the net loop is fully
 // unrolled, so dY_net has a static register).  NE == 0: the outer product with the columns of P.
 template <int NS, int NE>
@@ -428,8 +428,9 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, epi_min_ctas<NS>()) chem_
 #pragma unroll
       for (int net = 0; net < CAP; ++net) {
         v[net] = 0.0;
-        if (net < nn) {
-          const float o = net_out(net);
+        if (net < nn) {  // one layer-3 pass (checked at launch): raw output row `net`
+          const float o = reinterpret_cast<const float *>(sB4)[net] + S4[net * EPI_TILE];
+          if (c.o) c.o[net * c.ld + i] = o;
           const double y = S8[(2 + net) * EPI_TILE];
           const double dy = inv_boxcox_dy(y > 0.0 ? y : 0.0, (double)o * sYS[net] + sYM[net], a);
           v[net] = dy;
@@ -488,7 +489,8 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, epi_min_ctas<NS>()) chem_
         neg |= ((y > 0.0 ? y : 0.0) + v[k]) < 0.0;
         const double w = scale * v[k];
         c.wdot[k * c.ld + i] = w;
-        const double *h = (T <= tmid[k]) ? hlo + 6 * k : hhi + 6 * k;
+        // NE > 0 runs only for a mechanism with one T_mid (checked at launch): one range per cell
+        const double *h = NE > 0 ? (T <= s_tab[2] ? hlo : hhi) + 6 * k : (T <= tmid[k]) ? hlo + 6 * k : hhi + 6 * k;
         const double hk = fma(T, fma(T, fma(T, fma(T, fma(T, h[4], h[3]), h[2]), h[1]), h[0]), h[5]);
         q = fma(-hk, w, q);
         bad |= !isfinite(w);
@@ -875,7 +877,7 @@ int launch_l4(const rc_mlp *n, const void *h3, float *o, int rows, int cap, bool
 int launch_epilogue(const rc_mech *m, const rc_mlp *n, const EpiArgs &ea, const CellsDev &c, cudaStream_t s) {
   // factored projection when net i predicts species i (checked at rc_mlp_create) and the element
   // count has an instance
-  const bool ident = n->species_identity;
+  const bool ident = n->species_identity && ea.passes == 1 && m->uniform_tmid;
   if (m->ns == 9) return ident && m->ne == 3 ? launch_epilogue_t<9, 3>(m, ea, c, s) : launch_epilogue_t<9, 0>(m, ea, c, s);
   if (m->ns == 20) return ident && m->ne == 4 ? launch_epilogue_t<20, 4>(m, ea, c, s) : launch_epilogue_t<20, 0>(m, ea, c, s);
   return launch_epilogue_t<0, 0>(m, ea, c, s);
