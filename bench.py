@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--precision", default="bf16", choices=["bf16", "tf32", "tf32x3"])
     ap.add_argument("--strong", action="store_true", help="partition the config's cells (strong scaling)")
     ap.add_argument("--layerwise", action="store_true", help="rc_mlp_desc.flags = RC_MLP_LAYERWISE (comparison path)")
+    ap.add_argument("--serial", action="store_true",
+                    help="rc_mlp_desc.flags = RC_MLP_SERIAL: layer 3 not overlapped with the fused kernel (comparison)")
     ap.add_argument("--pasr", action="store_true", help="LES: PaSR scaling of wdot with per-cell tau_mix (NEXT-4)")
     ap.add_argument("--shared", action="store_true", help="one shared net with n_nets outputs (NEXT-2)")
     ap.add_argument("--laplacian", action="store_true",
@@ -279,7 +281,8 @@ def run_ours(a):
     bundle = make_bundle(cfg.mech, hidden=cfg.hidden, shared=a.shared)
     mech = rc.Mechanism(mech_d)
     prec = {"bf16": rc.RC_BF16, "tf32": rc.RC_TF32, "tf32x3": rc.RC_TF32X3}[a.precision]
-    mlp = rc.MLPBundle(mech, bundle, prec, flags=rc._rc.RC_MLP_LAYERWISE if a.layerwise else 0)
+    mlp = rc.MLPBundle(mech, bundle, prec, flags=(rc.RC_MLP_LAYERWISE if a.layerwise else 0) |
+                       (rc.RC_MLP_SERIAL if a.serial else 0))
     ns, nets = mech_d["ns"], bundle["n_nets"]
     st = rc.CellState(n, ns, nets, outputs=("cp", "rho", "mu", "lam", "D", "wdot", "qdot"))
     st.load(host["T_true"], host["p"], host["Y"])
@@ -357,6 +360,8 @@ def run_ours(a):
     else:
         rc.rc_profile_enable(True)
     rc.rc_profile_read(reset=True)
+    if hasattr(rc.lib(), "rc_overlap_read"):
+        rc.rc_overlap_read(reset=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -371,6 +376,7 @@ def run_ours(a):
         dist.barrier()
     ms = e0.elapsed_time(e1) / a.steps
     prof = rc.rc_profile_read(reset=True)
+    ovl = rc.rc_overlap_read(reset=True) if hasattr(rc.lib(), "rc_overlap_read") else {}
     rc.rc_profile_enable(False)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -408,6 +414,7 @@ def run_ours(a):
             ("L2", alg["L2_flops"], "TFLOP/s", "tensor", tpeak),
             ("L12", alg["L1_flops"] + alg["L2_flops"], "TFLOP/s", "tensor", tpeak),  # fused layers 1+2
             ("L3", alg["L3_flops"], "TFLOP/s", "tensor", tpeak),
+            ("L3_fill", alg["L3_flops"], "TFLOP/s", "tensor", tpeak),
             ("L4", alg["L4_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),  # shared net's output layer (CUDA cores)
             ("kinetics", alg["kinetics_fp64_flops"], "TFLOP/s", "fp64", f64),  # detailed kinetics (NEXT-3)
             ("laplacian", alg["laplacian_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),     # NEXT-1 assembly
@@ -417,14 +424,27 @@ def run_ours(a):
             t_ms, cnt = per(st_name)
             if t_ms <= 0:
                 continue
+            if st_name in ("L3", "L3_fill") and prof["L3_fill"][0] > 0:
+                # layer 3 overlapped with the fused kernel: the tiles the launches beside
+                # it ran (rc_overlap_read) are their work, the rest the main launches'; the side launches
+                # run on the SMs the fused kernel's clusters leave idle, their peak is that share of the GPU
+                l3_tiles = K * bundle["n_nets"] * (-(-n // 256)) if not bundle.get("shared") else 0
+                ffrac = min(1.0, ovl["tiles_fill"] / l3_tiles) if l3_tiles else 0.0
+                work = work * (ffrac if st_name == "L3_fill" else 1.0 - ffrac)
+                if st_name == "L3_fill":
+                    fill_sms = 2 * ovl["pairs_ran"] / max(1, prof["L3_fill"][1])  # SMs per side launch that ran
+                    peak = round(tpeak * fill_sms / torch.cuda.get_device_properties(0).multi_processor_count, 1)
             scale = 1e9 if unit == "GB/s" else 1e12
             ach = work / (t_ms * 1e-3) / scale
             kernels[st_name] = {"bound": bound, "achieved": round(ach, 2), "peak": peak, "unit": unit,
                                 "frac": round(ach / peak, 4), "ms_per_step": round(t_ms, 4),
                                 "launches_per_step": cnt, "share": None}
-        tot_k = sum(v["ms_per_step"] for v in kernels.values())
-        for v in kernels.values():
-            v["share"] = round(v["ms_per_step"] / tot_k, 4) if tot_k else None
+        tot_k = sum(v["ms_per_step"] for k, v in kernels.items() if k != "L3_fill")
+        for k, v in kernels.items():
+            v["share"] = round(v["ms_per_step"] / tot_k, 4) if tot_k and k != "L3_fill" else None
+        if "L3_fill" in kernels:  # concurrent with L12 on the otherwise idle SMs: not on the step's critical path
+            kernels["L3_fill"].update({"concurrent_with": "L12", "tiles_share": round(ffrac, 4),
+                                       "pairs_ran": ovl["pairs_ran"], "pairs_gave_up": ovl["pairs_gave_up"]})
         fused = "L12" in kernels
         l2 = kernels.get("L12" if fused else "L2", {})
         traffic = None
@@ -477,9 +497,15 @@ def run_ours(a):
                        **({"mlp": "one shared net, n_nets outputs (NEXT-2)"} if a.shared else {}),
                        **({"chem": "detailed kinetics, 12 reactions (NEXT-3)"} if a.chem == "kinetics" else {}),
                        **({"consumer": "Laplacian assembly of ns+1 systems (NEXT-1)"} if a.laplacian else {}),
-                       **({"launch": "one CUDA graph per step"} if a.graph else {})},
+                       **({"launch": "one CUDA graph per step"} if a.graph else {}),
+                       **({"mlp_schedule": "serial (RC_MLP_SERIAL)"} if a.serial else
+                          {"mlp_schedule": "layer 3 of chunk j-1 beside the fused L1+L2 kernel of chunk j on its idle SMs"}
+                          if prof["L3_fill"][0] > 0 else {})},
             "roofline": roofline,
+            # the whole MLP on the step's critical path (the layer-3 side launches run beside L12 and
+            # are not counted in mlp_ms): its FLOPs over that time, against the same tensor peak
             "mlp_tflops": round(alg["mlp_flops"] / (mlp_ms * 1e-3) / 1e12, 2) if mlp_ms else None,
+            "mlp_frac": round(alg["mlp_flops"] / (mlp_ms * 1e-3) / 1e12 / tpeak, 4) if mlp_ms and a.chem == "dnn" else None,
             "kernels": kernels,
             "clocks": clk.summary(),
             "gpu_launches": int(launches_per_step * a.steps),

@@ -53,7 +53,7 @@ enum {
 
 enum { RC_MODE_H = 0, RC_MODE_T = 1 };               /* rc_cells.mode */
 enum { RC_BF16 = 0, RC_TF32 = 1, RC_TF32X3 = 2 };     /* rc_mlp_desc.precision */
-enum { RC_MLP_LAYERWISE = 1, RC_MLP_SHARED = 2 };     /* rc_mlp_desc.flags */
+enum { RC_MLP_LAYERWISE = 1, RC_MLP_SHARED = 2, RC_MLP_SERIAL = 4 };     /* rc_mlp_desc.flags */
 
 /* Diagnostic counters in rc_cells.diag[] (int64, accumulated with atomics). */
 enum {
@@ -127,7 +127,16 @@ typedef struct {
                                      net per species (reading R20:
                                      the Table-1-consistent reading of PAPER.md:114/210); params is
                                      then one block W1 b1 W2 b2 W3 b3 W4[n_nets][h3] b4[n_nets] and
-                                     output i predicts species_of_net[i].  RC_BF16 or RC_TF32 only. */
+                                     output i predicts species_of_net[i].  RC_BF16 or RC_TF32 only;
+                                     RC_MLP_SERIAL: run every MLP kernel on the caller's stream, in
+                                     chunk order.  By default, where the fused layer-1/2 kernel runs
+                                     (and the net is not shared), layer 3 of a chunk runs partly
+                                     beside the fused kernel of the next chunk on the SMs that
+                                     kernel's 4-CTA clusters leave idle, on a library-owned
+                                     auxiliary stream (one per host thread and device) forked from
+                                     and joined back into the caller's stream by events inside the
+                                     call (so stream capture works); DESIGN.md 6.4.  Results are
+                                     bitwise identical either way. */
 } rc_mlp_desc;
 
 int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *desc, rc_mlp **out);
@@ -290,10 +299,16 @@ enum {
   RC_STAGE_KINETICS = 10, /* detailed kinetics (rc_kinetics) */
   RC_STAGE_LAPLACIAN = 11, /* Laplacian assembly (rc_laplacian) */
   RC_STAGE_CSR = 12,      /* ldu -> CSR (rc_ldu_to_csr) */
-  RC_STAGE_COUNT = 13
+  RC_STAGE_L3_FILL = 13,  /* layer-3 launches on the auxiliary stream, beside the fused kernel */
+  RC_STAGE_COUNT = 14
 };
 int rc_profile_enable(int on);
 int rc_profile_read(double *ms /* [RC_STAGE_COUNT] */, int64_t *launches /* [RC_STAGE_COUNT] */, int reset);
+/* Layer-3 overlap counters since the last reset (process-global, current device; synchronous):
+ * out[0] = layer-3 tiles (256 cells x one pass of one net) run by the launches beside the fused
+ * kernel, out[1] = CTA pairs of those launches that found the fused kernel not yet resident after
+ * 50 us and did nothing, out[2] = CTA pairs that ran.  Errors: RC_EINVAL (NULL out), RC_ECUDA. */
+int rc_overlap_read(int64_t *out /* [3] */, int reset);
 
 /* Number of kernel launches the last rc_* call on this thread enqueued. */
 int64_t rc_last_launch_count(void);

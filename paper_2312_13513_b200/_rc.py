@@ -16,7 +16,7 @@ SO = os.environ.get("RC_LIB") or os.path.join(HERE, "librc_b200.so")  # RC_LIB: 
 RC_OK, RC_EINVAL, RC_ENOMEM, RC_ECUDA, RC_EALIGN, RC_EUNSUPPORTED, RC_EDTMISMATCH = 0, -1, -2, -3, -4, -5, -6
 RC_MODE_H, RC_MODE_T = 0, 1
 RC_BF16, RC_TF32, RC_TF32X3 = 0, 1, 2
-RC_MLP_LAYERWISE, RC_MLP_SHARED = 1, 2
+RC_MLP_LAYERWISE, RC_MLP_SHARED, RC_MLP_SERIAL = 1, 2, 4
 DIAG_NAMES = ["newton_bisect", "newton_maxit", "nonfinite", "negY_in", "negY_out"]
 
 
@@ -79,6 +79,7 @@ EXPORTS = {
     "rc_last_launch_count": (C.c_int64, []),
     "rc_profile_enable": (C.c_int, [C.c_int]),
     "rc_profile_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+    "rc_overlap_read": (C.c_int, [C.c_void_p, C.c_int]),
     "rc_last_error": (C.c_char_p, []),
     "rc_version": (C.c_char_p, []),
 }
@@ -94,6 +95,8 @@ def lib():
             raise ImportError(f"{SO} not built; run `python -m paper_2312_13513_b200.build` (no CPU fallback exists)")
         L = C.CDLL(SO)
         for name, (res, args) in EXPORTS.items():
+            if os.environ.get("RC_LIB") and not hasattr(L, name):
+                continue  # an older build under A/B comparison (tools/ab.sh) may lack newer entry points
             f = getattr(L, name)
             f.restype, f.argtypes = res, args
         _lib = L
@@ -271,7 +274,7 @@ def rc_last_launch_count():
 
 
 STAGES = ["thermo", "transport", "prologue", "L1", "L2", "L3", "epilogue", "finalize", "L12", "L4", "kinetics",
-          "laplacian", "csr"]
+          "laplacian", "csr", "L3_fill"]
 
 
 def rc_profile_enable(on=True):
@@ -284,3 +287,10 @@ def rc_profile_read(reset=True):
     cnt = np.zeros(len(STAGES), dtype=np.int64)
     check(lib().rc_profile_read(ms.ctypes.data, cnt.ctypes.data, 1 if reset else 0))
     return {s: (float(ms[i]), int(cnt[i])) for i, s in enumerate(STAGES)}
+
+
+def rc_overlap_read(reset=True):
+    """Layer-3 overlap counters since the last reset: {tiles_fill, pairs_gave_up, pairs_ran}."""
+    out = np.zeros(3, dtype=np.int64)
+    check(lib().rc_overlap_read(out.ctypes.data, 1 if reset else 0))
+    return {"tiles_fill": int(out[0]), "pairs_gave_up": int(out[1]), "pairs_ran": int(out[2])}

@@ -122,6 +122,15 @@ extern "C" int rc_profile_read(double *ms, int64_t *launches, int reset) {
   return RC_OK;
 }
 
+extern "C" int rc_overlap_read(int64_t *out, int reset) {
+  if (!out) return rc_fail(RC_EINVAL, "rc_overlap_read: NULL out");
+  long long v[3];
+  const int r = l2_overlap_read(v, reset);
+  if (r) return r;
+  for (int i = 0; i < 3; ++i) out[i] = v[i];
+  return RC_OK;
+}
+
 extern "C" const char *rc_last_error(void) { return g_err; }
 extern "C" const char *rc_version(void) { return "rc-b200 0.1 (sm_100a)"; }
 extern "C" int64_t rc_last_launch_count(void) { return g_launches; }
@@ -296,7 +305,7 @@ extern "C" int rc_mlp_create(const rc_mech *m, const rc_mlp_desc *d, rc_mlp **ou
     return rc_fail(RC_EUNSUPPORTED, "rc_mlp_create: hidden (%d,%d,%d) must be multiples of (64,16,16)", h1, h2, h3);
   if (d->precision != RC_BF16 && d->precision != RC_TF32 && d->precision != RC_TF32X3)
     return rc_fail(RC_EINVAL, "rc_mlp_create: unknown precision %d", d->precision);
-  if (d->flags & ~(RC_MLP_LAYERWISE | RC_MLP_SHARED)) return rc_fail(RC_EINVAL, "rc_mlp_create: unknown flags 0x%x", d->flags);
+  if (d->flags & ~(RC_MLP_LAYERWISE | RC_MLP_SHARED | RC_MLP_SERIAL)) return rc_fail(RC_EINVAL, "rc_mlp_create: unknown flags 0x%x", d->flags);
   if ((d->flags & RC_MLP_SHARED) && d->precision == RC_TF32X3)
     return rc_fail(RC_EUNSUPPORTED, "rc_mlp_create: RC_MLP_SHARED runs in RC_BF16 or RC_TF32");
   if (!(d->lambda_bc > 0.0) || !(d->dt > 0.0)) return rc_fail(RC_EINVAL, "rc_mlp_create: lambda and dt must be > 0");

@@ -27,6 +27,16 @@ struct L2Args {
   int cap;
   int ktail;               // MMA K atoms in the last K chunk when K is not a multiple of it (0: full chunk)
   int prof_stage = -1;     // rc_profile stage (-1: L3 with w4, else L2)
+  // Dynamic tile schedule (layer 3 overlapped with the fused layer-1/2 kernel): the
+  // CTA pairs take tiles from *tile_ctr (zeroed before the first launch that shares it); nullptr:
+  // the static schedule cl, cl + ncl, ...
+  int *tile_ctr = nullptr;
+  // Filler launch (runs beside the fused layer-1/2 kernel on the SMs its 4-CTA clusters leave
+  // idle): take tiles only once *gate >= gate_target (every cluster of that kernel is resident,
+  // so this launch holds no SM the kernel needs); after gate_ns without that, do nothing.
+  const int *gate = nullptr;
+  int gate_target = 0;
+  unsigned gate_ns = 0;
 };
 // fused layers 1+2 (mlp_l12_sm100.cu, bf16, h2 = 800): clusters of two CTA pairs share h1 chunks
 // maps: {z (KZ x 128 rows), W1 (KZ x 16 rows), W2 piece 1 (32 x 128 rows), W2 piece 2 (32 x 72 rows),
@@ -34,10 +44,13 @@ struct L2Args {
 struct L12Args {
   int m_tiles, nets, chunks, N, stages;
   const float *bias;  // b2 [nets][N]
+  int *started = nullptr;  // += 1 per cluster once it is resident (the layer-3 filler's gate)
 };
 bool l12_supported(int h1, int h2, int kz, bool tf32);
-int launch_l12(int KZ, bool tf32, const CUtensorMap *maps, const L12Args &a, cudaStream_t s);
+// *clusters (optional) = the 4-CTA clusters launched
+int launch_l12(int KZ, bool tf32, const CUtensorMap *maps, const L12Args &a, cudaStream_t s, int *clusters = nullptr);
 
 // maps: {A, B piece 1, B piece 2, out store, A lo, B1 lo, B2 lo, out lo store, bias operand piece 1,
 //        bias operand piece 2} (lo: precision 2 only; bias operand tiles: bf16 only)
-int launch_l2_pair(int NP, int prec, const CUtensorMap *maps, const L2Args &a, cudaStream_t s);
+// pairs (optional): CTA pairs to launch (default: as many as are resident at once)
+int launch_l2_pair(int NP, int prec, const CUtensorMap *maps, const L2Args &a, cudaStream_t s, int pairs = 0);

@@ -150,6 +150,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(L12_THREADS, 1)
   rcx::tc_fence_before();
   rcx::cluster_sync();
   rcx::tc_fence_after();
+  // this cluster is resident: count it for the layer-3 filler's gate
+  if (a.started && rank == 0 && threadIdx.x == 0) rcx::red_release_gpu_add(a.started, 1);
   const uint32_t tmem = *tmem_slot;
   const int C = a.chunks;  // CW-column h1 chunks (K chunks of layer 2)
   const int pairs = a.m_tiles / 2;
@@ -588,7 +590,7 @@ constexpr size_t L12_SMEM_MAX = 232448;
 template <int KZ, bool TF> constexpr int l12_ring() { return TF && KZ == 32 ? 3 : L12_RING; }
 
 template <int KZ, bool TF>
-int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
+int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s, int *nclusters) {
   constexpr int R = l12_ring<KZ, TF>();
   const size_t smem = l12_smem(KZ, a.chunks, TF, R);
   if (smem > L12_SMEM_MAX) return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel: shared memory");
@@ -619,6 +621,7 @@ int launch_t(const CUtensorMap *M, L12Args a, cudaStream_t s) {
   const int total = a.nets * (a.m_tiles / 2);
   int clusters = resident;
   if (clusters > total) clusters = total;
+  if (nclusters) *nclusters = clusters;
   l12_kernel<KZ, R, TF><<<4 * clusters, L12_THREADS, smem, s>>>(M[0], M[1], M[2], M[3], M[4], M[5], M[6], a);
   RC_LAUNCH_CHECK();
   return RC_OK;
@@ -641,14 +644,14 @@ extern "C" __attribute__((visibility("default"))) int rc_debug_l12trace(void *ho
 }
 #endif
 
-int launch_l12(int KZ, bool tf, const CUtensorMap *maps, const L12Args &a, cudaStream_t s) {
+int launch_l12(int KZ, bool tf, const CUtensorMap *maps, const L12Args &a, cudaStream_t s, int *clusters) {
   ProfScope prof(RC_STAGE_L12, s);
   if (tf) {
-    if (KZ == 16) return launch_t<16, true>(maps, a, s);
-    if (KZ == 32) return launch_t<32, true>(maps, a, s);
+    if (KZ == 16) return launch_t<16, true>(maps, a, s, clusters);
+    if (KZ == 32) return launch_t<32, true>(maps, a, s, clusters);
     return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel (tf32): K = %d", KZ);
   }
-  if (KZ == 16) return launch_t<16, false>(maps, a, s);
-  if (KZ == 32) return launch_t<32, false>(maps, a, s);
+  if (KZ == 16) return launch_t<16, false>(maps, a, s, clusters);
+  if (KZ == 32) return launch_t<32, false>(maps, a, s, clusters);
   return rc_fail(RC_EUNSUPPORTED, "fused layer-1/2 kernel: K = %d", KZ);
 }

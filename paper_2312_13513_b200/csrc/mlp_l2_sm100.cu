@@ -69,6 +69,17 @@ __device__ __forceinline__ float2 f16x2_to_f2(uint32_t v) {
   return make_float2(lo, hi);
 }
 
+// tile queue: the pair leader's TMA thread decides the pair's next tile (static
+// schedule, or an atomic counter shared with other launches) and publishes it into both CTAs.
+// Readers per slot: rank 0's MMA warp and rank 1's TMA thread; each CTA's TMA thread hands the tile
+// to its epilogue warps with the tile's bias slice (sTile[zb], published by the bfull barrier), so the
+// register-bound epilogue warps carry no queue state.
+// The leader publishes TQ_AHEAD tiles past the one its TMA thread loads, so rank 1's TMA thread never
+// waits for a tile index at a tile boundary (publishing at the boundary cost ~1 us per tile).
+constexpr int TQD = 8, TQ_READERS = 2, TQ_AHEAD = 1;
+// [0] tiles run by filler launches, [1] filler pairs that gave up at the gate, [2] filler pairs that ran
+__device__ unsigned long long g_l2_overlap[3];
+
 #ifdef L2TRACE  // timing experiment: per-tile clock64 stamps of cluster 0 (tools/l2trace.py)
 constexpr int TR_TILES = 40;
 __device__ long long g_l2trace[2][20][TR_TILES][4];  // [DOT][warp][tile][event]
@@ -122,6 +133,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
   uint64_t *full = bar, *empty = full + S, *c2full = empty + S, *c2empty = c2full + 1, *c2emptyB = c2empty + 1,
            *bfull = c2emptyB + 1, *bempty = bfull + 2, *bkfull = bempty + 2, *bkempty = bkfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bkempty + 2);
+  uint64_t *tqfull = bkempty + 3, *tqempty = tqfull + TQD;  // (bkempty + 2 holds the TMEM address)
+  int *tq = reinterpret_cast<int *>(tqempty + TQD);
+  int *sTile = tq + TQD;  // [2]: the tile of bias slice zb, for the epilogue warps
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = rcx::cluster_rank();
@@ -151,6 +165,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
       rcx::mbar_init(&bkfull[z], 2);
       rcx::mbar_init(&bkempty[z], 1);
     }
+    for (int d = 0; d < TQD; ++d) {
+      rcx::mbar_init(&tqfull[d], 1);
+      rcx::mbar_init(&tqempty[d], TQ_READERS);  // used in the leader only
+    }
     rcx::fence_mbar_init();
   }
   if (BFOLD) {
@@ -166,6 +184,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
   const int pairs = a.m_tiles / 2;
   const int total = a.nets * pairs * a.passes;
   const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const uint32_t tqempty0 = rcx::map_cta(tqempty, 0);
+  // reader side: the pair's it-th tile (>= total: none left); `warp_reader`: the whole warp reads,
+  // then one lane reports the slot read.  Rank 0's readers see their own CTA's writer (CTA-scope
+  // acquire, local arrive); rank 1's slot is written from rank 0 (cluster-scope acquire).  The
+  // read-done arrivals need no release: the slot is rewritten only TQD tiles later.
+  // rank 1's slot arrives by st.async with completion on its tqfull (no release fence in the leader's
+  // TMA thread: a cluster-scope release there waited for the thread's outstanding TMA loads)
+  auto tq_take = [&](int it, bool warp_reader) -> int {
+    const int d = it % TQD;
+    rcx::mbar_wait(&tqfull[d], (uint32_t)(it / TQD) & 1);
+    const int t = rcx::ld_shared_s32(&tq[d]);
+    if (warp_reader) __syncwarp();
+    if (!warp_reader || lane == 0) {
+      if (leader) rcx::mbar_arrive(&tqempty[d]);
+      else rcx::mbar_arrive_relaxed_cluster(tqempty0 + d * 8);
+    }
+    return t;
+  };
 
   if (warp == W_TMA) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer (both CTAs)
@@ -173,11 +209,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
-      for (int tile = cl; tile < total; tile += ncl, ++it) {
-        const int pass = tile % a.passes, rest = tile / a.passes;
-        const int mp = rest % pairs, net = rest / pairs;
+      // leader: the next tile, decided a tile ahead (the counter's atomic latency hides behind a
+      // tile's loads).  A filler waits at the gate first and takes nothing if it stays closed.
+      int t_next = cl, n_done = 0, pub = 0;
+      bool pub_end = false;
+      if (leader && a.tile_ctr) {
+        bool go = true;
+        if (a.gate) {
+          const uint64_t t0 = rcx::global_ns();
+          while (rcx::ld_acquire_gpu(a.gate) < a.gate_target)
+            if (rcx::global_ns() - t0 > a.gate_ns) {
+              go = false;
+              break;
+            }
+          atomicAdd(&g_l2_overlap[go ? 2 : 1], 1ull);
+        }
+        t_next = go ? atomicAdd(a.tile_ctr, 1) : total;
+      }
+      for (;; ++it) {
+        int tile;
+        if (leader) {  // publish up to TQ_AHEAD tiles ahead into both CTAs' queue slots
+          for (; pub <= it + TQ_AHEAD && !pub_end; ++pub) {
+            const int tp = t_next < total ? t_next : total, d = pub % TQD;
+            rcx::mbar_wait(&tqempty[d], ((uint32_t)(pub / TQD) & 1) ^ 1);
+            *reinterpret_cast<volatile int *>(&tq[d]) = tp;
+            rcx::mbar_arrive(&tqfull[d]);
+            const uint32_t rbar = rcx::map_cta(&tqfull[d], 1);
+            rcx::mbar_arrive_expect_tx_relaxed_cluster(rbar, 4);
+            rcx::st_async_u32(rcx::map_cta(&tq[d], 1), (uint32_t)tp, rbar);
+            if (tp >= total) pub_end = true;
+            else t_next = a.tile_ctr ? atomicAdd(a.tile_ctr, 1) : tp + ncl;
+          }
+          // (slot it is not rewritten before this read: that needs pub = it + TQD)
+          tile = *reinterpret_cast<volatile int *>(&tq[it % TQD]);
+          if (tile < total) ++n_done;
+        } else {
+          tile = tq_take(it, false);
+        }
         const int zb = it & 1;
         rcx::mbar_wait_sleep(&bempty[zb], ((it >> 1) & 1) ^ 1);  // b2 slice for this CTA's drain
+        *reinterpret_cast<volatile int *>(&sTile[zb]) = tile;
+        if (tile >= total) {  // tell the epilogue warps: no more tiles
+          rcx::mbar_arrive(&bfull[zb]);
+          break;
+        }
+        const int pass = tile % a.passes, rest = tile / a.passes;
+        const int mp = rest % pairs, net = rest / pairs;
         rcx::mbar_arrive_expect_tx(&bfull[zb], VEC * 4);
         rcx::bulk_g2s(sB2 + zb * VEC, a.bias + (size_t)net * a.N + pass * NP, NP * 4, &bfull[zb]);
         if (DOT) rcx::bulk_g2s(sB2 + zb * VEC + NP, a.w4 + (size_t)net * a.N + pass * NP, NP * 4, &bfull[zb]);
@@ -205,6 +282,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
           if (++s == S) { s = 0; ph ^= 1; }
         }
       }
+      if (leader && a.gate && n_done) atomicAdd(&g_l2_overlap[0], (unsigned long long)n_done);
     }
   } else if (warp == W_MMA) {
     if (leader) {  // ------------- MMA issuer (even CTA; converged warp, one elected lane issues)
@@ -212,8 +290,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
       constexpr uint32_t idp2 = rcx::make_idesc(E::FMT, 256, P2 > 0 ? P2 : 16);
       int s = 0;
       uint32_t ph = 0;
-      int it = 0;
-      for (int tile = cl; tile < total; tile += ncl, ++it) {
+      for (int it = 0;; ++it) {
+        if (tq_take(it, true) >= total) break;
         TRACE(W_MMA, it, 0);
         if (!BFOLD) {
           rcx::mbar_wait(c2empty, (it & 1) ^ 1);  // previous tile drained
@@ -332,8 +410,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
       }
     };
     uint32_t nst = 0;
-    int it = 0;
-    for (int tile = cl; tile < total; tile += ncl, ++it) {
+    for (int it = 0;; ++it) {
+      rcx::mbar_wait_sleep(&bfull[it & 1], (it >> 1) & 1);  // this tile's bias slice and index
+      const int tile = *reinterpret_cast<volatile int *>(&sTile[it & 1]);
+      if (tile >= total) break;
       const int pass = tile % a.passes, rest = tile / a.passes;
       const int mp = rest % pairs, net = rest / pairs;
       TRACE(warp, it, 0);
@@ -343,7 +423,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
       rcx::mbar_wait_sleep(c2full, it & 1);  // parked for the whole mainloop: leave issue slots and power to the rest
 #endif
       TRACE(warp, it, 1);
-      rcx::mbar_wait(&bfull[it & 1], (it >> 1) & 1);
       rcx::tc_fence_after();
       const float *b2 = sB2 + (it & 1) * VEC;
       const int grow = mp * 256 + rank * 128 + q * 32;  // first global row of this warp's 32 rows
@@ -518,7 +597,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
 }
 
 template <int NP, bool DOT, int PREC>
-int launch_l2_pair_t(const CUtensorMap *M, L2Args a, cudaStream_t s) {
+int launch_l2_pair_t(const CUtensorMap *M, L2Args a, cudaStream_t s, int pairs) {
   constexpr int RB = row_bytes<PREC>();
   constexpr size_t STAGE = (rcm::Prec<PREC>::NOP * (128 * RB + (NP / 2) * RB) + 1023) & ~(size_t)1023;
   constexpr size_t BK = PREC == 0 ? 2 * ((((size_t)NP / 2) * 32 + 1023) & ~(size_t)1023) + 4096 : 0;  // b operand + ones
@@ -550,7 +629,7 @@ int launch_l2_pair_t(const CUtensorMap *M, L2Args a, cudaStream_t s) {
       resident = mlp_num_sms() / 2;
   }
   const int total = a.nets * (a.m_tiles / 2) * a.passes;
-  int clusters = resident;
+  int clusters = pairs > 0 ? pairs : resident;
   if (clusters > total) clusters = total;
   l2_pair_kernel<NP, DOT, PREC><<<2 * clusters, L2_THREADS, smem, s>>>(M[0], M[1], M[2], M[3], M[4], M[5], M[6], M[7], M[8], M[9], a);
   RC_LAUNCH_CHECK();
@@ -576,11 +655,22 @@ int l2_pass_width(int h) {
   return 0;
 }
 
-int launch_l2_pair(int NP, int prec, const CUtensorMap *maps, const L2Args &a, cudaStream_t s) {
+int l2_overlap_read(long long *out, int reset) {
+  unsigned long long v[3];
+  if (cudaMemcpyFromSymbol(v, g_l2_overlap, sizeof(v)) != cudaSuccess) return rc_fail(RC_ECUDA, "rc_overlap_read");
+  for (int i = 0; i < 3; ++i) out[i] = (long long)v[i];
+  if (reset) {
+    const unsigned long long z[3] = {0, 0, 0};
+    if (cudaMemcpyToSymbol(g_l2_overlap, z, sizeof(z)) != cudaSuccess) return rc_fail(RC_ECUDA, "rc_overlap_read");
+  }
+  return RC_OK;
+}
+
+int launch_l2_pair(int NP, int prec, const CUtensorMap *maps, const L2Args &a, cudaStream_t s, int pairs) {
   ProfScope prof(a.prof_stage >= 0 ? a.prof_stage : a.w4 ? RC_STAGE_L3 : RC_STAGE_L2, s);
 #define RC_L2P_PREC(np, dot)                                                                                \
-  return prec == 0 ? launch_l2_pair_t<np, dot, 0>(maps, a, s)                                               \
-                   : prec == 1 ? launch_l2_pair_t<np, dot, 1>(maps, a, s) : launch_l2_pair_t<np, dot, 2>(maps, a, s);
+  return prec == 0 ? launch_l2_pair_t<np, dot, 0>(maps, a, s, pairs)                                        \
+                   : prec == 1 ? launch_l2_pair_t<np, dot, 1>(maps, a, s, pairs) : launch_l2_pair_t<np, dot, 2>(maps, a, s, pairs);
 #define RC_L2P(np)                     \
   if (NP == np) {                      \
     if (a.w4) RC_L2P_PREC(np, true)    \

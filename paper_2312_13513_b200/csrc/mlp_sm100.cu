@@ -627,8 +627,9 @@ int mlp_num_sms() { return rc_sm_count(); }
 namespace {
 
 struct WsLayout {
-  size_t z, h1, h2, h3, opart, qpart, total;
+  size_t z, h1, h2, h2b, h3, opart, qpart, sched, total;
   int cap;
+  int64_t nchunks;
 };
 
 // z (the layer-1 A operand) is held for all `ncells` cells (one prologue launch per call; 32 B per
@@ -637,6 +638,11 @@ struct WsLayout {
 bool fused_path(const rc_mlp *n) {
   return (n->precision == RC_BF16 || n->precision == RC_TF32) &&
          l12_supported(n->h1, n->h2, n->kpad1, n->precision == RC_TF32) && !(n->flags & RC_MLP_LAYERWISE);
+}
+// layer 3 of chunk j - 1 overlapped with the fused layer-1/2 kernel of chunk j: a
+// second h2 buffer and per-chunk tile counters; RC_MLP_SERIAL keeps the one-stream order
+bool overlap_path(const rc_mlp *n) {
+  return fused_path(n) && !(n->flags & (RC_MLP_SHARED | RC_MLP_SERIAL));
 }
 
 WsLayout ws_layout(const rc_mlp *n, int cap, int64_t ncells) {
@@ -651,6 +657,10 @@ WsLayout ws_layout(const rc_mlp *n, int cap, int64_t ncells) {
   L.z = o; o = al(o + nc * zrows * n->kpad1 * eb);
   L.h1 = o; o = al(o + (fused_path(n) ? 0 : nc * (size_t)n->gnets * cap * n->h1 * eb));
   L.h2 = o; o = al(o + nc * (size_t)n->gnets * cap * n->h2 * eb);
+  L.nchunks = (ncells + cap - 1) / cap;
+  const bool ov = overlap_path(n) && L.nchunks >= 2;
+  L.h2b = o; o = al(o + (ov ? (size_t)n->gnets * cap * n->h2 * eb : 0));  // h2 of the odd chunks
+  L.sched = o; o = al(o + (ov ? (size_t)L.nchunks * 2 * 4 : 0));         // tile counters, cluster counts
   const bool shared = (n->flags & RC_MLP_SHARED) != 0;
   L.h3 = o; o = al(o + (shared ? (size_t)cap * n->h3 * eb : 0));  // shared net: h3 for the layer-4 kernel
   const int np3 = shared ? 1 : n->h3 / l2_pass_width(n->h3);  // raw outputs per row: one per layer-3 pass
@@ -693,15 +703,50 @@ int launch_combine_reductions(const double *rp, const int64_t *dp, int k, double
   return RC_OK;
 }
 
+// The auxiliary stream of the layer-3 overlap and its events, one set per host thread (a thread
+// enqueues its calls in order, so reusing them across calls never orders one call after a record of
+// another): `go` marks the point where the fused kernel of chunk j is enqueued, fill[j % 2] the end of
+// chunk j's filler launch.
+struct AuxStreams {
+  int device = -1;
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t go = nullptr, fill[2] = {nullptr, nullptr};
+};
+AuxStreams *aux_streams() {
+  thread_local AuxStreams a;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  if (a.device != dev) {  // (a thread that switches devices gets a new set; the old one is not reclaimed)
+    AuxStreams b;
+    b.device = dev;
+    if (cudaStreamCreateWithFlags(&b.s2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&b.go, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&b.fill[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&b.fill[1], cudaEventDisableTiming) != cudaSuccess)
+      return nullptr;
+    a = b;
+  }
+  return &a;
+}
+
 int cap_limit(const rc_mlp *n) { return n->precision == RC_TF32X3 ? std::min(MAX_CAP, 32768) : MAX_CAP; }
 
 size_t chem_workspace_min_bytes(const rc_mlp *n, int64_t ncells) { return ws_layout(n, 256, ncells).total; }
 
-size_t chem_workspace_bytes(const rc_mech *, const rc_mlp *n, int64_t ncells) {
-  int64_t cap = (ncells + 255) / 256 * 256;  // chunks of CTA-pair (256-row) tiles
+// chunk capacity for a call of ncells cells: chunks of CTA-pair (256-row) tiles, at most cap_limit;
+// with the layer-3 overlap a call that would be one chunk runs as two halves (from OVERLAP_SPLIT_MIN
+// cells), so layer 3 of the first half runs beside the fused kernel of the second
+constexpr int64_t OVERLAP_SPLIT_MIN = 65536;
+int chunk_cap(const rc_mlp *n, int64_t ncells) {
+  int64_t cap = (ncells + 255) / 256 * 256;
   if (cap > cap_limit(n)) cap = cap_limit(n);
+  if (overlap_path(n) && ncells >= OVERLAP_SPLIT_MIN && ncells <= cap) cap = ((ncells + 1) / 2 + 255) / 256 * 256;
   if (cap < 256) cap = 256;
-  return ws_layout(n, (int)cap, ncells).total;
+  return (int)cap;
+}
+
+size_t chem_workspace_bytes(const rc_mech *, const rc_mlp *n, int64_t ncells) {
+  return ws_layout(n, chunk_cap(n, ncells), ncells).total;
 }
 
 int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
@@ -887,7 +932,7 @@ int launch_epilogue(const rc_mech *m, const rc_mlp *n, const EpiArgs &ea, const 
 int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, size_t ws_bytes, cudaStream_t s) {
   if (c.n == 0) return RC_OK;
   // chunk capacity: largest multiple of 128 (<= MAX_CAP, <= n rounded up) whose layout fits the workspace
-  int cap = (int)std::min<int64_t>((c.n + 255) / 256 * 256, cap_limit(n));
+  int cap = chunk_cap(n, c.n);
   while (cap > 256 && ws_layout(n, cap, c.n).total > ws_bytes) cap -= 256;
   WsLayout L = ws_layout(n, cap, c.n);
   if (L.total > ws_bytes) return rc_fail(RC_EINVAL, "workspace too small (%zu < %zu)", ws_bytes, L.total);
@@ -901,6 +946,7 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   const bool shared = (n->flags & RC_MLP_SHARED) != 0;
   // activations: hi copy at the start of each region, X3's lo copy right after it
   uint8_t *z = w + L.z, *h1 = w + L.h1, *h2 = w + L.h2;
+  const bool overlap = overlap_path(n) && L.nchunks >= 2;
   const int64_t zrows = (c.n + 255) / 256 * 256;  // z holds every cell of the call
   const size_t zlo = (size_t)zrows * n->kpad1 * EB, h1lo = (size_t)nets * cap * n->h1 * EB,
                h2lo = (size_t)nets * cap * n->h2 * EB;
@@ -965,6 +1011,20 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
     m2[8] = m2[9] = m2[0];
     m3[8] = m3[9] = m3[0];
   }
+  // overlap: the odd chunks' h2 buffer (fused kernel's store map, layer 3's A map; never X3)
+  CUtensorMap m12b[7], m3b[10];
+  AuxStreams *aux = nullptr;
+  int *sched = reinterpret_cast<int *>(w + L.sched);  // [nchunks] layer-3 tile counters | [nchunks] resident clusters
+  if (overlap) {
+    for (int k = 0; k < 7; ++k) m12b[k] = m12[k];
+    for (int k = 0; k < 10; ++k) m3b[k] = m3[k];
+    if ((rc = make_map(&m12b[4], w + L.h2b, n->h2, cap, nets, 32, 16, EB)) ||
+        (rc = make_map(&m3b[0], w + L.h2b, n->h2, cap, nets, BM, KC, EB)))
+      return rc;
+    m3b[4] = m3b[0];
+    if (!(aux = aux_streams())) return rc_fail(RC_ECUDA, "layer-3 overlap: auxiliary stream");
+    RC_CUDA_TRY(cudaMemsetAsync(sched, 0, (size_t)L.nchunks * 2 * 4, s));
+  }
   RC_CUDA_TRY(cudaMemsetAsync(qpart, 0, QPART_BLOCKS * 8, s));
   int64_t launches = 1;
   {  // a3 for every cell of the call in one launch (HBM-bound: per-chunk launches were tail-dominated)
@@ -987,7 +1047,15 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
       launch_pro(std::integral_constant<int, 128>{});
     RC_LAUNCH_CHECK();
   }
-  for (int64_t c0 = 0; c0 < c.n; c0 += cap) {
+  // overlap: layer 3 of chunk j - 1 is launched after the fused kernel of chunk j, in two launches
+  // sharing one tile counter: a filler on the auxiliary stream that runs on the SMs the fused
+  // kernel's 4-CTA clusters leave idle (it takes tiles only once every cluster is resident), and
+  // the main launch on `s` once the fused kernel is done.  h2 alternates between two buffers.
+  int fill_pairs = 0;
+  L2Args pend{};
+  bool have_pend = false;
+  int j = 0;
+  for (int64_t c0 = 0; c0 < c.n; c0 += cap, ++j) {
     const int rows = (int)std::min<int64_t>(cap, c.n - c0);
     const int mt = (rows + 2 * BM - 1) / (2 * BM) * 2;  // even: CTA pairs of 128-row tiles
     if (c0 > 0) {  // this chunk's rows of z: re-point the layer-1 A operand maps
@@ -998,10 +1066,18 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
       if (!x3) m1[3] = m1[0];
       if (fused && (rc = make_map(&m12[0], zc, KZ, zr, 1, BM, KZ, EB))) return rc;
     }
+    const bool odd = overlap && (j & 1);
+    if (odd) m12b[0] = m12[0];
+    int ncl12 = 0;
     if (fused) {
+      if (overlap && j >= 2 && fill_pairs > 0)  // this chunk's h2 buffer: chunk j - 2's filler is done with it
+        RC_CUDA_TRY(cudaStreamWaitEvent(s, aux->fill[j & 1], 0));
+      if (overlap && j >= 1) RC_CUDA_TRY(cudaEventRecord(aux->go, s));  // chunk j - 1's h2 is complete here
       // layers 1+2 in one kernel: h1 stays on chip; clusters of two CTA pairs share h1 chunks
       L12Args g12{mt, nets, n->h1 / (tf32 ? 32 : 64), n->h2, 0, n->d_b2};
-      if ((rc = launch_l12(KZ, tf32, m12, g12, s))) return rc;
+      if (overlap) g12.started = sched + L.nchunks + j;
+      if ((rc = launch_l12(KZ, tf32, odd ? m12b : m12, g12, s, &ncl12))) return rc;
+      if (overlap && j == 0) fill_pairs = (rc_sm_count() - 4 * ncl12) / 2;
     } else {
       // layer 1: h1 = GELU(z W1^T) (b1 folded into z's constant-1 columns)
       L1Args g1{mt, (n->h1 + bn1 - 1) / bn1, nets, n->h1, 0, cap};
@@ -1013,7 +1089,25 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
     // layer 3 + folded layer 4: the same CTA-pair GEMM with the dot epilogue (K = h2, zero-filled to KC);
     // the raw outputs land in the all-cells array o [nets][passes][zrows] at this chunk's rows
     float *oc = opart + c0;
-    if (!shared) {
+    if (overlap) {
+      if (have_pend) {  // layer 3 of chunk j - 1 (h2 buffer (j - 1) % 2)
+        const CUtensorMap *mp3 = (j - 1) & 1 ? m3b : m3;
+        if (fill_pairs > 0) {
+          RC_CUDA_TRY(cudaStreamWaitEvent(aux->s2, aux->go, 0));
+          L2Args f = pend;
+          f.gate = sched + L.nchunks + j;
+          f.gate_target = ncl12;
+          f.gate_ns = 50000;  // 50 us: a cluster of the fused kernel this launch kept out starts that late
+          f.prof_stage = RC_STAGE_L3_FILL;
+          if ((rc = launch_l2_pair(NP3, prec, mp3, f, aux->s2, fill_pairs))) return rc;
+          RC_CUDA_TRY(cudaEventRecord(aux->fill[(j - 1) & 1], aux->s2));
+        }
+        if ((rc = launch_l2_pair(NP3, prec, mp3, pend, s))) return rc;
+      }
+      pend = L2Args{mt, n->h3 / NP3, nets, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, n->d_w4, oc, (int)zrows, (n->h2 % KC) / KATOM};
+      pend.tile_ctr = sched + j;
+      have_pend = true;
+    } else if (!shared) {
       L2Args l3{mt, n->h3 / NP3, nets, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, n->d_w4, oc, (int)zrows, (n->h2 % KC) / KATOM};
       if ((rc = launch_l2_pair(NP3, prec, m3, l3, s))) return rc;
     } else {
@@ -1024,6 +1118,10 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
       if ((rc = launch_l4(n, w + L.h3, oc, rows, (int)zrows, tf32, s))) return rc;
     }
     launches += 4;
+  }
+  if (overlap) {  // the last chunk's layer 3 (nothing left to overlap it with), then join the fillers
+    if ((rc = launch_l2_pair(NP3, prec, (j - 1) & 1 ? m3b : m3, pend, s))) return rc;
+    if (fill_pairs > 0) RC_CUDA_TRY(cudaStreamWaitEvent(s, aux->fill[j & 1], 0));
   }
   {  // a5 once over every cell of the call (one streaming pass, like the prologue)
     EpiArgs ea{0, (int)c.n, (int)zrows, nout, shared ? 1 : n->h3 / NP3, n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt,

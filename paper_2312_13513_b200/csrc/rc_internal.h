@@ -90,6 +90,8 @@ int rc_fail(int code, const char *fmt, ...);
 // SMs of the current device, and the resident CTAs of `kernel` at (threads, dynamic smem) over the
 // whole device (occupancy x SMs; persistent grids are sized with it).  Cached per device/kernel/config.
 int rc_sm_count();
+// layer-3 overlap counters (mlp_l2_sm100.cu; rc_overlap_read)
+int l2_overlap_read(long long *out, int reset);
 int rc_resident_blocks(const void *kernel, int threads, size_t smem);
 void rc_count_launch(int n = 1);
 void rc_reset_launches();

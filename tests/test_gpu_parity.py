@@ -472,3 +472,66 @@ def test_cuda_graph_capture_replays_rc_step_bitwise():
     out = st.host()
     for k in ("T", "cp", "rho", "mu", "lam", "D", "wdot", "qdot", "o", "red", "diag"):
         assert np.array_equal(out[k], ref[k]), k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", [0, 1])
+def test_layer3_overlap_bitwise_equals_serial(prec):
+    """Layer 3 of chunk j - 1 overlapped with the fused layer-1/2 kernel of chunk j (DESIGN.md 6.4:
+    side launches on the SMs the fused kernel's 4-CTA clusters leave idle, tiles from a shared
+    counter, h2 in two alternating buffers) gives bitwise the one-stream result (RC_MLP_SERIAL) on a
+    three-chunk call with a ragged last chunk; the side launches ran (rc_overlap_read)."""
+    import paper_2312_13513_b200 as rc
+    n = 2 * 262144 + 75_008
+    c = inputs("C2", begin=0, end=n)
+    G = Gpu("C2", precision=prec)
+    rc.rc_overlap_read(reset=True)
+    ov = G.run(c)
+    cnt = rc.rc_overlap_read(reset=True)
+    print(f"\n  overlap counters (precision {prec}): {cnt}")
+    assert cnt["pairs_ran"] + cnt["pairs_gave_up"] > 0  # two side launches were made
+    G.mlp = rc.MLPBundle(G.mech, bundle("h2_9sp", CONFIGS["C2"].hidden), prec, flags=rc.RC_MLP_SERIAL)
+    se = G.run(c)
+    assert rc.rc_overlap_read(reset=True)["pairs_ran"] == 0
+    for k in ("T", "cp", "rho", "mu", "lambda", "qdot", "D", "wdot", "o", "red", "diag"):
+        assert np.array_equal(ov[k], se[k]), k
+    # and against the oracle on a hashed sample of the three chunks
+    idx = np.unique(np.random.default_rng(7).integers(0, n, 96))
+    cs = inputs("C2", idx=idx)
+    ref = run_oracle("C2", cs, nthreads=0)
+    assert rel_fro(ov["o"][:, idx], ref["o"]) <= (BF16_TOL if prec == 0 else TF32_TOL)
+
+
+@pytest.mark.gpu
+def test_cuda_graph_capture_with_layer3_overlap():
+    """rc_step with the layer-3 overlap (auxiliary stream forked and joined by events inside the call)
+    captured into a CUDA graph replays bitwise the eager result."""
+    import torch
+
+    import paper_2312_13513_b200 as rc
+    n = 262144 + 40_000
+    c = inputs("C2", begin=0, end=n)
+    G = Gpu("C2")
+    st = rc.CellState(n, G.ns, G.n_nets)
+    st.load(c["T_guess"], c["p"], c["Y"], h=c["h"])
+    ws = rc.aligned_workspace(G.mlp, n)
+    cells = st.cells(rc.RC_MODE_H, dt=G.dt)
+    T0 = st.T.clone()
+    rc.rc_step(G.mech, G.mlp, cells, ws)
+    torch.cuda.synchronize()
+    ref = st.host()
+    st.T.copy_(T0)
+    for t in (st.cp, st.rho, st.mu, st.lam, st.D, st.wdot, st.qdot, st.o):
+        t.zero_()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=side):
+        rc.rc_step(G.mech, G.mlp, cells, ws, side)
+    for _ in range(2):
+        st.T.copy_(T0)
+        graph.replay()
+    torch.cuda.synchronize()
+    out = st.host()
+    for k in ("T", "cp", "rho", "mu", "lam", "D", "wdot", "qdot", "o", "red", "diag"):
+        assert np.array_equal(out[k], ref[k]), k
