@@ -474,6 +474,14 @@ def run_ours(a):
                                        + ("" if a.precision == "bf16" else f" x {tratio:.3f} ({a.precision}, nominal ratio)"),
                         "work_per_launch": ("2*cells_chunk*(d_in*1600 + 1600*800)*nets FLOP" if fused
                                             else "2*cells_chunk*1600*800*nets FLOP")}
+            # the step is power-capped: the SM clock it ran at against the one the sustained peak was
+            # measured at (MEASURED_PEAKS clocks_under_load); frac x peak_mhz / sm_mhz is the fraction
+            # per clock cycle
+            pmhz = (pk.get("clocks_under_load") or {}).get("sm_mhz_median")
+            cs = clk.summary()
+            if pmhz and cs.get("sm_mhz") and roofline.get("frac"):
+                roofline.update({"sm_mhz": cs["sm_mhz"], "peak_sm_mhz": pmhz,
+                                 "frac_per_clock": round(roofline["frac"] * pmhz / cs["sm_mhz"], 4)})
         out = {
             "metric": ("Mcells/s per thermo+transport+DNN-chem step" if a.chem == "dnn"
                        else "Mcells/s per thermo+transport+detailed-kinetics step (NEXT-3)"),

@@ -257,6 +257,7 @@ extern "C" int rc_mech_create(const rc_mech_desc *d, rc_mech **out) {
       EF[a * ns + k] = f;
       EF[(ne + a) * ns + k] = E[a * ns + k];
     }
+  m->EF_host = EF;
   if (cudaMalloc(&m->d_EF, EF.size() * 8) != cudaSuccess ||
       cudaMemcpy(m->d_EF, EF.data(), EF.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
     rc_mech_destroy(m);

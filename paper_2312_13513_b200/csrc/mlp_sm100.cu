@@ -51,6 +51,7 @@ struct ProArgs {
   void *z;  // [cap][kz] bf16 (or tf32-rounded fp32): z-scored inputs, two 1.0 columns (b1 hi/lo), zeros
   int tf32;         // 0 bf16, 1 tf32, 2 tf32 hi at z and tf32 lo at z + lo_off
   int64_t lo_off;   // elements
+  float xm[32], xs[32];  // z-score constants (d_in <= 30) as kernel-parameter (constant-bank) operands
 };
 
 // cells per stage = consumer threads (+ the producer warp, stream.cuh run_ws).  256-cell tiles for
@@ -90,20 +91,20 @@ __device__ __forceinline__ void store_z_row(const ProArgs &a, int64_t r, const f
 }
 
 // a3 for every cell of the call: T, p, Y streamed through the TMA tile ring (stream.cuh), one
-// thread per cell writes its z row; rows [rows, rows_pad) of the 256-row tiles are zero
-template <int PRO_TILE>
-__global__ void __launch_bounds__(pro_threads<PRO_TILE>()) prologue_kernel(ProArgs a, CellsDev c, int stages) {
+// thread per cell writes its z row; rows [rows, rows_pad) of the 256-row tiles are zero.
+// NS > 0: the species count of a compiled mechanism (loops without runtime bounds); 0: generic
+template <int PRO_TILE, int NS>
+__global__ void __launch_bounds__(pro_threads<PRO_TILE>()) prologue_kernel(const __grid_constant__ ProArgs a, CellsDev c,
+                                                                          int stages) {
   constexpr int PRO_THREADS = pro_threads<PRO_TILE>();
+  constexpr int CAP = NS ? NS : 30;
+  const int ns = NS ? NS : a.ns;
   extern __shared__ __align__(16) uint8_t pro_smem[];
   __shared__ __align__(8) uint64_t bars[16];
-  __shared__ float s_xm[32], s_xs[32];  // z-score constants (d_in <= 30)
-  const rcs::Ring<PRO_TILE> ring{pro_smem, bars, 2 + a.ns, 0, stages};
+  const rcs::Ring<PRO_TILE> ring{pro_smem, bars, 2 + ns, 0, stages};
   if (threadIdx.x == 0) ring.init(PRO_TILE / 32);
-  if (threadIdx.x < 32) {
-    s_xm[threadIdx.x] = threadIdx.x < a.d_in ? a.xmean[threadIdx.x] : 0.f;
-    s_xs[threadIdx.x] = threadIdx.x < a.d_in ? a.xinvstd[threadIdx.x] : 0.f;
-  }
   __syncthreads();
+  const float *s_xm = a.xm, *s_xs = a.xs;
   auto src8 = [&](int r) -> const double * {
     return (r == 0 ? c.T : r == 1 ? c.p : c.Y + (size_t)(r - 2) * c.ld) + a.c0;
   };
@@ -118,18 +119,15 @@ __global__ void __launch_bounds__(pro_threads<PRO_TILE>()) prologue_kernel(ProAr
     x[0] = ((float)S8[0] - s_xm[0]) * s_xs[0];
     x[1] = ((float)S8[PRO_TILE] - s_xm[1]) * s_xs[1];
 #pragma unroll
-    for (int k = 0; k < 30; ++k)
-      if (k < a.ns) {
+    for (int k = 0; k < CAP; ++k)
+      if (k < ns) {
         float y = (float)S8[(2 + k) * PRO_TILE];
         y = y > 0.f ? y : 0.f;                                       // Y^ = max(Y, 0)
-        // Y^^lambda with the MUFU lg2/ex2 (relative error ~1e-7, far below the bf16/tf32 rounding of z)
-        float b = 0.f;
-        if (y > 0.f) {
-          float l2, e2;
-          asm("lg2.approx.f32 %0, %1;" : "=f"(l2) : "f"(y));
-          asm("ex2.approx.f32 %0, %1;" : "=f"(e2) : "f"(a.lambda * l2));
-          b = e2;
-        }
+        // Y^^lambda with the MUFU lg2/ex2 (relative error ~1e-7, far below the bf16/tf32 rounding of z);
+        // Y^ = 0: lg2 = -inf, ex2(-inf) = 0 (lambda > 0), so no branch
+        float l2, b;
+        asm("lg2.approx.f32 %0, %1;" : "=f"(l2) : "f"(y));
+        asm("ex2.approx.f32 %0, %1;" : "=f"(b) : "f"(a.lambda * l2));
         x[2 + k] = ((b - 1.f) * a.inv_lambda - s_xm[2 + k]) * s_xs[2 + k];  // Box-Cox, z-score
       }
 #pragma unroll
@@ -323,6 +321,33 @@ __device__ __forceinline__ double inv_boxcox_dy(double ys, double delta, const E
   return u <= -1.0 ? -ys : ys * (g * u);
 }
 
+// the factored path's per-mechanism constants as a kernel parameter: with the species loops unrolled
+// each is a compile-time offset into the constant bank, a DFMA operand with no shared-memory load
+constexpr int EPI_KN = 20, EPI_KE = 4;
+struct EpiConst {
+  double F[EPI_KE][EPI_KN];  // F = (E E^T)^-1 E, column of net i's species (= i)
+  double E[EPI_KE][EPI_KN];  // E, column k
+  double ym[EPI_KN], ys[EPI_KN];
+  float b4[EPI_KN];
+};
+
+// inverse Box-Cox increment with lambda = 1/10 for Y^ >= 1e-30 (the fast branch of inv_boxcox_dy,
+// checked once per cell by the caller)
+__device__ __forceinline__ double inv_boxcox_dy10(double ys, double delta, double lambda) {
+  float l2, e2;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"((float)ys));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e2) : "f"(-0.1f * l2));
+  double r = (double)e2;
+  const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+  r = fma(0.1 * r, fma(-ys, r8 * r2, 1.0), r);
+  const double u = (lambda * delta) * r;
+  constexpr double C10[10] = {10.0, 45.0, 120.0, 210.0, 252.0, 210.0, 120.0, 45.0, 10.0, 1.0};
+  double g = C10[9];
+#pragma unroll
+  for (int m = 8; m >= 0; --m) g = fma(g, u, C10[m]);
+  return u <= -1.0 ? -ys : ys * (g * u);
+}
+
 __device__ __forceinline__ double2 lds2_epi(const double *p) {
   double2 v;
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(rcx::smem_u32(p)));
@@ -342,7 +367,8 @@ template <int NS> constexpr int epi_min_ctas() { return NS == 0 ? 1 : NS == 20 ?
 // accumulated per net (NE FMAs instead of Ns) and dY kept in registers (the net loop is fully
 // unrolled, so dY_net has a static register).  NE == 0: the outer product with the columns of P.
 template <int NS, int NE>
-__global__ void __launch_bounds__(epi_tile<NS>() + 32, epi_min_ctas<NS>()) chem_epilogue_kernel(EpiArgs a, CellsDev c, int stages) {
+__global__ void __launch_bounds__(epi_tile<NS>() + 32, epi_min_ctas<NS>())
+    chem_epilogue_kernel(EpiArgs a, CellsDev c, int stages, const __grid_constant__ EpiConst K) {
   constexpr int EPI_TILE = epi_tile<NS>(), EPI_THREADS = EPI_TILE + 32;
   constexpr int CAP = NS ? NS : RC_MAX_NS;
   constexpr int UR = NS ? NS : 1;
@@ -422,27 +448,39 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, epi_min_ctas<NS>()) chem_
     };
     double v[CAP];
     if constexpr (NE > 0) {
-      double w[NE];
-#pragma unroll
-      for (int e = 0; e < NE; ++e) w[e] = 0.0;
+      // 1/lambda = 10 (checked at launch): Y^ >= 1e-30 takes the check-free inverse transform, a
+      // smaller or zero Y^ the general one (per net: zero mass fractions are common in the air
+      // and fuel streams); the constants come from K
 #pragma unroll
       for (int net = 0; net < CAP; ++net) {
         v[net] = 0.0;
-        if (net < nn) {  // one layer-3 pass (checked at launch): raw output row `net`
-          const float o = reinterpret_cast<const float *>(sB4)[net] + S4[net * EPI_TILE];
+        if (net < nn) {  // one layer-3 pass (checked at launch)
+          const float o = K.b4[net] + S4[net * EPI_TILE];
           if (c.o) c.o[net * c.ld + i] = o;
-          const double y = S8[(2 + net) * EPI_TILE];
-          const double dy = inv_boxcox_dy(y > 0.0 ? y : 0.0, (double)o * sYS[net] + sYM[net], a);
-          v[net] = dy;
-#pragma unroll
-          for (int e = 0; e < NE; ++e) w[e] = fma(sPn[net * NE + e], dy, w[e]);  // F dY
+          const double y = S8[(2 + net) * EPI_TILE], delta = (double)o * K.ys[net] + K.ym[net];
+          if (y >= 1e-30) {
+            v[net] = inv_boxcox_dy10(y, delta, a.lambda);
+          } else if (!(y > 0.0)) {  // Y^ = 0 (b = 0): dY = (lambda Delta)^10 if positive (as the general form)
+            const double l = a.lambda * delta, l2 = l * l, l4 = l2 * l2;
+            v[net] = l > 0.0 ? l2 * (l4 * l4) : 0.0;
+          } else {
+            v[net] = inv_boxcox_dy_general(y, delta, a);
+          }
         }
+      }
+      double w[NE];
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {  // F dY
+        w[e] = 0.0;
+#pragma unroll
+        for (int net = 0; net < CAP; ++net)
+          if (net < nn) w[e] = fma(K.F[e][net], v[net], w[e]);
       }
 #pragma unroll
       for (int k = 0; k < CAP; ++k) {  // v = dY - E^T (F dY)
         double t = 0.0;
 #pragma unroll
-        for (int e = 0; e < NE; ++e) t = fma(sPn[(nn + k) * NE + e], w[e], t);
+        for (int e = 0; e < NE; ++e) t = fma(K.E[e][k], w[e], t);
         v[k] -= t;
       }
     } else {
@@ -482,18 +520,22 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, epi_min_ctas<NS>()) chem_
     }
     double q = 0.0;
     bool neg = false, bad = false;
+    double *wp = c.wdot + i;
 #pragma unroll UR
     for (int k = 0; k < CAP; ++k)
       if (k < ns) {
         const double y = S8[(2 + k) * EPI_TILE];
         neg |= ((y > 0.0 ? y : 0.0) + v[k]) < 0.0;
         const double w = scale * v[k];
-        c.wdot[k * c.ld + i] = w;
+        *wp = w;
+        wp += c.ld;
         // NE > 0 runs only for a mechanism with one T_mid (checked at launch): one range per cell
         const double *h = NE > 0 ? (T <= s_tab[2] ? hlo : hhi) + 6 * k : (T <= tmid[k]) ? hlo + 6 * k : hhi + 6 * k;
         const double hk = fma(T, fma(T, fma(T, fma(T, fma(T, h[4], h[3]), h[2]), h[1]), h[0]), h[5]);
         q = fma(-hk, w, q);
-        bad |= !isfinite(w);
+        // (NE > 0: a non-finite w_k makes q non-finite -- inf or NaN times the finite h_k, or NaN
+        // from 0 x inf -- so the test of q below counts the cell)
+        if constexpr (NE == 0) bad |= !isfinite(w);
       }
     if (c.qdot) c.qdot[i] = q;
     bad |= !isfinite(q);
@@ -869,6 +911,11 @@ int mlp_upload(rc_mlp *n, const rc_mlp_desc *d) {
             up((void **)&n->d_xmean, xm.data(), xm.size() * 4) && up((void **)&n->d_xinvstd, xi.data(), xi.size() * 4) &&
             up((void **)&n->d_ymean, d->y_mean, nout * 8) && up((void **)&n->d_ystd, d->y_std, nout * 8) &&
             up((void **)&n->d_species, d->species_of_net, nout * 4);
+  n->b4_host = b4;
+  n->xmean_host = xm;
+  n->xinvstd_host = xi;
+  n->ymean_host.assign(d->y_mean, d->y_mean + nout);
+  n->ystd_host.assign(d->y_std, d->y_std + nout);
   if (ok && !tf32) ok = up(&n->d_b2k, B2k.data(), B2k.size() * 2) && up(&n->d_b3k, B3k.data(), B3k.size() * 2);
   if (ok && tf32 && !x3) ok = up(&n->d_b2k, B2f.data(), B2f.size() * 4);
   if (ok && x3)
@@ -886,7 +933,7 @@ double binom(int n, int m) {
 }
 
 template <int NS, int NE>
-int launch_epilogue_t(const rc_mech *m, const EpiArgs &ea, const CellsDev &c, cudaStream_t s) {
+int launch_epilogue_t(const rc_mech *m, const rc_mlp *n, const EpiArgs &ea, const CellsDev &c, cudaStream_t s) {
   const int ns = m->ns, nn = ea.n_nets;
   const int stages = epi_stages<NS>();
   const int pn = NE ? ((nn + ns) * NE + 1) & ~1 : nn * ((ns + 1) & ~1);
@@ -897,8 +944,21 @@ int launch_epilogue_t(const rc_mech *m, const EpiArgs &ea, const CellsDev &c, cu
   int64_t grid = rc_resident_blocks((const void *)chem_epilogue_kernel<NS, NE>, EPI_THREADS, smem);
   if (grid > ntiles) grid = ntiles;
   if (grid > QPART_BLOCKS) grid = QPART_BLOCKS;
+  EpiConst K{};
+  if (NE > 0) {  // (launch_epilogue checked n_nets <= EPI_KN, ne <= EPI_KE, ns <= EPI_KN)
+    for (int e = 0; e < m->ne; ++e)
+      for (int k = 0; k < ns; ++k) {
+        K.E[e][k] = m->EF_host[(m->ne + e) * ns + k];
+        if (k < nn) K.F[e][k] = m->EF_host[e * ns + k];
+      }
+    for (int q = 0; q < nn; ++q) {
+      K.b4[q] = n->b4_host[q];
+      K.ym[q] = n->ymean_host[q];
+      K.ys[q] = n->ystd_host[q];
+    }
+  }
   ProfScope prof(RC_STAGE_EPILOGUE, s);
-  chem_epilogue_kernel<NS, NE><<<(unsigned)grid, EPI_THREADS, smem, s>>>(ea, c, stages);
+  chem_epilogue_kernel<NS, NE><<<(unsigned)grid, EPI_THREADS, smem, s>>>(ea, c, stages, K);
   RC_LAUNCH_CHECK();
   return RC_OK;
 }
@@ -922,10 +982,11 @@ int launch_l4(const rc_mlp *n, const void *h3, float *o, int rows, int cap, bool
 int launch_epilogue(const rc_mech *m, const rc_mlp *n, const EpiArgs &ea, const CellsDev &c, cudaStream_t s) {
   // factored projection when net i predicts species i (checked at rc_mlp_create) and the element
   // count has an instance
-  const bool ident = n->species_identity && ea.passes == 1 && m->uniform_tmid;
-  if (m->ns == 9) return ident && m->ne == 3 ? launch_epilogue_t<9, 3>(m, ea, c, s) : launch_epilogue_t<9, 0>(m, ea, c, s);
-  if (m->ns == 20) return ident && m->ne == 4 ? launch_epilogue_t<20, 4>(m, ea, c, s) : launch_epilogue_t<20, 0>(m, ea, c, s);
-  return launch_epilogue_t<0, 0>(m, ea, c, s);
+  const bool ident = n->species_identity && ea.passes == 1 && m->uniform_tmid && n->inv_lambda == 10 &&
+                     n->n_nets <= EPI_KN;
+  if (m->ns == 9) return ident && m->ne == 3 ? launch_epilogue_t<9, 3>(m, n, ea, c, s) : launch_epilogue_t<9, 0>(m, n, ea, c, s);
+  if (m->ns == 20) return ident && m->ne == 4 ? launch_epilogue_t<20, 4>(m, n, ea, c, s) : launch_epilogue_t<20, 0>(m, n, ea, c, s);
+  return launch_epilogue_t<0, 0>(m, n, ea, c, s);
 }
 }  // namespace
 
@@ -1029,22 +1090,28 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   int64_t launches = 1;
   {  // a3 for every cell of the call in one launch (HBM-bound: per-chunk launches were tail-dominated)
     ProArgs pa{0, (int)c.n, (int)zrows, n->d_in, n->ns, KZ, (float)n->lambda_bc, (float)(1.0 / n->lambda_bc),
-               n->d_xmean, n->d_xinvstd, z, prec, (int64_t)(zlo / EB)};
+               n->d_xmean, n->d_xinvstd, z, prec, (int64_t)(zlo / EB), {}, {}};
+    for (int k = 0; k < n->d_in && k < 32; ++k) pa.xm[k] = n->xmean_host[k], pa.xs[k] = n->xinvstd_host[k];
     ProfScope prof(RC_STAGE_PROLOGUE, s);
-    auto launch_pro = [&](auto tile_c) {
-      constexpr int TILE = decltype(tile_c)::value;
+    auto launch_pro = [&](auto tile_c, auto ns_c) {
+      constexpr int TILE = decltype(tile_c)::value, NS = decltype(ns_c)::value;
       const int pstages = 3;
       const size_t psmem = rcs::Ring<TILE>::smem_bytes(2 + n->ns, 0, pstages);
-      int64_t pgrid = rc_resident_blocks((const void *)prologue_kernel<TILE>, pro_threads<TILE>(), psmem);
+      int64_t pgrid = rc_resident_blocks((const void *)prologue_kernel<TILE, NS>, pro_threads<TILE>(), psmem);
       const int64_t ptiles = (c.n + TILE - 1) / TILE;
       if (pgrid > ptiles) pgrid = ptiles;
       if (pgrid < 1) pgrid = 1;  // n == 0 cannot reach here; padding rows only would need one CTA
-      prologue_kernel<TILE><<<(unsigned)pgrid, pro_threads<TILE>(), psmem, s>>>(pa, c, pstages);
+      prologue_kernel<TILE, NS><<<(unsigned)pgrid, pro_threads<TILE>(), psmem, s>>>(pa, c, pstages);
     };
-    if (n->ns <= 12)
-      launch_pro(std::integral_constant<int, 256>{});
+    using I = std::integral_constant<int, 0>;
+    if (n->ns == 9)
+      launch_pro(std::integral_constant<int, 256>{}, std::integral_constant<int, 9>{});
+    else if (n->ns == 20)
+      launch_pro(std::integral_constant<int, 128>{}, std::integral_constant<int, 20>{});
+    else if (n->ns <= 12)
+      launch_pro(std::integral_constant<int, 256>{}, I{});
     else
-      launch_pro(std::integral_constant<int, 128>{});
+      launch_pro(std::integral_constant<int, 128>{}, I{});
     RC_LAUNCH_CHECK();
   }
   // overlap: layer 3 of chunk j - 1 is launched after the fused kernel of chunk j, in two launches

@@ -60,6 +60,7 @@ struct rc_mech {
   double *d_transport = nullptr;  // TransportSeg
   double *d_P = nullptr;          // [ns][ns] element projection (R6)
   double *d_EF = nullptr;         // [2][ne][ns]: F = (E E^T)^-1 E, then E (P = I - E^T F; low-rank epilogue)
+  std::vector<double> EF_host;    // the same on the host (the epilogue's kernel-parameter constants)
 };
 
 struct rc_mlp {
@@ -71,6 +72,9 @@ struct rc_mlp {
   int inv_lambda;                 // 1/lambda as an integer power
   std::vector<int> species_of_net;
   bool species_identity = false;  // species_of_net[i] == i for every output (the epilogue's factored projection)
+  std::vector<float> b4_host;              // [n_nets] (the epilogue's kernel-parameter constants)
+  std::vector<double> ymean_host, ystd_host;
+  std::vector<float> xmean_host, xinvstd_host;  // [d_in] (the prologue's kernel-parameter constants)
   // device buffers
   void *d_W1 = nullptr, *d_W2 = nullptr, *d_W3 = nullptr;   // [nets][N][K] bf16 or fp32(tf32-rounded)
   void *d_W1lo = nullptr, *d_W2lo = nullptr, *d_W3lo = nullptr;  // RC_TF32X3: tf32(W - W_hi)
