@@ -362,8 +362,9 @@ template <int NS> constexpr int epi_tile() { return NS == 20 ? 128 : 256; }
 template <int NS> constexpr int epi_stages() { return NS == 20 ? 2 : 3; }
 template <int NS> constexpr int epi_min_ctas() { return NS == 0 ? 1 : NS == 20 ? 3 : 2; }
 
-// NE > 0: net `net` predicts species `net` (the usual layout: the inert species last), layer 3 ran in
-// one pass (h3 = 400, the paper width), the mechanism has one T_mid and NE elements; the projection is then applied in factored form, v = dY - E^T (F dY), with F dY
+// NE > 0: net `net` predicts species `net` for the first Ns - 1 species (the inert species last),
+// layer 3 ran in one pass (h3 = 400, the paper width), 1/lambda = 10, the mechanism has one T_mid and
+// NE elements (all checked at launch); the projection is then applied in factored form, v = dY - E^T (F dY), with F dY
 // accumulated per net (NE FMAs instead of Ns) and dY kept in registers (the net loop is fully
 // unrolled, so dY_net has a static register).  NE == 0: the outer product with the columns of P.
 template <int NS, int NE>
@@ -451,12 +452,13 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, epi_min_ctas<NS>())
       // 1/lambda = 10 (checked at launch): Y^ >= 1e-30 takes the check-free inverse transform, a
       // smaller or zero Y^ the general one (per net: zero mass fractions are common in the air
       // and fuel streams); the constants come from K
+      // nets = species - 1, the inert species last (checked at launch): no runtime net bound
+      constexpr int NN = NE > 0 ? CAP - 1 : 0;
 #pragma unroll
       for (int net = 0; net < CAP; ++net) {
         v[net] = 0.0;
-        if (net < nn) {  // one layer-3 pass (checked at launch)
+        if (net < NN) {  // one layer-3 pass (checked at launch)
           const float o = K.b4[net] + S4[net * EPI_TILE];
-          if (c.o) c.o[net * c.ld + i] = o;
           const double y = S8[(2 + net) * EPI_TILE], delta = (double)o * K.ys[net] + K.ym[net];
           if (y >= 1e-30) {
             v[net] = inv_boxcox_dy10(y, delta, a.lambda);
@@ -468,13 +470,17 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, epi_min_ctas<NS>())
           }
         }
       }
+      if (c.o) {  // the raw net outputs (a diagnostic output), outside the net loop
+        float *op = c.o + i;
+#pragma unroll
+        for (int net = 0; net < NN; ++net, op += c.ld) *op = K.b4[net] + S4[net * EPI_TILE];
+      }
       double w[NE];
 #pragma unroll
       for (int e = 0; e < NE; ++e) {  // F dY
         w[e] = 0.0;
 #pragma unroll
-        for (int net = 0; net < CAP; ++net)
-          if (net < nn) w[e] = fma(K.F[e][net], v[net], w[e]);
+        for (int net = 0; net < NN; ++net) w[e] = fma(K.F[e][net], v[net], w[e]);
       }
 #pragma unroll
       for (int k = 0; k < CAP; ++k) {  // v = dY - E^T (F dY)
@@ -983,7 +989,7 @@ int launch_epilogue(const rc_mech *m, const rc_mlp *n, const EpiArgs &ea, const 
   // factored projection when net i predicts species i (checked at rc_mlp_create) and the element
   // count has an instance
   const bool ident = n->species_identity && ea.passes == 1 && m->uniform_tmid && n->inv_lambda == 10 &&
-                     n->n_nets <= EPI_KN;
+                     n->n_nets == m->ns - 1 && n->n_nets <= EPI_KN;
   if (m->ns == 9) return ident && m->ne == 3 ? launch_epilogue_t<9, 3>(m, n, ea, c, s) : launch_epilogue_t<9, 0>(m, n, ea, c, s);
   if (m->ns == 20) return ident && m->ne == 4 ? launch_epilogue_t<20, 4>(m, n, ea, c, s) : launch_epilogue_t<20, 0>(m, n, ea, c, s);
   return launch_epilogue_t<0, 0>(m, n, ea, c, s);
