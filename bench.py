@@ -404,7 +404,13 @@ def run_ours(a):
         # tensor peak of the MLP's own arithmetic: the measured bf16 figure x the guide's nominal ratio
         # (tf32 dense = 1/2 of bf16; tf32x3 spends three tf32 MMAs per useful product)
         tratio = {"bf16": 1.0, "tf32": 0.5, "tf32x3": 0.5 / 3}[a.precision]
-        tpeak = round(pk[SUSTAINED] * tratio, 1)
+        # the sustained peak was measured under the power cap (MEASURED_PEAKS clocks_under_load); a short
+        # run that holds a clock well above that one (no cap reached) is held to the burst peak instead
+        cs0 = clk.summary()
+        pmhz_s = (pk.get("clocks_under_load") or {}).get("sm_mhz_median")
+        burst = bool(cs0.get("sm_mhz") and pmhz_s and cs0["sm_mhz"] > 1.2 * pmhz_s and "bf16_tflops" in pk)
+        pkey = "bf16_tflops" if burst else SUSTAINED
+        tpeak = round(pk[pkey] * tratio, 1)
         kernels = {}
         for st_name, work, unit, bound, peak in [
             ("thermo", alg["thermo_bytes"], "GB/s", "hbm", pk["hbm_gbs"]),
@@ -470,15 +476,15 @@ def run_ours(a):
                                    if fused else f"L2 GEMM (h1 1600 -> h2 800, tcgen05 {a.precision})"), "bound": "tensor",
                         "achieved": l2.get("achieved"), "peak": tpeak, "unit": "TFLOP/s",
                         "frac": l2.get("frac"), "traffic": traffic,
-                        "peak_source": f"{pk_src} {SUSTAINED} (MEASURED_PEAKS.json)"
+                        "peak_source": f"{pk_src} {pkey} (MEASURED_PEAKS.json)"
                                        + ("" if a.precision == "bf16" else f" x {tratio:.3f} ({a.precision}, nominal ratio)"),
                         "work_per_launch": ("2*cells_chunk*(d_in*1600 + 1600*800)*nets FLOP" if fused
                                             else "2*cells_chunk*1600*800*nets FLOP")}
             # the step is power-capped: the SM clock it ran at against the one the sustained peak was
             # measured at (MEASURED_PEAKS clocks_under_load); frac x peak_mhz / sm_mhz is the fraction
             # per clock cycle
-            pmhz = (pk.get("clocks_under_load") or {}).get("sm_mhz_median")
-            cs = clk.summary()
+            pmhz = pk.get("sm_max_mhz") if burst else pmhz_s
+            cs = cs0
             if pmhz and cs.get("sm_mhz") and roofline.get("frac"):
                 roofline.update({"sm_mhz": cs["sm_mhz"], "peak_sm_mhz": pmhz,
                                  "frac_per_clock": round(roofline["frac"] * pmhz / cs["sm_mhz"], 4)})

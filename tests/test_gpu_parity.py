@@ -535,3 +535,22 @@ def test_cuda_graph_capture_with_layer3_overlap():
     out = st.host()
     for k in ("T", "cp", "rho", "mu", "lam", "D", "wdot", "qdot", "o", "red", "diag"):
         assert np.array_equal(out[k], ref[k]), k
+
+
+@pytest.mark.gpu
+def test_layer3_overlap_bitwise_equals_serial_ch4():
+    """The same for CH4 (19 nets, KZ = 32 fused kernel): a 100,000-cell call runs as two chunks with
+    the layer-3 side launch; bitwise equal to RC_MLP_SERIAL."""
+    import paper_2312_13513_b200 as rc
+    n = 100_000
+    c = inputs("C4", begin=3_000_000, end=3_000_000 + n)
+    G = Gpu("C4")
+    rc.rc_overlap_read(reset=True)
+    ov = G.run(c)
+    cnt = rc.rc_overlap_read(reset=True)
+    print(f"\n  CH4 overlap counters: {cnt}")
+    assert cnt["pairs_ran"] + cnt["pairs_gave_up"] > 0
+    G.mlp = rc.MLPBundle(G.mech, bundle("ch4_20sp", CONFIGS["C4"].hidden), 0, flags=rc.RC_MLP_SERIAL)
+    se = G.run(c)
+    for k in ("T", "cp", "rho", "mu", "lambda", "qdot", "D", "wdot", "o", "red", "diag"):
+        assert np.array_equal(ov[k], se[k]), k
