@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(epi_tile<NS>() + 32, epi_min_ctas<NS>())
   const int pnt = NE ? ((nn + ns) * NE + 1) & ~1 : nn * nse;
   int *sSpec = reinterpret_cast<int *>(sPn + pnt);
   double *sB4 = sPn + pnt + 16, *sYM = sB4 + nn, *sYS = sYM + nn;
-  const rcs::Ring<EPI_TILE> ring{reinterpret_cast<uint8_t *>(sPn + pnsz), bars + 1, 2 + ns, nn * a.passes, stages};
+  const rcs::Ring<EPI_TILE, epi_stages<NS>()> ring{reinterpret_cast<uint8_t *>(sPn + pnsz), bars + 1, 2 + ns, nn * a.passes, stages};
   if (threadIdx.x == 0) {
     rcx::mbar_init(&bars[0], 1);
     ring.init(EPI_TILE / 32);

@@ -23,9 +23,12 @@
 
 namespace rcs {
 
-template <int TILE>
+// STAGES > 0: the stage count as a compile-time constant (must equal `stages`); a power of two lets
+// the consumers derive stage and phase from the tile counter with a mask and a shift (one register)
+template <int TILE, int STAGES = 0>
 struct Ring {
   static_assert(TILE % 4 == 0, "16-byte aligned rows");
+  static constexpr bool POW2 = STAGES > 0 && (STAGES & (STAGES - 1)) == 0;
   uint8_t *buf;     // [stages][n8 x TILE x 8 B | n4 x TILE x 4 B]
   uint64_t *full;   // [stages] mbarriers, count 1
   int n8, n4, stages;
@@ -72,14 +75,17 @@ struct Ring {
         const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
         if (t < ntiles) issue(s, t, n, src8, src4);
       }
-    int it = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      const int s = it % stages;
-      rcx::mbar_wait(&full[s], (uint32_t)(it / stages) & 1u);
+    // stage index and phase carried incrementally (a runtime `it % stages` is an integer division
+    // per tile in every thread)
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      rcx::mbar_wait(&full[s], ph);
       body(s, t);
       __syncthreads();  // every thread has read stage s
       const int64_t tn = t + (int64_t)stages * gridDim.x;
       if (threadIdx.x == 0 && tn < ntiles) issue(s, tn, n, src8, src4);
+      if (++s == stages) { s = 0; ph ^= 1u; }
     }
   }
 
@@ -97,24 +103,33 @@ struct Ring {
     const int warp = threadIdx.x >> 5;
     if (warp == 0) {
       if ((threadIdx.x & 31) == 0) {
-        int it = 0;
-        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-          const int s = it % stages;
-          if (it >= stages) rcx::mbar_wait_sleep(&empty[s], (uint32_t)(it / stages - 1) & 1u);
+        int s = 0;
+        uint32_t ph = 1;  // the first pass over the stages waits for nothing
+        bool first = true;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+          if (!first) rcx::mbar_wait_sleep(&empty[s], ph);
           issue(s, t, n, src8, src4);
+          if (++s == stages) { s = 0; ph ^= 1u; first = false; }
         }
       }
       __syncwarp();
       return;
     }
     const int j = threadIdx.x - 32;
-    int it = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      const int s = it % stages;
-      rcx::mbar_wait(&full[s], (uint32_t)(it / stages) & 1u);
+    int s = 0, it = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      if constexpr (POW2) {
+        s = it & (STAGES - 1);
+        ph = (uint32_t)(it / STAGES) & 1u;
+        ++it;
+      }
+      rcx::mbar_wait(&full[s], ph);
       body(s, t, j);
       __syncwarp();
       if ((threadIdx.x & 31) == 0) rcx::mbar_arrive(&empty[s]);
+      if constexpr (!POW2)
+        if (++s == stages) { s = 0; ph ^= 1u; }
     }
   }
 
@@ -129,26 +144,29 @@ struct Ring {
     const int warp = threadIdx.x >> 5;
     if (warp == 0) {
       if ((threadIdx.x & 31) == 0) {
-        int it = 0;
-        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-          const int s = it % stages;
-          if (it >= stages) rcx::mbar_wait_sleep(&empty[s], (uint32_t)(it / stages - 1) & 1u);
+        int s = 0;
+        uint32_t ph = 1;  // the first pass over the stages waits for nothing
+        bool first = true;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+          if (!first) rcx::mbar_wait_sleep(&empty[s], ph);
           issue(s, t, n, src8, src4);
+          if (++s == stages) { s = 0; ph ^= 1u; first = false; }
         }
       }
       __syncwarp();
       return;
     }
     const int j = threadIdx.x - 32;
-    int it = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      const int s = it % stages;
-      rcx::mbar_wait(&full[s], (uint32_t)(it / stages) & 1u);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      rcx::mbar_wait(&full[s], ph);
       auto release = [&]() {
         __syncwarp();
         if ((threadIdx.x & 31) == 0) rcx::mbar_arrive(&empty[s]);
       };
       body(s, t, j, release);
+      if (++s == stages) { s = 0; ph ^= 1u; }
     }
   }
 };
