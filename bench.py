@@ -434,7 +434,7 @@ def run_ours(a):
                 # layer 3 overlapped with the fused kernel: the tiles the launches beside
                 # it ran (rc_overlap_read) are their work, the rest the main launches'; the side launches
                 # run on the SMs the fused kernel's clusters leave idle, their peak is that share of the GPU
-                l3_tiles = K * bundle["n_nets"] * (-(-n // 256)) if not bundle.get("shared") else 0
+                l3_tiles = K * (1 if bundle.get("shared") else bundle["n_nets"]) * (-(-n // 256))
                 ffrac = min(1.0, ovl["tiles_fill"] / l3_tiles) if l3_tiles else 0.0
                 work = work * (ffrac if st_name == "L3_fill" else 1.0 - ffrac)
                 if st_name == "L3_fill":

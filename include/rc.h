@@ -129,8 +129,8 @@ typedef struct {
                                      then one block W1 b1 W2 b2 W3 b3 W4[n_nets][h3] b4[n_nets] and
                                      output i predicts species_of_net[i].  RC_BF16 or RC_TF32 only;
                                      RC_MLP_SERIAL: run every MLP kernel on the caller's stream, in
-                                     chunk order.  By default, where the fused layer-1/2 kernel runs
-                                     (and the net is not shared), layer 3 of a chunk runs partly
+                                     chunk order.  By default, where the fused layer-1/2 kernel runs,
+                                     layer 3 of a chunk runs partly
                                      beside the fused kernel of the next chunk on the SMs that
                                      kernel's 4-CTA clusters leave idle, on a library-owned
                                      auxiliary stream (one per host thread and device) forked from

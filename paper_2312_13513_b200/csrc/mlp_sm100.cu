@@ -688,9 +688,10 @@ bool fused_path(const rc_mlp *n) {
          l12_supported(n->h1, n->h2, n->kpad1, n->precision == RC_TF32) && !(n->flags & RC_MLP_LAYERWISE);
 }
 // layer 3 of chunk j - 1 overlapped with the fused layer-1/2 kernel of chunk j: a
-// second h2 buffer and per-chunk tile counters; RC_MLP_SERIAL keeps the one-stream order
+// second h2 buffer and per-chunk tile counters; RC_MLP_SERIAL keeps the one-stream order.  The
+// shared net's layer 4 follows both layer-3 launches of its chunk on the caller's stream.
 bool overlap_path(const rc_mlp *n) {
-  return fused_path(n) && !(n->flags & (RC_MLP_SHARED | RC_MLP_SERIAL));
+  return fused_path(n) && !(n->flags & RC_MLP_SERIAL);
 }
 
 WsLayout ws_layout(const rc_mlp *n, int cap, int64_t ncells) {
@@ -1127,6 +1128,8 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   int fill_pairs = 0;
   L2Args pend{};
   bool have_pend = false;
+  float *pend_oc = nullptr;  // shared net: the pending chunk's raw-output rows and row count (layer 4)
+  int pend_rows = 0;
   int j = 0;
   for (int64_t c0 = 0; c0 < c.n; c0 += cap, ++j) {
     const int rows = (int)std::min<int64_t>(cap, c.n - c0);
@@ -1176,9 +1179,21 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
           RC_CUDA_TRY(cudaEventRecord(aux->fill[(j - 1) & 1], aux->s2));
         }
         if ((rc = launch_l2_pair(NP3, prec, mp3, pend, s))) return rc;
+        if (shared) {  // layer 4 of chunk j - 1 once h3 is complete (both layer-3 launches)
+          if (fill_pairs > 0) RC_CUDA_TRY(cudaStreamWaitEvent(s, aux->fill[(j - 1) & 1], 0));
+          if ((rc = launch_l4(n, w + L.h3, pend_oc, pend_rows, (int)zrows, tf32, s))) return rc;
+        }
       }
-      pend = L2Args{mt, n->h3 / NP3, nets, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, n->d_w4, oc, (int)zrows, (n->h2 % KC) / KATOM};
+      if (shared) {  // layer 3 as a plain GELU layer into h3 (one buffer: layer 4 of a chunk runs
+                     // before the next fused kernel, whose side launch writes h3 next)
+        pend = L2Args{mt, n->h3 / NP3, 1, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, nullptr, nullptr, cap, (n->h2 % KC) / KATOM};
+        pend.prof_stage = RC_STAGE_L3;
+      } else {
+        pend = L2Args{mt, n->h3 / NP3, nets, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, n->d_w4, oc, (int)zrows, (n->h2 % KC) / KATOM};
+      }
       pend.tile_ctr = sched + j;
+      pend_oc = oc;
+      pend_rows = rows;
       have_pend = true;
     } else if (!shared) {
       L2Args l3{mt, n->h3 / NP3, nets, (n->h2 + KC - 1) / KC, n->h3, 0, n->d_b3, n->d_w4, oc, (int)zrows, (n->h2 % KC) / KATOM};
@@ -1195,6 +1210,7 @@ int launch_chem(const rc_mech *m, const rc_mlp *n, const CellsDev &c, void *ws, 
   if (overlap) {  // the last chunk's layer 3 (nothing left to overlap it with), then join the fillers
     if ((rc = launch_l2_pair(NP3, prec, (j - 1) & 1 ? m3b : m3, pend, s))) return rc;
     if (fill_pairs > 0) RC_CUDA_TRY(cudaStreamWaitEvent(s, aux->fill[j & 1], 0));
+    if (shared && (rc = launch_l4(n, w + L.h3, pend_oc, pend_rows, (int)zrows, tf32, s))) return rc;
   }
   {  // a5 once over every cell of the call (one streaming pass, like the prologue)
     EpiArgs ea{0, (int)c.n, (int)zrows, nout, shared ? 1 : n->h3 / NP3, n->inv_lambda, n->ns, n->lambda_bc, 1.0 / n->dt,

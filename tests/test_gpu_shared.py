@@ -78,3 +78,23 @@ def test_shared_flag_rejects_tf32x3():
     with pytest.raises(rc.RcError) as e:
         rc.MLPBundle(M, b, rc.RC_TF32X3)
     assert e.value.code == rc._rc.RC_EUNSUPPORTED
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_shared_net_layer3_overlap_bitwise_equals_serial(prec):
+    """The shared net with the layer-3 overlap (layer 4 of a chunk after both of its
+    layer-3 launches): three chunks with a ragged last one give bitwise the RC_MLP_SERIAL result."""
+    import paper_2312_13513_b200 as rc
+    b = make_bundle("h2_9sp", shared=True)
+    n = 2 * 262144 + 30_000
+    c = inputs("C2", begin=0, end=n)
+    G = Gpu("C2", precision=prec, b=b)
+    rc.rc_overlap_read(reset=True)
+    ov = G.run(c)
+    cnt = rc.rc_overlap_read(reset=True)
+    print(f"\n  shared-net overlap counters (precision {prec}): {cnt}")
+    assert cnt["pairs_ran"] + cnt["pairs_gave_up"] > 0
+    G.mlp = rc.MLPBundle(G.mech, b, prec, flags=rc.RC_MLP_SERIAL)
+    se = G.run(c)
+    for k in ("T", "cp", "rho", "mu", "lambda", "qdot", "D", "wdot", "o", "red", "diag"):
+        assert np.array_equal(ov[k], se[k]), k
