@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--precision", default="bf16", choices=["bf16", "tf32", "tf32x3"])
     ap.add_argument("--strong", action="store_true", help="partition the config's cells (strong scaling)")
     ap.add_argument("--layerwise", action="store_true", help="rc_mlp_desc.flags = RC_MLP_LAYERWISE (comparison path)")
+    ap.add_argument("--e2e-batches", type=int, default=4,
+                    help="sub-batches of the e2e pipeline (copies of one overlap the compute of another)")
     ap.add_argument("--serial", action="store_true",
                     help="rc_mlp_desc.flags = RC_MLP_SERIAL: layer 3 not overlapped with the fused kernel (comparison)")
     ap.add_argument("--pasr", action="store_true", help="LES: PaSR scaling of wdot with per-cell tau_mix (NEXT-4)")
@@ -594,7 +596,7 @@ def run_e2e(a, rc, mech, mlp, bundle, host, st, ws, n, ns, world, stream):
     """
     import torch
     from paper_2312_13513_b200.dist import GlobalReductions
-    B = 4 if n % (4 * 128) == 0 else 1
+    B = a.e2e_batches if n % (a.e2e_batches * 128) == 0 else 1
     nb = n // B
     pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
     h_all = st.h[:n].cpu().numpy()
