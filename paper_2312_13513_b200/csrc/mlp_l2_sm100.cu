@@ -186,11 +186,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
   const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const uint32_t tqempty0 = rcx::map_cta(tqempty, 0);
   // reader side: the pair's it-th tile (>= total: none left); `warp_reader`: the whole warp reads,
-  // then one lane reports the slot read.  Rank 0's readers see their own CTA's writer (CTA-scope
-  // acquire, local arrive); rank 1's slot is written from rank 0 (cluster-scope acquire).  The
-  // read-done arrivals need no release: the slot is rewritten only TQD tiles later.
-  // rank 1's slot arrives by st.async with completion on its tqfull (no release fence in the leader's
-  // TMA thread: a cluster-scope release there waited for the thread's outstanding TMA loads)
+  // then one lane reports the slot read.  Rank 0's slot is written by its own TMA thread (ordinary
+  // arrive); rank 1's arrives by st.async with completion (4 tx bytes) on rank 1's tqfull, so an
+  // ordinary wait orders it and the leader's TMA thread issues no release fence (a cluster-scope
+  // release there waited for the thread's outstanding TMA loads: layer 3 lost 5%).  The read-done
+  // arrivals order nothing: a slot is rewritten only TQD tiles later.
   auto tq_take = [&](int it, bool warp_reader) -> int {
     const int d = it % TQD;
     rcx::mbar_wait(&tqfull[d], (uint32_t)(it / TQD) & 1);

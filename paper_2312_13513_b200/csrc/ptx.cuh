@@ -222,23 +222,6 @@ __device__ __forceinline__ void mma_commit_pair_mask(uint64_t *bar, uint16_t mas
 __device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
-// wait on a local mbarrier whose arrivals release data written by another CTA of the cluster
-// (acquire at cluster scope); traps after ~20 s like mbar_wait
-__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t *bar, uint32_t phase) {
-  const uint64_t t0 = global_ns();
-  for (;;) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-    if (ok) return;
-    if (global_ns() - t0 > 20000000000ull) __trap();
-  }
-}
 // asynchronous 4-byte store into another CTA's shared memory, completion (4 tx bytes) on an mbarrier
 // of that CTA: the consumer's ordinary wait orders it (no release fence in the storing thread)
 __device__ __forceinline__ void st_async_u32(uint32_t cluster_addr, uint32_t v, uint32_t bar_cluster) {
@@ -253,9 +236,6 @@ __device__ __forceinline__ void mbar_arrive_expect_tx_relaxed_cluster(uint32_t c
 }
 __device__ __forceinline__ void mbar_arrive_relaxed_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, uint32_t v) {
-  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
 }
 __device__ __forceinline__ int ld_shared_s32(const int *p) {
   int v;
