@@ -116,71 +116,85 @@ __global__ void __launch_bounds__(KIN_THREADS) kinetics_kernel(const double *__r
     release();
     if (!valid) return;
     const double lnp0RT = log(KIN_P0 / RC_RU) - lnT;
-    // net rate of progress of reaction r (reads only: two reactions are evaluated back to back so
-    // their exp chains overlap; the rate updates follow)
+    // Reactions in blocks of KB: the Arrhenius and equilibrium exponents of the block first, then
+    // their 2 KB exponentials as independent straight-line code (the exp chains overlap; one reaction
+    // at a time left the FP64 pipe waiting on each chain), then the per-reaction rest (third body,
+    // falloff, concentration products) and the rate updates.  k_r = k_f / K_c is formed as
+    // exp(ln k_f + sum nu g - dnu ln(p0/RT)) (one exponential instead of exp(ln k_f) exp(...)).
     // per-thread scratch columns: sC / sG / sR + q * KIN_TILE + j (q = species offset from IREC)
     const double *cC = sC + j, *cG = sG + j;
     double *cR = sR + j;
-    auto rate = [&](int r) -> double {
-      const double *R = REC + 48 * r;
-      const int *I = IREC + I_N * r;
-      const int type = I[I_TYPE];
-      const double lnk = R[R_LNA] + R[R_B] * lnT - R[R_ER] * invT;
-      double kf = exp(lnk), M = 0.0;
-      if (type >= 1)
-        for (int k = 0; k < ns; ++k) M = fma(EFF[r * nse + k], cC[k * KIN_TILE], M);
-      if (type == 2) {  // falloff: k = k_inf Pr / (1 + Pr) F
-        const double Pr = exp(R[R_LNA0] + R[R_B0] * lnT - R[R_ER0] * invT - lnk) * M;
-        double F = 1.0;
-        if (R[R_TA] >= 0.0) {  // Troe
-          const double a = R[R_TA];
-          const double Fc = (1.0 - a) * exp(-T * R[R_IT3]) + a * exp(-T * R[R_IT1]) + exp(-R[R_T2] * invT);
-          const double lF = log10(Fc), cc = -0.4 - 0.67 * lF, nn = 0.75 - 1.27 * lF;
-          const double lp = log10(Pr) + cc, x = lp / (nn - 0.14 * lp);
-          F = exp10(lF / (1.0 + x * x));
-        }
-        kf *= Pr / (1.0 + Pr) * F;
-      }
-      double fwd = kf, rev = 0.0;
+    constexpr int KB = 4;
+#pragma unroll 1
+    for (int r0 = 0; r0 < nr; r0 += KB) {
+      double ef[KB], er[KB];
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const int o = I[I_REAC + q];
-        if (o >= 0) fwd *= cC[o];
-      }
-      if (I[I_REV]) {  // k_r = k_f / K_c, K_c = exp(-sum nu g) (p0 / (R T))^(sum nu)
+      for (int q = 0; q < KB; ++q) {  // exponents (a reaction past nr: both exponentials 0)
+        const int r = r0 + q < nr ? r0 + q : nr - 1;
+        const double *R = REC + 48 * r;
+        const int *I = IREC + I_N * r;
+        const double lnk = R[R_LNA] + R[R_B] * lnT - R[R_ER] * invT;
         double sg = 0.0;
 #pragma unroll
-        for (int q = 0; q < 6; ++q) {
-          const int o = I[I_PSP + q];
-          if (o >= 0) sg = fma((double)I[I_PNU + q], cG[o], sg);
+        for (int u = 0; u < 6; ++u) {
+          const int o = I[I_PSP + u];
+          if (o >= 0) sg = fma((double)I[I_PNU + u], cG[o], sg);
         }
-        rev = kf * exp(sg - (double)I[I_DNU] * lnp0RT);
+        const bool live = r0 + q < nr;
+        ef[q] = live ? lnk : -INFINITY;
+        er[q] = live && I[I_REV] ? lnk + (sg - (double)I[I_DNU] * lnp0RT) : -INFINITY;
+      }
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          const int o = I[I_PROD + q];
+      for (int q = 0; q < KB; ++q) {
+        ef[q] = exp(ef[q]);
+        er[q] = exp(er[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < KB; ++q) {
+        const int r = r0 + q;
+        if (r >= nr) break;
+        const double *R = REC + 48 * r;
+        const int *I = IREC + I_N * r;
+        const int type = I[I_TYPE];
+        double fwd = ef[q], rev = er[q], M = 0.0;
+        if (type >= 1)
+          for (int k = 0; k < ns; ++k) M = fma(EFF[r * nse + k], cC[k * KIN_TILE], M);
+        if (type == 2) {  // falloff: k = k_inf Pr / (1 + Pr) F (the same factor on k_r = k_f / K_c)
+          const double lnk = R[R_LNA] + R[R_B] * lnT - R[R_ER] * invT;
+          const double Pr = exp(R[R_LNA0] + R[R_B0] * lnT - R[R_ER0] * invT - lnk) * M;
+          double F = 1.0;
+          if (R[R_TA] >= 0.0) {  // Troe
+            const double a = R[R_TA];
+            const double Fc = (1.0 - a) * exp(-T * R[R_IT3]) + a * exp(-T * R[R_IT1]) + exp(-R[R_T2] * invT);
+            const double lF = log10(Fc), cc = -0.4 - 0.67 * lF, nn = 0.75 - 1.27 * lF;
+            const double lp = log10(Pr) + cc, x = lp / (nn - 0.14 * lp);
+            F = exp10(lF / (1.0 + x * x));
+          }
+          const double fac = Pr / (1.0 + Pr) * F;
+          fwd *= fac;
+          rev *= fac;
+        }
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const int o = I[I_REAC + u];
+          if (o >= 0) fwd *= cC[o];
+        }
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const int o = I[I_PROD + u];
           if (o >= 0) rev *= cC[o];
         }
-      }
-      if (type == 1) {
-        fwd *= M;
-        rev *= M;
-      }
-      return fwd - rev;
-    };
-    auto update = [&](int r, double qn) {
-      const int *I = IREC + I_N * r;
+        if (type == 1) {
+          fwd *= M;
+          rev *= M;
+        }
+        const double qn = fwd - rev;
 #pragma unroll
-      for (int q = 0; q < 6; ++q) {
-        const int o = I[I_PSP + q];
-        if (o >= 0) cR[o] = fma((double)I[I_PNU + q], qn, cR[o]);
+        for (int u = 0; u < 6; ++u) {
+          const int o = I[I_PSP + u];
+          if (o >= 0) cR[o] = fma((double)I[I_PNU + u], qn, cR[o]);
+        }
       }
-    };
-#pragma unroll 1
-    for (int r = 0; r < nr; r += 2) {
-      const double q0 = rate(r);
-      const double q1 = r + 1 < nr ? rate(r + 1) : 0.0;
-      update(r, q0);
-      if (r + 1 < nr) update(r + 1, q1);
     }
     // wdot_k = W_k sum_r nu_rk q_r; LES: PaSR factor (rc.h tau_mix, R19); qdot
     double scale = 1.0;
