@@ -377,6 +377,12 @@ def run_ours(a):
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1) / a.steps
+    # the launches on one time axis (CUDA events on both streams): how long the layer-3 side launches
+    # ran while a fused L1+L2 launch was running
+    tl = rc.rc_profile_timeline() if hasattr(rc.lib(), "rc_profile_timeline") else []
+    l12_iv = [(t0, t1) for s_, t0, t1 in tl if s_ == "L12"]
+    fill_iv = [(t0, t1) for s_, t0, t1 in tl if s_ == "L3_fill"]
+    fill_conc = sum(max(0.0, min(b1, b2) - max(a1, a2)) for a1, b1 in fill_iv for a2, b2 in l12_iv)
     prof = rc.rc_profile_read(reset=True)
     ovl = rc.rc_overlap_read(reset=True) if hasattr(rc.lib(), "rc_overlap_read") else {}
     rc.rc_profile_enable(False)
@@ -453,6 +459,7 @@ def run_ours(a):
             v["share"] = round(v["ms_per_step"] / tot_k, 4) if tot_k and k != "L3_fill" else None
         if "L3_fill" in kernels:  # concurrent with L12 on the otherwise idle SMs: not on the step's critical path
             kernels["L3_fill"].update({"concurrent_with": "L12", "tiles_share": round(ffrac, 4),
+                                       "ms_per_step_during_L12": round(fill_conc / K, 4),
                                        "pairs_ran": ovl["pairs_ran"], "pairs_gave_up": ovl["pairs_gave_up"]})
         fused = "L12" in kernels
         l2 = kernels.get("L12" if fused else "L2", {})

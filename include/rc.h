@@ -304,6 +304,12 @@ enum {
 };
 int rc_profile_enable(int on);
 int rc_profile_read(double *ms /* [RC_STAGE_COUNT] */, int64_t *launches /* [RC_STAGE_COUNT] */, int reset);
+/* The recorded launches one by one, in record order (call before rc_profile_read resets them): stage[i]
+ * and the start / end of launch i in ms relative to the first recorded start (CUDA events, so
+ * launches on different streams share one time axis -- the layer-3 side launches next to the fused
+ * kernel show as intersecting intervals).  Fills at most `max` entries; returns the number recorded
+ * (>= 0) or an error status (RC_EINVAL: NULL arrays with max > 0; RC_ECUDA). */
+int rc_profile_timeline(int32_t *stage, double *t_start_ms, double *t_end_ms, int max);
 /* Layer-3 overlap counters since the last reset (process-global, current device; synchronous):
  * out[0] = layer-3 tiles (256 cells x one pass of one net) run by the launches beside the fused
  * kernel, out[1] = CTA pairs of those launches that found the fused kernel not yet resident after

@@ -14,14 +14,15 @@ from . import _rc
 from ._rc import (RC_BF16, RC_TF32, RC_TF32X3, RC_MODE_H, RC_MODE_T, DIAG_NAMES, Kinetics, Mechanism, MLPBundle, RcError,
                   lib, make_cells, rc_chem, rc_kinetics, rc_laplacian, rc_ldu_to_csr, rc_pack_planes, RC_LAP_GATHER,
                   RC_LAP_ATOMIC, rc_combine_reductions, rc_last_launch_count, rc_partition, rc_profile_enable, rc_profile_read, rc_step,
-                  rc_thermo, rc_transport, STAGES, RC_MLP_LAYERWISE, RC_MLP_SHARED, RC_MLP_SERIAL, rc_overlap_read)
+                  rc_thermo, rc_transport, STAGES, RC_MLP_LAYERWISE, RC_MLP_SHARED, RC_MLP_SERIAL, rc_overlap_read,
+                  rc_profile_timeline)
 
 __all__ = ["Mechanism", "MLPBundle", "Kinetics", "rc_kinetics", "rc_laplacian", "rc_ldu_to_csr", "rc_pack_planes",
            "RC_LAP_GATHER", "RC_LAP_ATOMIC", "CellState", "RcError", "RC_BF16", "RC_TF32", "RC_TF32X3", "RC_MODE_H", "RC_MODE_T",
            "rc_step", "rc_thermo", "rc_transport", "rc_chem", "rc_partition", "rc_combine_reductions",
            "rc_last_launch_count", "lib",
            "DIAG_NAMES", "make_cells", "rc_profile_enable", "rc_profile_read", "STAGES", "aligned_workspace",
-           "RC_MLP_LAYERWISE", "RC_MLP_SHARED", "RC_MLP_SERIAL", "rc_overlap_read"]
+           "RC_MLP_LAYERWISE", "RC_MLP_SHARED", "RC_MLP_SERIAL", "rc_overlap_read", "rc_profile_timeline"]
 
 
 class CellState:

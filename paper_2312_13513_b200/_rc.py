@@ -80,6 +80,7 @@ EXPORTS = {
     "rc_profile_enable": (C.c_int, [C.c_int]),
     "rc_profile_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "rc_overlap_read": (C.c_int, [C.c_void_p, C.c_int]),
+    "rc_profile_timeline": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "rc_last_error": (C.c_char_p, []),
     "rc_version": (C.c_char_p, []),
 }
@@ -294,3 +295,15 @@ def rc_overlap_read(reset=True):
     out = np.zeros(3, dtype=np.int64)
     check(lib().rc_overlap_read(out.ctypes.data, 1 if reset else 0))
     return {"tiles_fill": int(out[0]), "pairs_gave_up": int(out[1]), "pairs_ran": int(out[2])}
+
+
+def rc_profile_timeline(max_entries=100000):
+    """[(stage name, start_ms, end_ms)] of the recorded launches (before rc_profile_read resets them)."""
+    st = np.zeros(max_entries, dtype=np.int32)
+    t0 = np.zeros(max_entries, dtype=np.float64)
+    t1 = np.zeros(max_entries, dtype=np.float64)
+    n = lib().rc_profile_timeline(st.ctypes.data, t0.ctypes.data, t1.ctypes.data, max_entries)
+    if n < 0:
+        check(n)
+    n = min(n, max_entries)
+    return [(STAGES[s] if 0 <= s < len(STAGES) else str(s), float(a), float(b)) for s, a, b in zip(st[:n], t0[:n], t1[:n])]

@@ -131,6 +131,26 @@ extern "C" int rc_overlap_read(int64_t *out, int reset) {
   return RC_OK;
 }
 
+extern "C" int rc_profile_timeline(int32_t *stage, double *t0, double *t1, int max) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  if (max > 0 && (!stage || !t0 || !t1)) return rc_fail(RC_EINVAL, "rc_profile_timeline: NULL arrays");
+  if (g_prof.empty()) return 0;
+  for (auto &r : g_prof)
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return rc_fail(RC_ECUDA, "rc_profile_timeline: event sync failed");
+  const cudaEvent_t origin = g_prof.front().a;
+  const int n = (int)g_prof.size();
+  for (int i = 0; i < n && i < max; ++i) {
+    float a = 0.f, b = 0.f;
+    if (cudaEventElapsedTime(&a, origin, g_prof[i].a) != cudaSuccess ||
+        cudaEventElapsedTime(&b, origin, g_prof[i].b) != cudaSuccess)
+      return rc_fail(RC_ECUDA, "rc_profile_timeline: elapsed time");
+    stage[i] = g_prof[i].stage;
+    t0[i] = a;
+    t1[i] = b;
+  }
+  return n;
+}
+
 extern "C" const char *rc_last_error(void) { return g_err; }
 extern "C" const char *rc_version(void) { return "rc-b200 0.1 (sm_100a)"; }
 extern "C" int64_t rc_last_launch_count(void) { return g_launches; }

@@ -554,3 +554,31 @@ def test_layer3_overlap_bitwise_equals_serial_ch4():
     se = G.run(c)
     for k in ("T", "cp", "rho", "mu", "lambda", "qdot", "D", "wdot", "o", "red", "diag"):
         assert np.array_equal(ov[k], se[k]), k
+
+
+@pytest.mark.gpu
+def test_layer3_side_launches_run_concurrently_with_fused_kernel():
+    """The event timeline (rc_profile_timeline, one time axis for both streams) shows the layer-3 side
+    launches running while fused-kernel launches run: their intervals intersect."""
+    import paper_2312_13513_b200 as rc
+    n = 3 * 262144
+    c = inputs("C2", begin=0, end=n)
+    G = Gpu("C2")
+    G.run(c)  # warm the host-side caches
+    rc.rc_overlap_read(reset=True)
+    rc.rc_profile_enable(True)
+    rc.rc_profile_read(reset=True)
+    try:
+        G.run(c)
+        tl = rc.rc_profile_timeline()
+        rc.rc_profile_read(reset=True)
+    finally:
+        rc.rc_profile_enable(False)
+    cnt = rc.rc_overlap_read(reset=True)
+    l12 = [(a, b) for s, a, b in tl if s == "L12"]
+    fill = [(a, b) for s, a, b in tl if s == "L3_fill"]
+    assert len(l12) == 3 and len(fill) == 2, (len(l12), len(fill))
+    conc = sum(max(0.0, min(b1, b2) - max(a1, a2)) for a1, b1 in fill for a2, b2 in l12)
+    print(f"\n  side launches {sum(b - a for a, b in fill):.3f} ms, {conc:.3f} ms of it during the fused kernel; {cnt}")
+    if cnt["pairs_ran"] > 0:
+        assert conc > 0.5 * min(b - a for a, b in l12)
