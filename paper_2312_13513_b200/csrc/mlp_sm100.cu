@@ -757,17 +757,19 @@ int launch_combine_reductions(const double *rp, const int64_t *dp, int k, double
 // another): `go` marks the point where the fused kernel of chunk j is enqueued, fill[j % 2] the end of
 // chunk j's filler launch.
 struct AuxStreams {
-  int device = -1;
   cudaStream_t s2 = nullptr;
   cudaEvent_t go = nullptr, fill[2] = {nullptr, nullptr};
 };
+constexpr int AUX_MAX_DEVICES = 64;
+// one set per (host thread, device), created on first use and kept for the thread's lifetime (a
+// thread that alternates between devices reuses each device's set)
 AuxStreams *aux_streams() {
-  thread_local AuxStreams a;
+  thread_local AuxStreams per_dev[AUX_MAX_DEVICES];
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  if (a.device != dev) {  // (a thread that switches devices gets a new set; the old one is not reclaimed)
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= AUX_MAX_DEVICES) return nullptr;
+  AuxStreams &a = per_dev[dev];
+  if (!a.s2) {
     AuxStreams b;
-    b.device = dev;
     if (cudaStreamCreateWithFlags(&b.s2, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&b.go, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&b.fill[0], cudaEventDisableTiming) != cudaSuccess ||
