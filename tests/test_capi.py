@@ -86,3 +86,11 @@ def test_next_row_entry_points_reject_bad_arguments_before_any_cuda_call(rclib):
     # rc_kin_create with a NULL description
     h = C.c_void_p()
     assert L.rc_kin_create(None, None, C.byref(h)) == rclib.RC_EINVAL
+
+
+def test_profiling_entry_points_reject_null_output_before_any_cuda_call(rclib):
+    """rc_overlap_read and rc_profile_timeline check their output arrays first (CPU-safe)."""
+    L = rclib.lib()
+    assert L.rc_overlap_read(None, 0) == rclib.RC_EINVAL
+    assert L.rc_profile_timeline(None, None, None, 4) == rclib.RC_EINVAL
+    assert L.rc_profile_timeline(None, None, None, 0) == 0  # nothing recorded, nothing asked for
