@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--precision", default="bf16", choices=["bf16", "tf32", "tf32x3"])
     ap.add_argument("--strong", action="store_true", help="partition the config's cells (strong scaling)")
     ap.add_argument("--layerwise", action="store_true", help="rc_mlp_desc.flags = RC_MLP_LAYERWISE (comparison path)")
-    ap.add_argument("--e2e-batches", type=int, default=4,
+    ap.add_argument("--e2e-batches", type=int, default=1,
                     help="sub-batches of the e2e pipeline (copies of one overlap the compute of another)")
     ap.add_argument("--serial", action="store_true",
                     help="rc_mlp_desc.flags = RC_MLP_SERIAL: layer 3 not overlapped with the fused kernel (comparison)")
@@ -596,10 +596,11 @@ def tf32_variant(a, rc, mech, bundle, cells, st, T_guess, n, stream):
 def run_e2e(a, rc, mech, mlp, bundle, host, st, ws, n, ns, world, stream):
     """Same metric, timed from pinned host inputs to host outputs through the C ABI.
 
-    The step is run as B sub-batches with their own device cell states: the host->device
-    copy of batch b+1 and the device->host copy of batch b-1 run on two copy streams
-    while batch b computes (rc_step), and rc_combine_reductions forms the step's a6
-    values from the per-batch reductions (then the NCCL allreduce across ranks).
+    Two device cell states alternate between steps (each split into B sub-batches, default one):
+    the host->device copy of step k+1's inputs and the device->host copy of step k-1's outputs run
+    on two copy streams while step k computes (rc_step on the caller's stream), and
+    rc_combine_reductions forms each step's a6 values from the per-batch reductions (then the NCCL
+    allreduce across ranks).  Every step copies its own inputs in and its outputs out.
     """
     import torch
     from paper_2312_13513_b200.dist import GlobalReductions
@@ -607,55 +608,62 @@ def run_e2e(a, rc, mech, mlp, bundle, host, st, ws, n, ns, world, stream):
     nb = n // B
     pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
     h_all = st.h[:n].cpu().numpy()
-    batches = []
-    for b in range(B):
+    hin_all, hout_all = [], []
+    for b in range(B):  # host buffers, shared by the two device sets (copies of one stream are ordered)
         sl = slice(b * nb, (b + 1) * nb)
-        sb = rc.CellState(nb, ns, mlp.n_nets, outputs=("cp", "rho", "mu", "lam", "D", "wdot", "qdot"))
-        hin = {"h": pin(h_all[sl]), "T": pin(host["T_guess"][sl]), "p": pin(host["p"][sl]),
-               "Y": pin(host["Y"][:, sl])}
-        hout = {k: torch.empty((nb,) if k not in ("D", "wdot") else (ns, nb), dtype=torch.float64).pin_memory()
-                for k in ("T", "cp", "rho", "mu", "lam", "D", "wdot", "qdot")}
-        batches.append((sb, hin, hout))
-    red_parts = torch.zeros(B, 2, dtype=torch.float64, device="cuda")
-    diag_parts = torch.zeros(B, 5, dtype=torch.int64, device="cuda")
+        hin_all.append({"h": pin(h_all[sl]), "T": pin(host["T_guess"][sl]), "p": pin(host["p"][sl]),
+                        "Y": pin(host["Y"][:, sl])})
+        hout_all.append({k: torch.empty((nb,) if k not in ("D", "wdot") else (ns, nb), dtype=torch.float64).pin_memory()
+                         for k in ("T", "cp", "rho", "mu", "lam", "D", "wdot", "qdot")})
+    sets = []  # [parity] -> (batches, cells, red_parts, diag_parts)
+    for _ in range(2):
+        batches = [(rc.CellState(nb, ns, mlp.n_nets, outputs=("cp", "rho", "mu", "lam", "D", "wdot", "qdot")),
+                    hin_all[b], hout_all[b]) for b in range(B)]
+        red_parts = torch.zeros(B, 2, dtype=torch.float64, device="cuda")
+        diag_parts = torch.zeros(B, 5, dtype=torch.int64, device="cuda")
+        cells = []
+        for b, (sb, _, _) in enumerate(batches):
+            c = sb.cells(rc.RC_MODE_H, dt=bundle["dt"])
+            c.red, c.diag = red_parts[b].data_ptr(), diag_parts[b].data_ptr()
+            cells.append(c)
+        sets.append((batches, cells, red_parts, diag_parts))
     red = torch.zeros(2, dtype=torch.float64, device="cuda")
     diag = torch.zeros(5, dtype=torch.int64, device="cuda")
-    cells = []
-    for b, (sb, _, _) in enumerate(batches):
-        c = sb.cells(rc.RC_MODE_H, dt=bundle["dt"])
-        c.red, c.diag = red_parts[b].data_ptr(), diag_parts[b].data_ptr()
-        cells.append(c)
     reduce_a6 = GlobalReductions("cuda")
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    in_done = [torch.cuda.Event() for _ in range(B)]
-    cmp_done = [torch.cuda.Event() for _ in range(B)]
-    out_done = [torch.cuda.Event() for _ in range(B)]
-    for e in cmp_done + out_done:
+    in_done = [[torch.cuda.Event() for _ in range(B)] for _ in range(2)]
+    cmp_done = [[torch.cuda.Event() for _ in range(B)] for _ in range(2)]
+    out_done = [[torch.cuda.Event() for _ in range(B)] for _ in range(2)]
+    for e in [e for ev in cmp_done + out_done for e in ev]:
         e.record(stream)
-    h2d = sum(t.numel() for _, hin, _ in batches for t in hin.values()) * 8
-    d2h = sum(t.numel() for _, _, hout in batches for t in hout.values()) * 8
+    h2d = sum(t.numel() for hin in hin_all for t in hin.values()) * 8
+    d2h = sum(t.numel() for hout in hout_all for t in hout.values()) * 8
+    k_step = [0]
 
     def step():
+        par = k_step[0] & 1
+        k_step[0] += 1
+        batches, cells, red_parts, diag_parts = sets[par]
         for b, (sb, hin, hout) in enumerate(batches):
-            # batch b's buffers are reused: the previous step's compute has read its inputs AND the
-            # previous D2H has read its outputs (T included) before the H2D / compute rewrite them;
-            # compute waits on in_done[b], which is recorded after this wait, so it is ordered too
-            s_in.wait_event(out_done[b])
+            # this set's buffers were last used two steps ago: its compute has read the inputs and its
+            # D2H has read the outputs (T included) before the H2D / compute rewrite them; compute
+            # waits on in_done, which is recorded after this wait, so it is ordered too
+            s_in.wait_event(out_done[par][b])
             with torch.cuda.stream(s_in):
                 sb.h[:nb].copy_(hin["h"], non_blocking=True)
                 sb.T[:nb].copy_(hin["T"], non_blocking=True)
                 sb.p[:nb].copy_(hin["p"], non_blocking=True)
                 sb.Y[:, :nb].copy_(hin["Y"], non_blocking=True)
-                in_done[b].record(s_in)
-            stream.wait_event(in_done[b])
+                in_done[par][b].record(s_in)
+            stream.wait_event(in_done[par][b])
             rc.rc_step(mech, mlp, cells[b], ws, stream)
-            cmp_done[b].record(stream)
-            s_out.wait_event(cmp_done[b])
+            cmp_done[par][b].record(stream)
+            s_out.wait_event(cmp_done[par][b])
             with torch.cuda.stream(s_out):
                 for k, v in hout.items():
                     src = getattr(sb, k)
                     v.copy_(src[:nb] if src.dim() == 1 else src[:, :nb], non_blocking=True)
-                out_done[b].record(s_out)
+                out_done[par][b].record(s_out)
         rc.rc_combine_reductions(red_parts, diag_parts, red, diag, stream)
         reduce_a6(red, diag)
 
@@ -680,8 +688,8 @@ def run_e2e(a, rc, mech, mlp, bundle, host, st, ws, n, ns, world, stream):
     val = n * world / (t.item() * 1e-3) / 1e6
     return {"value": round(val, 4), "unit": "Mcells/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": round(t.item(), 4),
-            "api": f"rc_step (C ABI) on {B} sub-batches, pinned host buffers, H2D/D2H on copy streams overlapping compute, "
-                   f"rc_combine_reductions + NCCL for a6"}
+            "api": f"rc_step (C ABI) on two alternating device states ({B} sub-batch(es) each), pinned host buffers, "
+                   f"H2D of step k+1 / D2H of step k-1 on copy streams overlapping step k, rc_combine_reductions + NCCL for a6"}
 
 
 def oracle_time(cfg, bundle, mech_d, idx, chem="dnn"):
